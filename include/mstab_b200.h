@@ -1,0 +1,204 @@
+/*
+ * mstab_b200.h — C-ABI drop-in boundary for the M(s,l)stab / IDR(s)stab(l) solve loop.
+ *
+ * Plain C: opaque handles, plain pointers and sizes, no torch or C++ types.
+ * Every entry point below replaces one piece of the reference's proj/core interface;
+ * the citation after each declaration names the reference symbol (file:line under
+ * /root/reference/proj/core) whose behaviour it keeps.
+ *
+ * Two libraries export exactly this ABI:
+ *   - paper_1604_06043_b200/libmstab_b200.so : the B200 product (sm_100a kernels, device-resident state);
+ *   - oracle/_ref/libmstab_ref.so            : the unmodified reference compiled from its own sources
+ *                                              (test/bench baseline only, see oracle/Makefile).
+ * so a caller (tests, bench.py, a cgo/ctypes binding) can switch implementations by library path.
+ *
+ * Data model: real fp64 values (the reference stores complex<double>; every real input keeps
+ * a zero imaginary part bit-for-bit through the solve), int64 CSR indices at
+ * the boundary (the reference uses size_t), column-major N x s blocks (dense.hpp:23-24).
+ *
+ * Errors: every function returns 0 on success or a negative MSTAB_E_* code that maps 1:1 to the
+ * exception class the reference would throw (errors.hpp:9-72). mstab_last_error() returns the
+ * message of the last failure on the calling thread. Breakdowns inside a solve are NOT errors:
+ * like the reference (idrstab.cpp:290-293) they end the solve with status MSTAB_STATUS_BREAKDOWN.
+ *
+ * Threading: one in-flight call per context; operators and recycle handles are immutable after
+ * creation and may be shared read-only (operator.hpp:12-14, recycle.hpp:14-17).
+ */
+#ifndef MSTAB_B200_H
+#define MSTAB_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes (errors.hpp:9-72) ------------------------------------------------------- */
+#define MSTAB_OK 0
+#define MSTAB_E_ERROR (-1)         /* mstab::Error (non-finite input, zero start vector, csr validate) */
+#define MSTAB_E_DIMENSION (-2)     /* mstab::DimensionMismatch */
+#define MSTAB_E_CONFIG (-3)        /* mstab::ConfigError */
+#define MSTAB_E_FINGERPRINT (-4)   /* mstab::FingerprintMismatch */
+#define MSTAB_E_STALE (-5)         /* mstab::StaleData */
+#define MSTAB_E_PARSE (-6)         /* mstab::ParseError */
+#define MSTAB_E_IO (-7)            /* mstab::IoError */
+#define MSTAB_E_SINGULAR (-8)      /* mstab::SingularProjection (only from the kernel helpers) */
+#define MSTAB_E_RANK (-9)          /* mstab::RankDeficient (only from the kernel helpers) */
+#define MSTAB_E_CUDA (-20)         /* device/runtime failure (no reference counterpart) */
+#define MSTAB_E_NOTREAL (-21)      /* complex data rejected: this build is the real fp64 path */
+
+/* ---- memory spaces for pointer arguments --------------------------------------------------- */
+#define MSTAB_MEM_HOST 0
+#define MSTAB_MEM_DEVICE 1
+
+/* ---- status (report.hpp:12) ---------------------------------------------------------------- */
+#define MSTAB_STATUS_CONVERGED 0
+#define MSTAB_STATUS_MAXMV 1
+#define MSTAB_STATUS_BREAKDOWN 2
+
+/* ---- fetch policy kinds (recycle.hpp:31-42) ------------------------------------------------ */
+#define MSTAB_FETCH_AT_CYCLE 0
+#define MSTAB_FETCH_AT_HALF_TOLERANCE 1
+#define MSTAB_FETCH_MANUAL 2
+
+typedef struct mstab_context mstab_context;
+typedef struct mstab_operator mstab_operator;
+typedef struct mstab_recycle mstab_recycle;
+typedef struct mstab_result mstab_result;
+
+/* SolverConfig (report.hpp:24-33; validated as report.cpp:16-22) */
+typedef struct mstab_solver_config {
+  int64_t s;
+  int64_t ell;
+  double tol;
+  int64_t max_mv;
+  int32_t true_residual_each_cycle;
+  int32_t _pad;
+  uint64_t seed;
+} mstab_solver_config;
+
+/* FetchPolicy (recycle.hpp:31-42) */
+typedef struct mstab_fetch_policy {
+  int32_t kind;
+  int32_t _pad;
+  int64_t cycle;
+} mstab_fetch_policy;
+
+/* HistoryPoint (report.hpp:16-22) */
+typedef struct mstab_history_point {
+  int64_t cycle;
+  int64_t mv;
+  int64_t level;
+  double resnorm;
+  int64_t wall_ns;
+} mstab_history_point;
+
+/* SolveReport scalars (report.hpp:35-58); histories come from the accessors below */
+typedef struct mstab_report {
+  int64_t h_mv;
+  int64_t h_mv_aux;
+  int64_t h_rd;
+  int64_t cycles;
+  int32_t status;
+  int32_t has_fetched;       /* SolveResult::fetched has a value (idrstab.hpp:76) */
+  double bnorm;
+  double final_resnorm;
+  int64_t wall_ns_total;
+  int64_t history_len;       /* residual_history.size() */
+  int64_t tau_len;           /* total tau coefficients over all cycles (cycles * ell) */
+  int64_t ell;
+  char breakdown_reason[128];
+} mstab_report;
+
+/* RecycleData header fields (recycle.hpp:18-29) */
+typedef struct mstab_recycle_info {
+  int64_t n;
+  int64_t s;
+  int64_t level_j;
+  int64_t omega_count;
+  uint64_t fingerprint;
+} mstab_recycle_info;
+
+/* ValidationReport (recycle.hpp:44-48) */
+typedef struct mstab_validation_report {
+  double max_deviation;
+  double sigma_min_ratio;
+  int32_t low_rank_warning;
+  int32_t _pad;
+} mstab_validation_report;
+
+/* ---- library / context -------------------------------------------------------------------- */
+const char* mstab_last_error(void);
+const char* mstab_impl_name(void); /* "b200" or "reference" */
+
+/* Binds a device and creates the solver's CUDA stream. device < 0 selects the current device. */
+int mstab_context_create(int32_t device, mstab_context** out);
+void mstab_context_destroy(mstab_context* ctx);
+/* Blocks until all work queued on the context's stream is complete. */
+int mstab_context_synchronize(mstab_context* ctx);
+/* The CUDA stream (cudaStream_t) the context launches on, as an opaque pointer (NULL on host impls). */
+void* mstab_context_stream(mstab_context* ctx);
+
+/* ---- operator (operator.hpp:15-50, csr.hpp:17-52) ----------------------------------------- */
+/* Builds a CsrOperator from host CSR arrays: validates like CsrMatrix::validate (csr.cpp:11-24),
+ * requires a square matrix (operator.cpp:21-23), computes the reference FNV-1a fingerprint
+ * once (csr.cpp:28-43 over the size_t/complex<double> byte layout) and uploads the matrix. */
+int mstab_operator_create_csr(mstab_context* ctx, int64_t n, const int64_t* row_ptr,
+                              const int64_t* col_idx, const double* values, mstab_operator** out);
+void mstab_operator_destroy(mstab_operator* op);
+int64_t mstab_operator_size(const mstab_operator* op);        /* LinearOperator::size (operator.hpp:21) */
+int64_t mstab_operator_nnz(const mstab_operator* op);
+uint64_t mstab_operator_fingerprint(const mstab_operator* op); /* operator.cpp:35 */
+/* y = A x (CsrOperator::apply, operator.cpp:25-28 -> spmv csr.cpp:103-113). */
+int mstab_operator_apply(mstab_context* ctx, const mstab_operator* op, const double* x, double* y,
+                         int32_t mem);
+
+/* ---- recycle data (recycle.hpp:18-64) ----------------------------------------------------- */
+/* fetch(): deep copy of column-major P, U, V (N x s) plus omega history (re,im pairs),
+ * level J and the operator fingerprint (recycle.cpp:26-38). */
+int mstab_recycle_create(mstab_context* ctx, int64_t n, int64_t s, const double* p, const double* u,
+                         const double* v, int32_t mem, const double* omega_re_im,
+                         int64_t omega_count, int64_t level_j, uint64_t fingerprint,
+                         mstab_recycle** out);
+void mstab_recycle_destroy(mstab_recycle* rd);
+int mstab_recycle_info_get(const mstab_recycle* rd, mstab_recycle_info* out);
+/* Copies P, U, V (each N x s column-major; any may be NULL) and omega (re,im pairs; may be NULL). */
+int mstab_recycle_download(mstab_context* ctx, const mstab_recycle* rd, double* p, double* u,
+                           double* v, double* omega_re_im);
+/* validate() (recycle.cpp:40-83): FingerprintMismatch / DimensionMismatch / StaleData. */
+int mstab_recycle_validate(mstab_context* ctx, const mstab_recycle* rd, const mstab_operator* op,
+                           mstab_validation_report* out);
+/* save()/load() of the bit-exact .mrd file (recycle.cpp:85-192). */
+int mstab_recycle_save(mstab_context* ctx, const mstab_recycle* rd, const char* path);
+int mstab_recycle_load(mstab_context* ctx, const char* path, mstab_recycle** out);
+
+/* ---- the solve loop (idrstab.hpp:88-96, idrstab.cpp:193-307) ------------------------------ */
+/* idrstab_solve / mstab_solve. b and x0 (NULL = empty guess) live in `mem`. recycle == NULL runs
+ * the fresh branch (make_cut_space + arnoldi_init); otherwise the recycled branch (validate,
+ * then continue in the donor's M-spaces). fetch may be NULL. Returns 0 when the solve ran
+ * (status in the report, breakdown included) or a negative error code for the exceptions the
+ * reference lets escape (ConfigError, DimensionMismatch, Error, FingerprintMismatch, StaleData). */
+int mstab_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
+                int32_t mem, const mstab_solver_config* cfg, const mstab_recycle* recycle,
+                const mstab_fetch_policy* fetch, mstab_result** out);
+void mstab_result_destroy(mstab_result* res);
+int mstab_result_report(const mstab_result* res, mstab_report* out);
+/* SolveResult::x, copied into x (N values in `mem`). */
+int mstab_result_x(mstab_context* ctx, const mstab_result* res, double* x, int32_t mem);
+/* residual_history: copies min(cap, history_len) points; returns the number copied (<0 on error). */
+int64_t mstab_result_history(const mstab_result* res, mstab_history_point* out, int64_t cap);
+/* omega_history (report.hpp:38-39): tau per cycle, flattened cycle-major, (re,im) pairs.
+ * Copies min(cap, tau_len) coefficients; returns the number copied. */
+int64_t mstab_result_taus(const mstab_result* res, double* re_im, int64_t cap);
+/* New handles on the result's RecycleData: final_data, fetched (MSTAB_E_ERROR if none), and
+ * handoff() = fetched if present else final_data (idrstab.hpp:80). Handles share the immutable
+ * device buffers with the result; destroy each one independently. */
+int mstab_result_final_data(const mstab_result* res, mstab_recycle** out);
+int mstab_result_fetched(const mstab_result* res, mstab_recycle** out);
+int mstab_result_handoff(const mstab_result* res, mstab_recycle** out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MSTAB_B200_H */

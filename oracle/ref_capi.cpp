@@ -1,0 +1,345 @@
+// ref_capi.cpp — TEST INFRASTRUCTURE ONLY. The C-ABI of include/mstab_b200.h implemented over
+// the unmodified reference library (mstab:: from /root/reference/proj/core), so tests and the
+// bench's reference arm drive the reference through exactly the boundary the B200 library
+// exports. Host memory only (MSTAB_MEM_DEVICE -> MSTAB_E_CONFIG). Built by oracle/Makefile.
+#include <complex>
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <random>
+#include <string>
+
+#include "mstab/csr.hpp"
+#include "mstab/errors.hpp"
+#include "mstab/kernels.hpp"
+#include "mstab/operator.hpp"
+#include "mstab/recycle.hpp"
+#include "mstab/solvers/baselines.hpp"
+#include "mstab/solvers/idrstab.hpp"
+#include "mstab_b200.h"
+#include "mstab_b200_kernels.h"
+
+using mstab::Complex;
+
+struct mstab_context {
+  int device = -1;
+};
+struct mstab_operator {
+  mstab::CsrMatrix m;
+  std::unique_ptr<mstab::CsrOperator> op;
+  uint64_t fp = 0;
+};
+struct mstab_recycle {
+  std::shared_ptr<const mstab::RecycleData> d;
+};
+struct mstab_result {
+  mstab::SolveResult r;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+struct ConfigErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MSTAB_OK;
+  } catch (const mstab::FingerprintMismatch& e) {
+    g_err = e.what();
+    return MSTAB_E_FINGERPRINT;
+  } catch (const mstab::StaleData& e) {
+    g_err = e.what();
+    return MSTAB_E_STALE;
+  } catch (const mstab::DimensionMismatch& e) {
+    g_err = e.what();
+    return MSTAB_E_DIMENSION;
+  } catch (const mstab::ConfigError& e) {
+    g_err = e.what();
+    return MSTAB_E_CONFIG;
+  } catch (const mstab::ParseError& e) {
+    g_err = e.what();
+    return MSTAB_E_PARSE;
+  } catch (const mstab::IoError& e) {
+    g_err = e.what();
+    return MSTAB_E_IO;
+  } catch (const mstab::SingularProjection& e) {
+    g_err = e.what();
+    return MSTAB_E_SINGULAR;
+  } catch (const mstab::RankDeficient& e) {
+    g_err = e.what();
+    return MSTAB_E_RANK;
+  } catch (const mstab::Error& e) {
+    g_err = e.what();
+    return MSTAB_E_ERROR;
+  } catch (const ConfigErr& e) {
+    g_err = e.what();
+    return MSTAB_E_CONFIG;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MSTAB_E_ERROR;
+  }
+}
+
+void host_only(int32_t mem) {
+  if (mem != MSTAB_MEM_HOST) throw ConfigErr("reference implementation: host memory only");
+}
+
+mstab::Vector to_vec(const double* x, int64_t n) {
+  mstab::Vector v((size_t)n);
+  for (int64_t i = 0; i < n; ++i) v[(size_t)i] = Complex(x[i], 0.0);
+  return v;
+}
+
+mstab::DenseMatrix to_dense(const double* a, int64_t n, int64_t s) {
+  mstab::DenseMatrix m((size_t)n, (size_t)s);
+  for (int64_t j = 0; j < s; ++j)
+    for (int64_t i = 0; i < n; ++i) m((size_t)i, (size_t)j) = Complex(a[i + j * n], 0.0);
+  return m;
+}
+
+void from_dense(const mstab::DenseMatrix& m, double* out) {
+  if (!out) return;
+  for (size_t j = 0; j < m.cols(); ++j)
+    for (size_t i = 0; i < m.rows(); ++i) out[i + j * m.rows()] = m(i, j).real();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mstab_last_error(void) { return g_err.c_str(); }
+const char* mstab_impl_name(void) { return "reference"; }
+
+int mstab_context_create(int32_t device, mstab_context** out) {
+  return guarded([&] {
+    *out = new mstab_context();
+    (*out)->device = device;
+  });
+}
+void mstab_context_destroy(mstab_context* ctx) { delete ctx; }
+int mstab_context_synchronize(mstab_context*) { return MSTAB_OK; }
+void* mstab_context_stream(mstab_context*) { return nullptr; }
+
+int mstab_operator_create_csr(mstab_context*, int64_t n, const int64_t* row_ptr,
+                              const int64_t* col_idx, const double* values, mstab_operator** out) {
+  return guarded([&] {
+    auto o = std::make_unique<mstab_operator>();
+    o->m.n_rows = o->m.n_cols = (size_t)n;
+    const int64_t nnz = row_ptr[n];
+    o->m.row_ptr.assign(row_ptr, row_ptr + n + 1);
+    o->m.col_idx.assign(col_idx, col_idx + nnz);
+    o->m.values.resize((size_t)nnz);
+    for (int64_t k = 0; k < nnz; ++k) o->m.values[(size_t)k] = Complex(values[k], 0.0);
+    o->m.validate();
+    o->op = std::make_unique<mstab::CsrOperator>(o->m);
+    o->fp = o->op->fingerprint();
+    *out = o.release();
+  });
+}
+void mstab_operator_destroy(mstab_operator* op) { delete op; }
+int64_t mstab_operator_size(const mstab_operator* op) { return (int64_t)op->m.n_rows; }
+int64_t mstab_operator_nnz(const mstab_operator* op) { return (int64_t)op->m.nnz(); }
+uint64_t mstab_operator_fingerprint(const mstab_operator* op) { return op->fp; }
+
+int mstab_operator_apply(mstab_context*, const mstab_operator* op, const double* x, double* y,
+                         int32_t mem) {
+  return guarded([&] {
+    host_only(mem);
+    const int64_t n = (int64_t)op->m.n_rows;
+    mstab::Vector out = op->op->apply(to_vec(x, n));
+    for (int64_t i = 0; i < n; ++i) y[i] = out[(size_t)i].real();
+  });
+}
+
+int mstab_recycle_create(mstab_context*, int64_t n, int64_t s, const double* p, const double* u,
+                         const double* v, int32_t mem, const double* omega_re_im,
+                         int64_t omega_count, int64_t level_j, uint64_t fingerprint,
+                         mstab_recycle** out) {
+  return guarded([&] {
+    host_only(mem);
+    std::vector<Complex> om;
+    for (int64_t i = 0; i < omega_count; ++i) om.emplace_back(omega_re_im[2 * i], omega_re_im[2 * i + 1]);
+    auto d = std::make_shared<mstab::RecycleData>(mstab::fetch(to_dense(p, n, s), to_dense(u, n, s),
+                                                               to_dense(v, n, s), om, (size_t)level_j,
+                                                               fingerprint));
+    *out = new mstab_recycle{d};
+  });
+}
+void mstab_recycle_destroy(mstab_recycle* rd) { delete rd; }
+
+int mstab_recycle_info_get(const mstab_recycle* rd, mstab_recycle_info* out) {
+  return guarded([&] {
+    out->n = (int64_t)rd->d->p.rows();
+    out->s = (int64_t)rd->d->s;
+    out->level_j = (int64_t)rd->d->level_J;
+    out->omega_count = (int64_t)rd->d->omega_history.size();
+    out->fingerprint = rd->d->matrix_fingerprint;
+  });
+}
+
+int mstab_recycle_download(mstab_context*, const mstab_recycle* rd, double* p, double* u,
+                           double* v, double* omega_re_im) {
+  return guarded([&] {
+    from_dense(rd->d->p, p);
+    from_dense(rd->d->u, u);
+    from_dense(rd->d->v, v);
+    if (omega_re_im)
+      for (size_t i = 0; i < rd->d->omega_history.size(); ++i) {
+        omega_re_im[2 * i] = rd->d->omega_history[i].real();
+        omega_re_im[2 * i + 1] = rd->d->omega_history[i].imag();
+      }
+  });
+}
+
+int mstab_recycle_validate(mstab_context*, const mstab_recycle* rd, const mstab_operator* op,
+                           mstab_validation_report* out) {
+  return guarded([&] {
+    mstab::ValidationReport r = mstab::validate(*rd->d, *op->op);
+    if (out) {
+      out->max_deviation = r.max_deviation;
+      out->sigma_min_ratio = r.sigma_min_ratio;
+      out->low_rank_warning = r.low_rank_warning ? 1 : 0;
+    }
+  });
+}
+
+int mstab_recycle_save(mstab_context*, const mstab_recycle* rd, const char* path) {
+  return guarded([&] { mstab::save(*rd->d, path); });
+}
+
+int mstab_recycle_load(mstab_context*, const char* path, mstab_recycle** out) {
+  return guarded([&] {
+    auto d = std::make_shared<mstab::RecycleData>(mstab::load(path));
+    *out = new mstab_recycle{d};
+  });
+}
+
+int mstab_solve(mstab_context*, const mstab_operator* op, const double* b, const double* x0,
+                int32_t mem, const mstab_solver_config* cfg, const mstab_recycle* recycle,
+                const mstab_fetch_policy* fetch, mstab_result** out) {
+  return guarded([&] {
+    host_only(mem);
+    const int64_t n = (int64_t)op->m.n_rows;
+    mstab::SolverConfig sc{(size_t)cfg->s, (size_t)cfg->ell, cfg->tol, cfg->max_mv,
+                           cfg->true_residual_each_cycle != 0, cfg->seed};
+    std::optional<mstab::FetchPolicy> fp;
+    if (fetch) {
+      if (fetch->kind == MSTAB_FETCH_AT_CYCLE) fp = mstab::FetchPolicy::at_cycle((size_t)fetch->cycle);
+      else if (fetch->kind == MSTAB_FETCH_AT_HALF_TOLERANCE) fp = mstab::FetchPolicy::at_half_tolerance();
+      else fp = mstab::FetchPolicy::manual();
+    }
+    mstab::Vector bv = to_vec(b, n);
+    mstab::Vector xv = x0 ? to_vec(x0, n) : mstab::Vector{};
+    auto r = std::make_unique<mstab_result>();
+    r->r = mstab::idrstab_solve(*op->op, bv, xv, sc, recycle ? recycle->d.get() : nullptr,
+                                fp ? &*fp : nullptr);
+    *out = r.release();
+  });
+}
+
+void mstab_result_destroy(mstab_result* res) { delete res; }
+
+int mstab_result_report(const mstab_result* res, mstab_report* out) {
+  return guarded([&] {
+    const mstab::SolveReport& rep = res->r.report;
+    std::memset(out, 0, sizeof(*out));
+    out->h_mv = rep.h_mv;
+    out->h_mv_aux = rep.h_mv_aux;
+    out->h_rd = rep.h_rd;
+    out->cycles = (int64_t)rep.cycles;
+    out->status = rep.status == mstab::SolveStatus::Converged ? MSTAB_STATUS_CONVERGED
+                  : rep.status == mstab::SolveStatus::MaxMV   ? MSTAB_STATUS_MAXMV
+                                                              : MSTAB_STATUS_BREAKDOWN;
+    out->has_fetched = res->r.fetched ? 1 : 0;
+    out->bnorm = rep.bnorm;
+    out->final_resnorm = rep.final_resnorm;
+    out->wall_ns_total = rep.wall_ns_total;
+    out->history_len = (int64_t)rep.residual_history.size();
+    int64_t taus = 0;
+    for (const auto& t : rep.omega_history) taus += (int64_t)t.size();
+    out->tau_len = taus;
+    out->ell = rep.omega_history.empty() ? 0 : (int64_t)rep.omega_history.front().size();
+    std::snprintf(out->breakdown_reason, sizeof(out->breakdown_reason), "%s", rep.breakdown_reason.c_str());
+  });
+}
+
+int mstab_result_x(mstab_context*, const mstab_result* res, double* x, int32_t mem) {
+  return guarded([&] {
+    host_only(mem);
+    for (size_t i = 0; i < res->r.x.size(); ++i) x[i] = res->r.x[i].real();
+  });
+}
+
+int64_t mstab_result_history(const mstab_result* res, mstab_history_point* out, int64_t cap) {
+  const auto& h = res->r.report.residual_history;
+  int64_t cnt = std::min<int64_t>(cap, (int64_t)h.size());
+  for (int64_t i = 0; i < cnt; ++i)
+    out[i] = {(int64_t)h[i].cycle, h[i].mv, (int64_t)h[i].level, h[i].resnorm, h[i].wall_ns};
+  return cnt;
+}
+
+int64_t mstab_result_taus(const mstab_result* res, double* re_im, int64_t cap) {
+  int64_t k = 0;
+  for (const auto& t : res->r.report.omega_history)
+    for (const Complex& z : t) {
+      if (k >= cap) return k;
+      re_im[2 * k] = z.real();
+      re_im[2 * k + 1] = z.imag();
+      ++k;
+    }
+  return k;
+}
+
+int mstab_result_final_data(const mstab_result* res, mstab_recycle** out) {
+  return guarded([&] { *out = new mstab_recycle{std::make_shared<mstab::RecycleData>(res->r.final_data)}; });
+}
+
+int mstab_result_fetched(const mstab_result* res, mstab_recycle** out) {
+  return guarded([&] {
+    if (!res->r.fetched) throw mstab::Error("no fetched recycle data");
+    *out = new mstab_recycle{std::make_shared<mstab::RecycleData>(*res->r.fetched)};
+  });
+}
+
+int mstab_result_handoff(const mstab_result* res, mstab_recycle** out) {
+  return guarded([&] { *out = new mstab_recycle{std::make_shared<mstab::RecycleData>(res->r.handoff())}; });
+}
+
+// ---- kernel-level helpers -----------------------------------------------------------------
+int mstab_kernel_solve_small(mstab_context*, int64_t s, const double* m, const double* rhs, double* x) {
+  return guarded([&] {
+    mstab::Vector out = mstab::solve_small(to_dense(m, s, s), to_vec(rhs, s));
+    for (int64_t i = 0; i < s; ++i) x[i] = out[(size_t)i].real();
+  });
+}
+
+int mstab_kernel_least_squares(mstab_context*, int64_t n, int64_t ell, const double* z,
+                               const double* r, double* tau) {
+  return guarded([&] {
+    mstab::Vector t = mstab::least_squares_tall(to_dense(z, n, ell), to_vec(r, n));
+    for (int64_t i = 0; i < ell; ++i) tau[i] = t[(size_t)i].real();
+  });
+}
+
+int mstab_kernel_cut_space(mstab_context*, int64_t n, int64_t s, uint64_t seed, double* p) {
+  return guarded([&] { from_dense(mstab::make_cut_space((size_t)n, (size_t)s, seed, true), p); });
+}
+
+int mstab_kernel_arnoldi(mstab_context*, const mstab_operator* op, const double* r0, int64_t s,
+                         uint64_t rng_seed, double* u, double* v, int64_t* mv_cost) {
+  return guarded([&] {
+    std::mt19937_64 rng(rng_seed);
+    mstab::Vector r = to_vec(r0, (int64_t)op->m.n_rows);
+    mstab::ArnoldiResult ar = mstab::arnoldi_init(*op->op, r, (size_t)s, rng);
+    from_dense(ar.u, u);
+    from_dense(ar.v, v);
+    if (mv_cost) *mv_cost = ar.mv_cost;
+  });
+}
+
+}  // extern "C"

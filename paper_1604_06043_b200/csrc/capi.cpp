@@ -1,0 +1,387 @@
+// capi.cpp — extern "C" entry points of include/mstab_b200.h over solver.cpp.
+// Exceptions never cross the boundary: each call returns the MSTAB_E_* code of the reference
+// exception class (errors.hpp) and leaves the message in mstab_last_error().
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "solver.h"
+
+using namespace mstab_b200;
+
+struct mstab_context {
+  std::unique_ptr<Context> impl;
+};
+struct mstab_operator {
+  std::shared_ptr<Operator> impl;
+};
+struct mstab_recycle {
+  RecyclePtr impl;
+};
+struct mstab_result {
+  std::unique_ptr<SolveResultImpl> impl;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MSTAB_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return MSTAB_E_ERROR;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return MSTAB_E_ERROR;
+  }
+}
+
+void bind(mstab_context* ctx) {
+  if (!ctx || !ctx->impl) throw Error(MSTAB_E_CONFIG, "null context");
+  cudaSetDevice(ctx->impl->device);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mstab_last_error(void) { return g_last_error.c_str(); }
+const char* mstab_impl_name(void) { return "b200"; }
+
+int mstab_context_create(int32_t device, mstab_context** out) {
+  return guarded([&] {
+    auto c = std::make_unique<mstab_context>();
+    c->impl = std::make_unique<Context>(device);
+    *out = c.release();
+  });
+}
+
+void mstab_context_destroy(mstab_context* ctx) { delete ctx; }
+
+int mstab_context_synchronize(mstab_context* ctx) {
+  return guarded([&] {
+    bind(ctx);
+    ctx->impl->sync();
+  });
+}
+
+void* mstab_context_stream(mstab_context* ctx) {
+  return ctx && ctx->impl ? static_cast<void*>(ctx->impl->stream()) : nullptr;
+}
+
+int mstab_operator_create_csr(mstab_context* ctx, int64_t n, const int64_t* row_ptr,
+                              const int64_t* col_idx, const double* values, mstab_operator** out) {
+  return guarded([&] {
+    bind(ctx);
+    auto o = std::make_unique<mstab_operator>();
+    o->impl = make_operator(*ctx->impl, n, row_ptr, col_idx, values);
+    *out = o.release();
+  });
+}
+
+void mstab_operator_destroy(mstab_operator* op) { delete op; }
+int64_t mstab_operator_size(const mstab_operator* op) { return op->impl->n; }
+int64_t mstab_operator_nnz(const mstab_operator* op) { return op->impl->nnz; }
+uint64_t mstab_operator_fingerprint(const mstab_operator* op) { return op->impl->fingerprint; }
+
+int mstab_operator_apply(mstab_context* ctx, const mstab_operator* op, const double* x, double* y,
+                         int32_t mem) {
+  return guarded([&] {
+    bind(ctx);
+    Context& c = *ctx->impl;
+    const int64_t n = op->impl->n;
+    if (mem == MSTAB_MEM_DEVICE) {
+      spmv(c, *op->impl, x, y);
+      c.sync();
+      return;
+    }
+    DevPtr dx = c.alloc_vecs(n, 1), dy = c.alloc_vecs(n, 1);
+    if (cudaMemcpyAsync(dx->ptr, x, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream()) != cudaSuccess)
+      throw Error(MSTAB_E_CUDA, "upload x");
+    spmv(c, *op->impl, dx->d(), dy->d());
+    if (cudaMemcpyAsync(y, dy->ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream()) != cudaSuccess)
+      throw Error(MSTAB_E_CUDA, "download y");
+    c.sync();
+  });
+}
+
+int mstab_recycle_create(mstab_context* ctx, int64_t n, int64_t s, const double* p, const double* u,
+                         const double* v, int32_t mem, const double* omega_re_im,
+                         int64_t omega_count, int64_t level_j, uint64_t fingerprint,
+                         mstab_recycle** out) {
+  return guarded([&] {
+    bind(ctx);
+    Context& c = *ctx->impl;
+    if (n < 1 || s < 1) throw Error(MSTAB_E_DIMENSION, "recycle data has inconsistent shapes");
+    auto r = std::make_shared<Recycle>();
+    r->n = n;
+    r->s = s;
+    r->level_j = level_j;
+    r->fingerprint = fingerprint;
+    const int64_t ld = padded_ld(n);
+    const auto kind = mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    auto up = [&](const double* src) {
+      DevPtr d = c.alloc_vecs(n, s);
+      if (cudaMemcpy2DAsync(d->ptr, sizeof(double) * ld, src, sizeof(double) * n, sizeof(double) * n, s,
+                            kind, c.stream()) != cudaSuccess)
+        throw Error(MSTAB_E_CUDA, "recycle upload");
+      return d;
+    };
+    r->p = up(p);
+    r->u = up(u);
+    r->v = up(v);
+    for (int64_t i = 0; i < omega_count; ++i)
+      r->omega.emplace_back(omega_re_im[2 * i], omega_re_im[2 * i + 1]);
+    c.sync();
+    auto h = std::make_unique<mstab_recycle>();
+    h->impl = r;
+    *out = h.release();
+  });
+}
+
+void mstab_recycle_destroy(mstab_recycle* rd) { delete rd; }
+
+int mstab_recycle_info_get(const mstab_recycle* rd, mstab_recycle_info* out) {
+  return guarded([&] {
+    out->n = rd->impl->n;
+    out->s = rd->impl->s;
+    out->level_j = rd->impl->level_j;
+    out->omega_count = (int64_t)rd->impl->omega.size();
+    out->fingerprint = rd->impl->fingerprint;
+  });
+}
+
+int mstab_recycle_download(mstab_context* ctx, const mstab_recycle* rd, double* p, double* u,
+                           double* v, double* omega_re_im) {
+  return guarded([&] {
+    bind(ctx);
+    Context& c = *ctx->impl;
+    const Recycle& r = *rd->impl;
+    const int64_t ld = padded_ld(r.n);
+    auto down = [&](const DevPtr& src, double* dst) {
+      if (!dst) return;
+      if (cudaMemcpy2DAsync(dst, sizeof(double) * r.n, src->ptr, sizeof(double) * ld, sizeof(double) * r.n,
+                            r.s, cudaMemcpyDeviceToHost, c.stream()) != cudaSuccess)
+        throw Error(MSTAB_E_CUDA, "recycle download");
+    };
+    down(r.p, p);
+    down(r.u, u);
+    down(r.v, v);
+    if (omega_re_im)
+      for (size_t i = 0; i < r.omega.size(); ++i) {
+        omega_re_im[2 * i] = r.omega[i].real();
+        omega_re_im[2 * i + 1] = r.omega[i].imag();
+      }
+    c.sync();
+  });
+}
+
+int mstab_recycle_validate(mstab_context* ctx, const mstab_recycle* rd, const mstab_operator* op,
+                           mstab_validation_report* out) {
+  return guarded([&] {
+    bind(ctx);
+    mstab_validation_report r = validate(*ctx->impl, *rd->impl, *op->impl);
+    if (out) *out = r;
+  });
+}
+
+int mstab_recycle_save(mstab_context* ctx, const mstab_recycle* rd, const char* path) {
+  return guarded([&] {
+    bind(ctx);
+    const Recycle& r = *rd->impl;
+    MrdData d;
+    d.n = r.n;
+    d.s = r.s;
+    d.level_j = r.level_j;
+    d.fingerprint = r.fingerprint;
+    d.p.resize((size_t)r.n * r.s);
+    d.u.resize(d.p.size());
+    d.v.resize(d.p.size());
+    d.omega = r.omega;
+    int rc = mstab_recycle_download(ctx, rd, d.p.data(), d.u.data(), d.v.data(), nullptr);
+    if (rc != MSTAB_OK) throw Error(rc, g_last_error);
+    mrd_write(path, d);
+  });
+}
+
+int mstab_recycle_load(mstab_context* ctx, const char* path, mstab_recycle** out) {
+  return guarded([&] {
+    bind(ctx);
+    MrdData d = mrd_read(path);
+    std::vector<double> om(2 * d.omega.size());
+    for (size_t i = 0; i < d.omega.size(); ++i) {
+      om[2 * i] = d.omega[i].real();
+      om[2 * i + 1] = d.omega[i].imag();
+    }
+    int rc = mstab_recycle_create(ctx, d.n, d.s, d.p.data(), d.u.data(), d.v.data(), MSTAB_MEM_HOST,
+                                  om.data(), (int64_t)d.omega.size(), d.level_j, d.fingerprint, out);
+    if (rc != MSTAB_OK) throw Error(rc, g_last_error);
+  });
+}
+
+int mstab_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
+                int32_t mem, const mstab_solver_config* cfg, const mstab_recycle* recycle,
+                const mstab_fetch_policy* fetch, mstab_result** out) {
+  return guarded([&] {
+    bind(ctx);
+    auto r = std::make_unique<mstab_result>();
+    r->impl = solve(*ctx->impl, *op->impl, b, x0, mem, *cfg, recycle ? recycle->impl.get() : nullptr,
+                    fetch);
+    *out = r.release();
+  });
+}
+
+void mstab_result_destroy(mstab_result* res) { delete res; }
+
+int mstab_result_report(const mstab_result* res, mstab_report* out) {
+  return guarded([&] { *out = res->impl->report; });
+}
+
+int mstab_result_x(mstab_context* ctx, const mstab_result* res, double* x, int32_t mem) {
+  return guarded([&] {
+    bind(ctx);
+    Context& c = *ctx->impl;
+    if (cudaMemcpyAsync(x, res->impl->x->ptr, sizeof(double) * res->impl->n,
+                        mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                        c.stream()) != cudaSuccess)
+      throw Error(MSTAB_E_CUDA, "download x");
+    c.sync();
+  });
+}
+
+int64_t mstab_result_history(const mstab_result* res, mstab_history_point* out, int64_t cap) {
+  const auto& h = res->impl->history;
+  const int64_t cnt = std::min<int64_t>(cap, (int64_t)h.size());
+  if (cnt > 0) std::memcpy(out, h.data(), sizeof(mstab_history_point) * cnt);
+  return cnt;
+}
+
+int64_t mstab_result_taus(const mstab_result* res, double* re_im, int64_t cap) {
+  const auto& t = res->impl->taus;
+  const int64_t cnt = std::min<int64_t>(cap, (int64_t)t.size());
+  for (int64_t i = 0; i < cnt; ++i) {
+    re_im[2 * i] = t[i];
+    re_im[2 * i + 1] = 0.0;
+  }
+  return cnt;
+}
+
+int mstab_result_final_data(const mstab_result* res, mstab_recycle** out) {
+  return guarded([&] {
+    auto h = std::make_unique<mstab_recycle>();
+    h->impl = res->impl->final_data;
+    *out = h.release();
+  });
+}
+
+int mstab_result_fetched(const mstab_result* res, mstab_recycle** out) {
+  return guarded([&] {
+    if (!res->impl->fetched) throw Error(MSTAB_E_ERROR, "no fetched recycle data");
+    auto h = std::make_unique<mstab_recycle>();
+    h->impl = res->impl->fetched;
+    *out = h.release();
+  });
+}
+
+int mstab_result_handoff(const mstab_result* res, mstab_recycle** out) {
+  return guarded([&] {
+    auto h = std::make_unique<mstab_recycle>();
+    h->impl = res->impl->fetched ? res->impl->fetched : res->impl->final_data;
+    *out = h.release();
+  });
+}
+
+}  // extern "C"
+
+// ---- kernel-level entry points (include/mstab_b200_kernels.h) -------------------------------
+#include "../../include/mstab_b200_kernels.h"
+
+extern "C" {
+
+int mstab_kernel_solve_small(mstab_context* ctx, int64_t s, const double* m, const double* rhs,
+                             double* x) {
+  return guarded([&] {
+    bind(ctx);
+    Context& c = *ctx->impl;
+    if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: solve_small supports 1 <= s <= 16");
+    DevPtr buf = c.alloc(sizeof(double) * (size_t)(s * s + 2 * s + 1));
+    double* dm = buf->d();
+    double* drhs = dm + s * s;
+    double* dx = drhs + s;
+    int32_t* dok = reinterpret_cast<int32_t*>(dx + s);
+    cudaMemcpyAsync(dm, m, sizeof(double) * s * s, cudaMemcpyHostToDevice, c.stream());
+    cudaMemcpyAsync(drhs, rhs, sizeof(double) * s, cudaMemcpyHostToDevice, c.stream());
+    launch_small_solve(c.stream(), (int)s, dm, drhs, dx, dok);
+    int32_t ok = 0;
+    cudaMemcpyAsync(x, dx, sizeof(double) * s, cudaMemcpyDeviceToHost, c.stream());
+    cudaMemcpyAsync(&ok, dok, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream());
+    c.sync();
+    if (!ok) throw Error(MSTAB_E_SINGULAR, "solve_small: pivot collapse");
+  });
+}
+
+int mstab_kernel_least_squares(mstab_context* ctx, int64_t n, int64_t ell, const double* z,
+                               const double* r, double* tau) {
+  return guarded([&] {
+    bind(ctx);
+    Context& c = *ctx->impl;
+    if (ell < 1 || n < ell) throw Error(MSTAB_E_DIMENSION, "least_squares_tall: need N >= ell >= 1");
+    if (ell > kMaxEll) throw Error(MSTAB_E_CONFIG, "b200: least squares supports ell <= 8");
+    const int64_t ld = padded_ld(n);
+    DevPtr zr = c.alloc_vecs(n, ell + 1);
+    cudaMemcpyAsync(zr->d(), r, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream());
+    cudaMemcpy2DAsync(zr->d() + ld, sizeof(double) * ld, z, sizeof(double) * n, sizeof(double) * n, ell,
+                      cudaMemcpyHostToDevice, c.stream());
+    const double* cols[kMaxEll + 1];
+    for (int64_t i = 0; i <= ell; ++i) cols[i] = zr->d() + i * ld;
+    reset_status(c);
+    launch_ls(c.stream(), n, ld, (int)ell, 1, cols, c.reducer());
+    const CycleStatus& st = read_status(c);
+    if (st.breakdown == kBreakRank) throw Error(MSTAB_E_RANK, "least_squares_tall: stabilization block lost rank");
+    const double* h = read_scal(c, 32 + (int)ell);
+    for (int64_t i = 0; i < ell; ++i) tau[i] = h[32 + i];
+  });
+}
+
+int mstab_kernel_cut_space(mstab_context* ctx, int64_t n, int64_t s, uint64_t seed, double* p) {
+  return guarded([&] {
+    bind(ctx);
+    Context& c = *ctx->impl;
+    if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: 1 <= s <= 16");
+    DevPtr P = make_cut_space(c, n, (int)s, seed);
+    cudaMemcpy2DAsync(p, sizeof(double) * n, P->ptr, sizeof(double) * padded_ld(n), sizeof(double) * n, s,
+                      cudaMemcpyDeviceToHost, c.stream());
+    c.sync();
+  });
+}
+
+int mstab_kernel_arnoldi(mstab_context* ctx, const mstab_operator* op, const double* r0, int64_t s,
+                         uint64_t rng_seed, double* u, double* v, int64_t* mv_cost) {
+  return guarded([&] {
+    bind(ctx);
+    Context& c = *ctx->impl;
+    if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: 1 <= s <= 16");
+    const int64_t n = op->impl->n, ld = padded_ld(n);
+    DevPtr r = c.alloc_vecs(n, 1), U = c.alloc_vecs(n, s), V = c.alloc_vecs(n, s);
+    cudaMemcpyAsync(r->ptr, r0, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream());
+    reset_status(c);
+    arnoldi_init(c, *op->impl, r->d(), (int)s, rng_seed, U->d(), V->d());
+    cudaMemcpy2DAsync(u, sizeof(double) * n, U->ptr, sizeof(double) * ld, sizeof(double) * n, s,
+                      cudaMemcpyDeviceToHost, c.stream());
+    cudaMemcpy2DAsync(v, sizeof(double) * n, V->ptr, sizeof(double) * ld, sizeof(double) * n, s,
+                      cudaMemcpyDeviceToHost, c.stream());
+    c.sync();
+    if (mv_cost) *mv_cost = s;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,46 @@
+// device_state.h — POD structures shared by the sm_100a kernels (kernels.cu) and the host
+// orchestration (solver.cpp). No CUDA headers here so g++ can include it.
+//
+// Layout conventions:
+//   * every N-vector / block column is fp64 with column stride `ld` (N rounded up to 64);
+//   * an N x s block is s consecutive columns (column-major, like DenseMatrix, dense.hpp:23-24);
+//   * CSR is int32 row_ptr / col_idx + fp64 values (all BASELINE configs have nnz < 2^31).
+#pragma once
+#include <cstdint>
+
+namespace mstab_b200 {
+
+constexpr int kMaxS = 16;    // s in {1..16} (BASELINE c5 sweep tops at 16)
+constexpr int kMaxEll = 8;   // ell in {1..8}
+constexpr int kBlock = 256;  // threads per CTA for every streaming kernel
+constexpr int kMaxGrid = 148 * 8;
+
+// Breakdown codes written by the device finalizers (idrstab.cpp:290-293 reasons).
+enum : int32_t { kBreakNone = 0, kBreakSingular = 1, kBreakRank = 2 };
+
+// Small, per-solve scalar state living in device memory. The "status" head is copied back to
+// the host once per cycle (one small D2H); the rest stays on the device.
+struct CycleStatus {
+  double resnorm;          // ||r|| after the cycle (norm2, types.cpp:9-13)
+  double tau[kMaxEll];     // stabilisation coefficients of the cycle (after the tail guard)
+  int32_t breakdown;       // kBreak*
+  int32_t mv_at_breakdown; // operator applications done in the cycle before the failing solve
+  int32_t tail_perturbed;  // PolyOut::tail_perturbed (idrstab.cpp:165-174)
+  int32_t pending_singular;// gamma_0 for the NEXT cycle came out singular (raised when it starts)
+};
+
+struct DevState {
+  CycleStatus st;
+  double Ma[kMaxS * kMaxS];    // P^H V^(k), column-major s x s (ld = s)
+  double Mn[kMaxS * kMaxS];    // P^H V^(k+1), filled column by column during step (c)
+  double g[kMaxS];             // P^H r^(k)
+  double rhs[kMaxS];           // P^H r^(k+1)
+  double gamma[kMaxEll * kMaxS];  // BiCG coefficients per level k (bicg_projection), row k
+  double eta[kMaxS * kMaxS];   // eta_q of the current level, row q = eta for column q
+  double scal[64];             // misc reduced scalars (norms, dots for init/validate)
+  double gram[2 * kMaxS * kMaxS];  // validate: P^H P then V^H V
+  uint32_t ticket;             // last-CTA-done counter (reset by the finaliser)
+  uint32_t _pad;
+};
+
+}  // namespace mstab_b200

@@ -1,0 +1,120 @@
+// kernels.h — host-callable launchers for the sm_100a kernels in kernels.cu.
+//
+// Every launcher enqueues on `stream` and never synchronises. Reductions are deterministic:
+// per-CTA partials in a fixed order, then the last CTA to finish (ticket counter) reduces all
+// partials in a fixed order and runs the small dense step that follows (LU solve, LS solve),
+// so no extra kernel and no host round trip sits between a reduction and its consumer.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "device_state.h"
+
+typedef struct CUstream_st* cudaStream_t;
+
+namespace mstab_b200 {
+
+struct DevCsr {
+  int64_t n = 0;
+  int64_t nnz = 0;
+  const int32_t* row_ptr = nullptr;  // n + 1
+  const int32_t* col_idx = nullptr;  // nnz (+ padding)
+  const double* values = nullptr;    // nnz (+ padding)
+};
+
+// Reduction workspace: `partials` holds at least kMaxGrid * max_slots doubles.
+struct Reducer {
+  double* partials = nullptr;
+  DevState* ds = nullptr;
+};
+
+// What the last CTA does with the reduced vector of an SpMV (see kernels.cu, finalize_spmv).
+enum FinOp : int32_t {
+  kFinStore = 0,    // copy the reduced values to `dst`
+  kFinRhsEta0 = 1,  // level k step (b): rhs := P^H r^(k+1); eta_0 := solve(Ma, rhs)
+  kFinColEta = 2,   // level k column q: Mn[:,q] := P^H V^(k+1)_q; eta_{q+1} or gamma_{k+1}
+  kFinTrueRes = 3,  // true residual refresh: resnorm, g := P^H r, pending gamma_0
+};
+
+struct FinParams {
+  int32_t op = kFinStore;
+  int32_t s = 0;
+  int32_t k = 0;    // level
+  int32_t q = 0;    // column
+  int32_t ell = 0;
+  int32_t _pad = 0;
+  double* dst = nullptr;
+};
+
+// Occupancy-derived persistent grid size for the streaming kernels (multiple of the SM count).
+int grid_for(int64_t n);
+void kernels_init(int device);
+
+// ---- the Mstab cycle ----------------------------------------------------------------------
+// y = A x, fused partial dots P^H y (s of them) and the finaliser `fin`. When `b` != nullptr the
+// kernel instead writes y = b - A x and also reduces ||y||^2 (true residual refresh).
+void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
+                    int64_t ld, int s, const double* b, const FinParams& fin, const Reducer& red);
+
+// step (a), top level only: r_out = r_in - V^(k) gamma (gemv + subtract, idrstab.cpp:113-117).
+// At k == 0 the kernel first raises a pending singular gamma_0 as a breakdown.
+void launch_level_update(cudaStream_t st, int64_t n, int64_t ld, int s, int k, const double* r_in,
+                         double* r_out, const double* vk, DevState* ds);
+
+// step (c), top level, column q: V^(k)_q = r^(k+1) - sum_c eta_qc * mixed_c (idrstab.cpp:140-148)
+void launch_rebuild_top(cudaStream_t st, int64_t n, int64_t ld, int s, int q, const double* rnext,
+                        const double* vk_in, double* vk_out, const double* vk1, DevState* ds);
+
+// Deferred lower-level pass of level k: the (a) updates of r^(0..k-1) and x, then the rebuild of
+// V^(-1..k-1) for every column, top-down, in one HBM pass. lv_in/lv_out index level+1 (0..k+1).
+void launch_rebuild_deferred(cudaStream_t st, int64_t n, int64_t ld, int s, int k,
+                             const double* const* lv_in, double* const* lv_out,
+                             const double* const* r_in, double* const* r_out, const double* x_in,
+                             double* x_out, DevState* ds);
+
+// least_squares_tall(Z=[r^(1)..r^(ell)], r^(0)) by one-pass Givens TSQR + tail guard.
+void launch_ls(cudaStream_t st, int64_t n, int64_t ld, int ell, int s, const double* const* r,
+               const Reducer& red);
+
+// poly_combination + fused ||r||^2, P^H r, P^H V and the pending gamma_0 solve.
+void launch_poly(cudaStream_t st, int64_t n, int64_t ld, int s, int ell, const double* const* lv,
+                 double* u_out, double* v_out, const double* const* r, double* r_out,
+                 const double* x_in, double* x_out, const double* p, const Reducer& red);
+
+// Start of a solve: Ma := P^H V, g := P^H r, pending gamma_0 := solve(Ma, g).
+void launch_prologue(cudaStream_t st, int64_t n, int64_t ld, int s, const double* p,
+                     const double* v, const double* r, const Reducer& red);
+
+// ---- validate (recycle.cpp:40-83): ||V - A U||^2, ||V||^2 per column, P^H P, V^H V ----------
+// Results land in ds->scal[0..1] (dev_num, dev_den) and ds->gram (P^H P then V^H V).
+void launch_validate(cudaStream_t st, const DevCsr& a, const double* p, const double* u,
+                     const double* v, int64_t ld, int s, const Reducer& red);
+
+// ---- generic helpers (initialisation paths; not per-cycle) --------------------------------
+// dst[j] = dot(A_j, y) for j < na (A_j = a + j*ld); dst[na] = ||y||^2 when with_norm.
+void launch_dots(cudaStream_t st, int64_t n, int64_t ld, const double* a, int na, const double* y,
+                 bool with_norm, double* dst, const Reducer& red);
+// y += (-coef[j]) * A_j for j = 0..na-1 in order (axpy(-c, a_j, y), types.cpp:21-23)
+void launch_axpy_neg(cudaStream_t st, int64_t n, int64_t ld, const double* a, int na,
+                     const double* coef, double* y);
+// y = x / sqrt(*d2)   (u0 = r0 / ||r0||, idrstab.cpp:57-58 and :83-84)
+void launch_div_by_sqrt(cudaStream_t st, int64_t n, const double* x, const double* d2, double* y);
+// y = x * (1.0 / sqrt(*d2))   (orthonormalize's q = w * inv, kernels.cpp:43-45)
+void launch_mul_inv_sqrt(cudaStream_t st, int64_t n, const double* x, const double* d2, double* y);
+// y = b - y (initial residual r = b - A x0)
+void launch_rsub(cudaStream_t st, int64_t n, const double* b, double* y);
+// out: dst[0] = sum x^2, dst[1] = #non-finite, dst[2] = #non-zero
+void launch_vec_stats(cudaStream_t st, int64_t n, const double* x, double* dst, const Reducer& red);
+// b_next = h2 * (x / dt + f) (implicit-Euler chain of the BASELINE configs)
+void launch_euler_rhs(cudaStream_t st, int64_t n, const double* x, const double* f, double dt,
+                      double h2, double* b);
+// b_next = x + alpha * g (banded-random chain)
+void launch_axpby_chain(cudaStream_t st, int64_t n, const double* x, const double* g, double alpha,
+                        double* b);
+
+// ---- standalone kernel helpers (parity tests of the dense steps) --------------------------
+// x = solve_small(M, rhs) on the device (single-warp LU, kernels.cpp:95-154); *ok = 1 / 0.
+void launch_small_solve(cudaStream_t st, int s, const double* m, const double* rhs, double* x,
+                        int32_t* ok);
+
+}  // namespace mstab_b200

@@ -1,0 +1,557 @@
+// solver.cpp — host orchestration of the Mstab solve loop on one B200.
+//
+// Mirrors idrstab_solve / mstab_solve (proj/core/src/idrstab.cpp:193-307) step for step; all
+// length-N work is enqueued as sm_100a kernels on the context stream (kernels.cu) and the host
+// only reads back one CycleStatus per cycle (residual norm, tau, breakdown flag) to drive the
+// loop condition, the counters and the fetch policy, exactly where the reference branches.
+#include "solver.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstddef>
+#include <cstring>
+#include <limits>
+
+namespace mstab_b200 {
+
+#define CUDA_OK(expr)                                                                        \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      throw Error(MSTAB_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+int64_t ns_since(Clock::time_point t0) {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count();
+}
+
+void check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(MSTAB_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+int64_t padded_ld(int64_t n) { return std::max<int64_t>(64, (n + 63) & ~int64_t(63)); }
+
+StreamHolder::~StreamHolder() {
+  if (stream) {
+    cudaStreamSynchronize(stream);
+    cudaStreamDestroy(stream);
+  }
+}
+
+DevMem::DevMem(std::shared_ptr<StreamHolder> st, size_t b) : bytes(b), stream(std::move(st)) {
+  CUDA_OK(cudaMallocAsync(&ptr, b == 0 ? 64 : b, stream->stream));
+}
+
+DevMem::~DevMem() {
+  if (ptr) cudaFreeAsync(ptr, stream->stream);
+}
+
+Context::Context(int dev) {
+  if (dev < 0) CUDA_OK(cudaGetDevice(&dev));
+  device = dev;
+  CUDA_OK(cudaSetDevice(dev));
+  sh = std::make_shared<StreamHolder>();
+  sh->device = dev;
+  CUDA_OK(cudaStreamCreateWithFlags(&sh->stream, cudaStreamNonBlocking));
+  cudaMemPool_t pool;
+  CUDA_OK(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t keep = std::numeric_limits<uint64_t>::max();
+  CUDA_OK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  kernels_init(dev);
+  ds_mem = alloc(sizeof(DevState));
+  CUDA_OK(cudaMemsetAsync(ds_mem->ptr, 0, sizeof(DevState), stream()));
+  partials = alloc(sizeof(double) * (size_t)kMaxGrid * 640);
+  CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host_status), sizeof(CycleStatus)));
+  CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host_scal), sizeof(double) * 64));
+  sync();
+}
+
+Context::~Context() {
+  if (sh && sh->stream) cudaStreamSynchronize(sh->stream);
+  if (host_status) cudaFreeHost(host_status);
+  if (host_scal) cudaFreeHost(host_scal);
+}
+
+void Context::sync() { CUDA_OK(cudaStreamSynchronize(stream())); }
+
+// ---- small device<->host helpers ----------------------------------------------------------
+void reset_status(Context& ctx) {
+  CUDA_OK(cudaMemsetAsync(ctx.ds(), 0, sizeof(CycleStatus), ctx.stream()));
+  CUDA_OK(cudaMemsetAsync(reinterpret_cast<char*>(ctx.ds()) + offsetof(DevState, ticket), 0,
+                          sizeof(uint32_t), ctx.stream()));
+}
+
+double* scal(Context& ctx, int i) { return ctx.ds()->scal + i; }
+
+const double* read_scal(Context& ctx, int count) {
+  CUDA_OK(cudaMemcpyAsync(ctx.host_scal, ctx.ds()->scal, sizeof(double) * count,
+                          cudaMemcpyDeviceToHost, ctx.stream()));
+  ctx.sync();
+  return ctx.host_scal;
+}
+
+const CycleStatus& read_status(Context& ctx) {
+  CUDA_OK(cudaMemcpyAsync(ctx.host_status, &ctx.ds()->st, sizeof(CycleStatus),
+                          cudaMemcpyDeviceToHost, ctx.stream()));
+  ctx.sync();
+  return *ctx.host_status;
+}
+
+namespace {
+
+DevPtr copy_block(Context& ctx, const DevPtr& src, int64_t n, int64_t cols) {
+  DevPtr dst = ctx.alloc_vecs(n, cols);
+  CUDA_OK(cudaMemcpyAsync(dst->ptr, src->ptr, sizeof(double) * (size_t)padded_ld(n) * cols,
+                          cudaMemcpyDeviceToDevice, ctx.stream()));
+  return dst;
+}
+
+// Upload (or device-copy) an N-vector into a fresh padded device vector.
+DevPtr to_device(Context& ctx, const double* src, int64_t n, int mem) {
+  DevPtr d = ctx.alloc_vecs(n, 1);
+  CUDA_OK(cudaMemcpyAsync(d->ptr, src, sizeof(double) * n,
+                          mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                          ctx.stream()));
+  return d;
+}
+
+// Plain SpMV through the fused kernel (s = 1, dot with x discarded).
+void spmv_dev(Context& ctx, const Operator& op, const double* x, double* y) {
+  FinParams f;
+  f.op = kFinStore;
+  f.s = 1;
+  f.dst = scal(ctx, 63);
+  launch_spmv_ph(ctx.stream(), op.csr(), x, y, x, padded_ld(op.n), 1, nullptr, f, ctx.reducer());
+  check_launch();
+}
+
+// ||y||^2 -> scal[i]
+void norm2sq(Context& ctx, int64_t n, const double* y, int i) {
+  launch_dots(ctx.stream(), n, padded_ld(n), nullptr, 0, y, true, scal(ctx, i), ctx.reducer());
+  check_launch();
+}
+
+}  // namespace
+
+// make_cut_space (baselines.cpp:36-47): seeded Gaussian draws (host std::mt19937_64 +
+// std::normal_distribution, column-major, so P's draws are the reference's) orthonormalised on
+// the device by classical Gram-Schmidt applied twice (orthonormalize, kernels.cpp:21-50).
+DevPtr make_cut_space(Context& ctx, int64_t n, int s, uint64_t seed) {
+  const int64_t ld = padded_ld(n);
+  cudaStream_t st = ctx.stream();
+  NormalStream* rng = normal_stream_create(seed);
+  std::unique_ptr<NormalStream, void (*)(NormalStream*)> guard(rng, normal_stream_destroy);
+  std::vector<double> g((size_t)n * s);
+  DevPtr G = ctx.alloc_vecs(n, s);
+  DevPtr Q = ctx.alloc_vecs(n, s);
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    normal_stream_fill(rng, g.data(), (int64_t)g.size());
+    CUDA_OK(cudaMemcpy2DAsync(G->ptr, sizeof(double) * ld, g.data(), sizeof(double) * n,
+                              sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
+    int rank = 0;
+    for (int j = 0; j < s; ++j) {
+      const double* gj = G->d() + (size_t)j * ld;
+      double* w = Q->d() + (size_t)rank * ld;
+      norm2sq(ctx, n, gj, 0);
+      CUDA_OK(cudaMemcpyAsync(w, gj, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      for (int pass = 0; pass < 2 && rank > 0; ++pass) {
+        launch_dots(st, n, ld, Q->d(), rank, w, false, scal(ctx, 8), ctx.reducer());
+        launch_axpy_neg(st, n, ld, Q->d(), rank, scal(ctx, 8), w);
+        check_launch();
+      }
+      norm2sq(ctx, n, w, 1);
+      const double* h = read_scal(ctx, 2);
+      const double norm0 = std::sqrt(h[0]), res = std::sqrt(h[1]);
+      if (res <= 1e-10 * norm0 || norm0 == 0.0) continue;  // kRankTol (kernels.hpp:16)
+      launch_mul_inv_sqrt(st, n, w, scal(ctx, 1), w);
+      check_launch();
+      ++rank;
+    }
+    if (rank == s) return Q;
+  }
+  throw Error(MSTAB_E_ERROR, "make_cut_space: could not draw a full-rank cut-space");
+}
+
+// arnoldi_init (idrstab.cpp:45-87): U orthonormal basis of K_s(A; r0) by MGS with reiteration,
+// V = A U from the same sweep, happy breakdowns padded with seeded Gaussian directions.
+void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s, uint64_t seed,
+                  double* U, double* V) {
+  const int64_t n = op.n, ld = padded_ld(n);
+  cudaStream_t st = ctx.stream();
+  norm2sq(ctx, n, r0, 0);
+  if (read_scal(ctx, 1)[0] == 0.0) throw Error(MSTAB_E_ERROR, "arnoldi_init: zero start vector");
+  launch_div_by_sqrt(st, n, r0, scal(ctx, 0), U);
+  check_launch();
+  std::unique_ptr<NormalStream, void (*)(NormalStream*)> rng(nullptr, normal_stream_destroy);
+  DevPtr w = ctx.alloc_vecs(n, 1);
+  std::vector<double> hw;
+  auto mgs2 = [&](int k) {
+    for (int pass = 0; pass < 2; ++pass)
+      for (int i = 0; i <= k; ++i) {
+        launch_dots(st, n, ld, U + (size_t)i * ld, 1, w->d(), false, scal(ctx, 2), ctx.reducer());
+        launch_axpy_neg(st, n, ld, U + (size_t)i * ld, 1, scal(ctx, 2), w->d());
+        check_launch();
+      }
+  };
+  for (int k = 0; k < s; ++k) {
+    spmv_dev(ctx, op, U + (size_t)k * ld, V + (size_t)k * ld);
+    if (k + 1 == s) break;
+    CUDA_OK(cudaMemcpyAsync(w->ptr, V + (size_t)k * ld, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    norm2sq(ctx, n, w->d(), 1);
+    mgs2(k);
+    norm2sq(ctx, n, w->d(), 3);
+    const double* h = read_scal(ctx, 4);
+    const double wnorm0 = std::sqrt(h[1]);
+    double wnorm = std::sqrt(h[3]);
+    while (wnorm <= 1e-12 * std::max(wnorm0, 1.0)) {
+      if (!rng) rng.reset(normal_stream_create(seed));
+      hw.resize(n);
+      normal_stream_fill(rng.get(), hw.data(), n);
+      CUDA_OK(cudaMemcpyAsync(w->ptr, hw.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      mgs2(k);
+      norm2sq(ctx, n, w->d(), 3);
+      wnorm = std::sqrt(read_scal(ctx, 4)[3]);
+    }
+    launch_div_by_sqrt(st, n, w->d(), scal(ctx, 3), U + (size_t)(k + 1) * ld);
+    check_launch();
+  }
+}
+
+namespace {
+
+struct WSet {
+  DevPtr x, r, U, V;
+  bool ro = false;  // U/V alias an immutable RecycleData
+};
+
+// One outer cycle: ell level iterations + poly_combination, S -> D (idrstab.cpp:250-259).
+void enqueue_cycle(Context& ctx, const Operator& op, const double* P, int s, int ell,
+                   const WSet& S, const WSet& D, const std::vector<DevPtr>& R,
+                   const std::vector<DevPtr>& VL) {
+  const int64_t n = op.n, ld = padded_ld(n);
+  cudaStream_t st = ctx.stream();
+  DevState* ds = ctx.ds();
+  const Reducer red = ctx.reducer();
+  const DevCsr A = op.csr();
+  auto col = [ld](double* base, int q) { return base + (size_t)q * ld; };
+  for (int k = 0; k < ell; ++k) {
+    // (a) top level: r^(k) -= V^(k) gamma_k
+    const double* r_in = (k == 0) ? S.r->d() : R[k]->d();
+    double* r_out = (k == 0) ? D.r->d() : R[k]->d();
+    const double* vk_old = (k == 0) ? S.V->d() : VL[k]->d();
+    double* vk_new = (k == 0) ? D.V->d() : VL[k]->d();
+    launch_level_update(st, n, ld, s, k, r_in, r_out, vk_old, ds);
+    // (b) r^(k+1) = A r^(k); rhs = P^H r^(k+1); eta_0
+    FinParams fb;
+    fb.op = kFinRhsEta0;
+    fb.s = s;
+    fb.k = k;
+    fb.ell = ell;
+    launch_spmv_ph(st, A, r_out, R[k + 1]->d(), P, ld, s, nullptr, fb, red);
+    // (c) column rebuilds at the top level, each raised by one SpMV
+    for (int q = 0; q < s; ++q) {
+      launch_rebuild_top(st, n, ld, s, q, R[k + 1]->d(), vk_old, vk_new, VL[k + 1]->d(), ds);
+      FinParams fc;
+      fc.op = kFinColEta;
+      fc.s = s;
+      fc.k = k;
+      fc.q = q;
+      fc.ell = ell;
+      launch_spmv_ph(st, A, col(vk_new, q), col(VL[k + 1]->d(), q), P, ld, s, nullptr, fc, red);
+    }
+    // deferred (a) for r^(0..k-1), x and (c) for levels -1..k-1
+    const double* lv_in[kMaxEll + 2];
+    double* lv_out[kMaxEll + 2];
+    const double* rin[kMaxEll + 1];
+    double* rout[kMaxEll + 1];
+    lv_in[0] = (k == 0) ? S.U->d() : D.U->d();
+    lv_out[0] = D.U->d();
+    lv_in[1] = D.V->d();
+    lv_out[1] = D.V->d();
+    for (int L = 1; L <= k; ++L) {
+      lv_in[L + 1] = VL[L]->d();
+      lv_out[L + 1] = VL[L]->d();
+    }
+    rin[0] = D.r->d();
+    rout[0] = D.r->d();
+    for (int i = 1; i <= k; ++i) {
+      rin[i] = R[i]->d();
+      rout[i] = R[i]->d();
+    }
+    launch_rebuild_deferred(st, n, ld, s, k, lv_in, lv_out, rin, rout,
+                            (k == 0) ? S.x->d() : D.x->d(), D.x->d(), ds);
+  }
+  check_launch();
+  // poly_combination: least squares, then the combined x, r, U, V (+ next cycle's P^H r, P^H V)
+  const double* rr[kMaxEll + 1];
+  rr[0] = D.r->d();
+  for (int i = 1; i <= ell; ++i) rr[i] = R[i]->d();
+  launch_ls(st, n, ld, ell, s, rr, red);
+  const double* lv[kMaxEll + 2];
+  lv[0] = D.U->d();
+  lv[1] = D.V->d();
+  for (int i = 1; i <= ell; ++i) lv[i + 1] = VL[i]->d();
+  launch_poly(st, n, ld, s, ell, lv, D.U->d(), D.V->d(), rr, D.r->d(), D.x->d(), D.x->d(), P, red);
+  check_launch();
+}
+
+}  // namespace
+
+std::shared_ptr<Operator> make_operator(Context& ctx, int64_t n, const int64_t* row_ptr,
+                                        const int64_t* col_idx, const double* values) {
+  if (n < 0) throw Error(MSTAB_E_DIMENSION, "CsrOperator: negative size");
+  // CsrMatrix::validate (csr.cpp:11-24)
+  if (row_ptr[0] != 0) throw Error(MSTAB_E_ERROR, "csr: row_ptr bounds");
+  const int64_t nnz = row_ptr[n];
+  for (int64_t i = 0; i < n; ++i) {
+    if (row_ptr[i] > row_ptr[i + 1]) throw Error(MSTAB_E_ERROR, "csr: row_ptr not nondecreasing");
+    for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+      if (col_idx[k] < 0 || col_idx[k] >= n) throw Error(MSTAB_E_ERROR, "csr: column index out of range");
+      if (k > row_ptr[i] && col_idx[k - 1] >= col_idx[k])
+        throw Error(MSTAB_E_ERROR, "csr: columns not strictly increasing within a row");
+    }
+  }
+  if (nnz >= (int64_t(1) << 31)) throw Error(MSTAB_E_CONFIG, "b200: nnz >= 2^31 not supported (int32 indices)");
+  auto op = std::make_shared<Operator>();
+  op->n = n;
+  op->nnz = nnz;
+  op->fingerprint = fnv_csr_fingerprint(n, row_ptr, col_idx, values, nnz);
+  std::vector<int32_t> rp32(n + 1), ci32(nnz + 32, 0);
+  for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)row_ptr[i];
+  for (int64_t k = 0; k < nnz; ++k) ci32[k] = (int32_t)col_idx[k];
+  op->rp = ctx.alloc(sizeof(int32_t) * (n + 1));
+  op->ci = ctx.alloc(sizeof(int32_t) * (nnz + 32));
+  op->val = ctx.alloc(sizeof(double) * (nnz + 32));
+  cudaStream_t st = ctx.stream();
+  CUDA_OK(cudaMemcpyAsync(op->rp->ptr, rp32.data(), sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, st));
+  CUDA_OK(cudaMemcpyAsync(op->ci->ptr, ci32.data(), sizeof(int32_t) * (nnz + 32), cudaMemcpyHostToDevice, st));
+  CUDA_OK(cudaMemsetAsync(op->val->ptr, 0, sizeof(double) * (nnz + 32), st));
+  CUDA_OK(cudaMemcpyAsync(op->val->ptr, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+  ctx.sync();
+  return op;
+}
+
+void spmv(Context& ctx, const Operator& op, const double* x_dev, double* y_dev) {
+  reset_status(ctx);
+  spmv_dev(ctx, op, x_dev, y_dev);
+}
+
+mstab_validation_report validate(Context& ctx, const Recycle& rd, const Operator& op) {
+  if (rd.fingerprint != op.fingerprint)
+    throw Error(MSTAB_E_FINGERPRINT, "recycle data belongs to a different operator");
+  if (rd.n != op.n) throw Error(MSTAB_E_DIMENSION, "recycle data has inconsistent shapes");
+  if (!rd.omega.empty() && (int64_t)rd.omega.size() != rd.level_j)
+    throw Error(MSTAB_E_STALE, "recycle data: omega history length disagrees with level");
+  const int s = (int)rd.s;
+  if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: recycle s must be in 1..16");
+  launch_validate(ctx.stream(), op.csr(), rd.p->d(), rd.u->d(), rd.v->d(), padded_ld(rd.n), s,
+                  ctx.reducer());
+  check_launch();
+  std::vector<double> gram(2 * (size_t)s * s);
+  CUDA_OK(cudaMemcpyAsync(gram.data(), ctx.ds()->gram, sizeof(double) * gram.size(),
+                          cudaMemcpyDeviceToHost, ctx.stream()));
+  const double* h = read_scal(ctx, 2);
+  const double dev_num = h[0], dev_den = h[1];
+  const double dev_v = dev_den > 0.0 ? std::sqrt(dev_num) / std::sqrt(dev_den) : std::sqrt(dev_num);
+  double dev_p = 0.0;
+  for (int j = 0; j < s; ++j)
+    for (int i = 0; i < s; ++i) {
+      const double want = (i == j) ? 1.0 : 0.0;
+      dev_p = std::max(dev_p, std::abs(gram[(size_t)i + (size_t)j * s] - want));
+    }
+  mstab_validation_report rep{};
+  rep.max_deviation = std::max(dev_v, dev_p);
+  if (rep.max_deviation > 1e-6) throw Error(MSTAB_E_STALE, "recycle data deviates from its invariants");
+  const auto ev = symmetric_eigenvalues(gram.data() + (size_t)s * s, s);
+  const double smin = std::sqrt(std::max(0.0, ev.front()));
+  const double smax = std::sqrt(std::max(0.0, ev.back()));
+  rep.sigma_min_ratio = smax > 0.0 ? smin / smax : 0.0;
+  rep.low_rank_warning = rep.sigma_min_ratio < 1e-10 ? 1 : 0;
+  return rep;
+}
+
+std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const double* b_in,
+                                       const double* x0_in, int mem, const mstab_solver_config& cfg,
+                                       const Recycle* recycle, const mstab_fetch_policy* fetch) {
+  // SolverConfig::validate (report.cpp:16-22)
+  if (cfg.s < 1) throw Error(MSTAB_E_CONFIG, "config: s >= 1 required");
+  if (cfg.ell < 1) throw Error(MSTAB_E_CONFIG, "config: ell >= 1 required");
+  if (!(cfg.tol > 0.0)) throw Error(MSTAB_E_CONFIG, "config: tol > 0 required");
+  if (cfg.max_mv < cfg.s + 1) throw Error(MSTAB_E_CONFIG, "config: max_mv >= s + 1 required");
+  if (cfg.s > kMaxS || cfg.ell > kMaxEll)
+    throw Error(MSTAB_E_CONFIG, "b200: s <= 16 and ell <= 8 are supported");
+  if (fetch && fetch->kind == MSTAB_FETCH_AT_CYCLE && fetch->cycle < 1)
+    throw Error(MSTAB_E_CONFIG, "fetch policy: cycle >= 1 required");
+  const int s = (int)cfg.s, ell = (int)cfg.ell;
+  const int64_t n = op.n, ld = padded_ld(n);
+  cudaStream_t st = ctx.stream();
+  reset_status(ctx);
+
+  // b: ensure_finite + bnorm (idrstab.cpp:200, :205)
+  DevPtr b = to_device(ctx, b_in, n, mem);
+  launch_vec_stats(st, n, b->d(), scal(ctx, 0), ctx.reducer());
+  check_launch();
+  const double* h = read_scal(ctx, 3);
+  if (h[1] > 0.0) throw Error(MSTAB_E_ERROR, "idrstab rhs: non-finite entries");
+  const auto t0 = Clock::now();
+  auto res = std::make_unique<SolveResultImpl>();
+  res->n = n;
+  mstab_report& rep = res->report;
+  std::memset(&rep, 0, sizeof(rep));
+  rep.ell = ell;
+  rep.bnorm = std::sqrt(h[0]);
+
+  WSet cur, alt;
+  cur.x = ctx.alloc_vecs(n, 1);
+  cur.r = ctx.alloc_vecs(n, 1);
+  bool x_zero = true;
+  if (x0_in) {
+    CUDA_OK(cudaMemcpyAsync(cur.x->ptr, x0_in, sizeof(double) * n,
+                            mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    launch_vec_stats(st, n, cur.x->d(), scal(ctx, 0), ctx.reducer());
+    check_launch();
+    const double* hx = read_scal(ctx, 3);
+    x_zero = hx[2] == 0.0;
+    if (!x_zero && hx[1] > 0.0) throw Error(MSTAB_E_ERROR, "idrstab guess: non-finite entries");
+  } else {
+    CUDA_OK(cudaMemsetAsync(cur.x->ptr, 0, sizeof(double) * n, st));
+  }
+  if (x_zero) {
+    CUDA_OK(cudaMemcpyAsync(cur.r->ptr, b->ptr, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  } else {  // r = b - A x0, one auxiliary MV (idrstab.cpp:210-216)
+    spmv_dev(ctx, op, cur.x->d(), cur.r->d());
+    launch_rsub(st, n, b->d(), cur.r->d());
+    check_launch();
+    rep.h_mv_aux++;
+  }
+
+  DevPtr P;
+  int64_t base_level = 0;
+  std::vector<std::complex<double>> omega_levels;
+  bool omegas_complete = true;
+  if (recycle) {
+    validate(ctx, *recycle, op);
+    rep.h_mv_aux += recycle->s;
+    if (recycle->s != cfg.s) throw Error(MSTAB_E_CONFIG, "idrstab: recycle s != config s");
+    P = recycle->p;
+    cur.U = recycle->u;
+    cur.V = recycle->v;
+    cur.ro = true;
+    base_level = recycle->level_j;
+    omega_levels = recycle->omega;
+    omegas_complete = (int64_t)omega_levels.size() == base_level;
+    if (!omegas_complete) omega_levels.clear();
+  } else {
+    P = make_cut_space(ctx, n, s, cfg.seed);
+    cur.U = ctx.alloc_vecs(n, s);
+    cur.V = ctx.alloc_vecs(n, s);
+    arnoldi_init(ctx, op, cur.r->d(), s, cfg.seed ^ 0x9e3779b97f4a7c15ull, cur.U->d(), cur.V->d());
+    rep.h_mv += s;
+  }
+
+  // P^H V, P^H r, ||r|| and gamma_0 of the first cycle
+  reset_status(ctx);
+  launch_prologue(st, n, ld, s, P->d(), cur.V->d(), cur.r->d(), ctx.reducer());
+  check_launch();
+  double resnorm = read_status(ctx).resnorm;
+  int64_t level = 0;
+  res->history.push_back({0, rep.h_mv + rep.h_mv_aux, base_level, resnorm, ns_since(t0)});
+  const double threshold = cfg.tol * rep.bnorm;
+
+  std::vector<DevPtr> R(ell + 1), VL(ell + 1);
+  for (int i = 1; i <= ell; ++i) {
+    R[i] = ctx.alloc_vecs(n, 1);
+    VL[i] = ctx.alloc_vecs(n, s);
+  }
+  alt.x = ctx.alloc_vecs(n, 1);
+  alt.r = ctx.alloc_vecs(n, 1);
+  alt.U = ctx.alloc_vecs(n, s);
+  alt.V = ctx.alloc_vecs(n, s);
+
+  bool broke = false;
+  while (resnorm > threshold && rep.h_mv < cfg.max_mv) {
+    if (alt.ro) {  // never write into the caller's immutable recycle blocks
+      alt.U = ctx.alloc_vecs(n, s);
+      alt.V = ctx.alloc_vecs(n, s);
+      alt.ro = false;
+    }
+    enqueue_cycle(ctx, op, P->d(), s, ell, cur, alt, R, VL);
+    if (cfg.true_residual_each_cycle) {  // r = b - A x (idrstab.cpp:268-273)
+      FinParams ft;
+      ft.op = kFinTrueRes;
+      ft.s = s;
+      ft.ell = ell;
+      launch_spmv_ph(st, op.csr(), alt.x->d(), alt.r->d(), P->d(), ld, s, b->d(), ft, ctx.reducer());
+      check_launch();
+    }
+    const CycleStatus& cs = read_status(ctx);
+    if (cs.breakdown) {  // BreakdownError: keep the last completed cycle (idrstab.cpp:290-293)
+      rep.h_mv += cs.mv_at_breakdown;
+      rep.status = MSTAB_STATUS_BREAKDOWN;
+      std::snprintf(rep.breakdown_reason, sizeof(rep.breakdown_reason), "%s",
+                    cs.breakdown == kBreakRank ? "least_squares_tall: stabilization block lost rank"
+                                               : "solve_small: pivot collapse");
+      broke = true;
+      break;
+    }
+    std::swap(cur, alt);
+    rep.cycles++;
+    level += ell;
+    rep.h_mv += (int64_t)ell * (s + 1);
+    rep.h_rd = level * s + (recycle ? base_level * (s - 1) : 0);
+    std::vector<double> tau(cs.tau, cs.tau + ell);
+    if (omegas_complete) omegas_complete = extract_omegas(tau, omega_levels);
+    res->taus.insert(res->taus.end(), tau.begin(), tau.end());
+    if (cfg.true_residual_each_cycle) rep.h_mv_aux++;
+    resnorm = cs.resnorm;
+    res->history.push_back({(int64_t)rep.cycles, rep.h_mv + rep.h_mv_aux, base_level + level, resnorm,
+                            ns_since(t0)});
+    if (fetch && !res->fetched) {
+      const bool hit = (fetch->kind == MSTAB_FETCH_AT_CYCLE && rep.cycles == fetch->cycle) ||
+                       (fetch->kind == MSTAB_FETCH_AT_HALF_TOLERANCE &&
+                        resnorm <= std::sqrt(cfg.tol) * rep.bnorm);
+      if (hit) {
+        auto f = std::make_shared<Recycle>();
+        f->n = n;
+        f->s = s;
+        f->level_j = base_level + level;
+        f->fingerprint = op.fingerprint;
+        f->p = P;
+        f->u = copy_block(ctx, cur.U, n, s);
+        f->v = copy_block(ctx, cur.V, n, s);
+        if (omegas_complete) f->omega = omega_levels;
+        res->fetched = f;
+      }
+    }
+  }
+  if (!broke) rep.status = resnorm <= threshold ? MSTAB_STATUS_CONVERGED : MSTAB_STATUS_MAXMV;
+  rep.final_resnorm = resnorm;
+  res->x = cur.x;
+  auto fin = std::make_shared<Recycle>();
+  fin->n = n;
+  fin->s = s;
+  fin->level_j = base_level + level;
+  fin->fingerprint = op.fingerprint;
+  fin->p = P;
+  fin->u = cur.U;  // handed over: the working set is not reused after the solve
+  fin->v = cur.V;
+  if (omegas_complete) fin->omega = omega_levels;
+  res->final_data = fin;
+  rep.has_fetched = res->fetched ? 1 : 0;
+  rep.history_len = (int64_t)res->history.size();
+  rep.tau_len = (int64_t)res->taus.size();
+  ctx.sync();
+  rep.wall_ns_total = ns_since(t0);
+  return res;
+}
+
+}  // namespace mstab_b200

@@ -1,0 +1,112 @@
+// solver.h — C++ objects behind the C-ABI handles of include/mstab_b200.h.
+#pragma once
+#include <complex>
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/mstab_b200.h"
+#include "device_state.h"
+#include "host_util.h"
+#include "kernels.h"
+
+namespace mstab_b200 {
+
+// Device allocation freed stream-ordered on the owning stream (cudaMallocAsync pool).
+struct DevMem {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  std::shared_ptr<struct StreamHolder> stream;
+  DevMem(std::shared_ptr<StreamHolder> st, size_t b);
+  ~DevMem();
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  double* d() const { return static_cast<double*>(ptr); }
+};
+using DevPtr = std::shared_ptr<DevMem>;
+
+struct StreamHolder {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  ~StreamHolder();
+};
+
+int64_t padded_ld(int64_t n);
+
+struct Context {
+  std::shared_ptr<StreamHolder> sh;
+  int device = 0;
+  DevPtr ds_mem;        // DevState
+  DevPtr partials;      // reduction partials
+  CycleStatus* host_status = nullptr;  // pinned
+  double* host_scal = nullptr;         // pinned, 64 doubles
+  cudaStream_t stream() const { return sh->stream; }
+  DevState* ds() const { return static_cast<DevState*>(ds_mem->ptr); }
+  Reducer reducer() const { return Reducer{partials->d(), ds()}; }
+  DevPtr alloc(size_t bytes) { return std::make_shared<DevMem>(sh, bytes); }
+  DevPtr alloc_vecs(int64_t n, int64_t cols) {
+    return alloc(sizeof(double) * (size_t)padded_ld(n) * (size_t)std::max<int64_t>(cols, 1));
+  }
+  void sync();
+  explicit Context(int device);
+  ~Context();
+};
+
+struct Operator {
+  int64_t n = 0, nnz = 0;
+  uint64_t fingerprint = 0;
+  DevPtr rp, ci, val;
+  DevCsr csr() const {
+    DevCsr c;
+    c.n = n;
+    c.nnz = nnz;
+    c.row_ptr = static_cast<const int32_t*>(rp->ptr);
+    c.col_idx = static_cast<const int32_t*>(ci->ptr);
+    c.values = val->d();
+    return c;
+  }
+};
+
+struct Recycle {
+  int64_t n = 0, s = 0, level_j = 0;
+  uint64_t fingerprint = 0;
+  DevPtr p, u, v;  // n x s blocks with ld = padded_ld(n); immutable
+  std::vector<std::complex<double>> omega;
+};
+using RecyclePtr = std::shared_ptr<const Recycle>;
+
+struct SolveResultImpl {
+  DevPtr x;
+  int64_t n = 0;
+  mstab_report report{};
+  std::vector<mstab_history_point> history;
+  std::vector<double> taus;  // cycle-major, ell per cycle (real parts; imaginary parts are 0)
+  RecyclePtr final_data;
+  RecyclePtr fetched;
+};
+
+// idrstab_solve / mstab_solve (idrstab.cpp:193-307) on the device.
+std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const double* b,
+                                       const double* x0, int mem, const mstab_solver_config& cfg,
+                                       const Recycle* recycle, const mstab_fetch_policy* fetch);
+
+// validate (recycle.cpp:40-83). Throws Error with the reference's class code.
+mstab_validation_report validate(Context& ctx, const Recycle& rd, const Operator& op);
+
+std::shared_ptr<Operator> make_operator(Context& ctx, int64_t n, const int64_t* row_ptr,
+                                        const int64_t* col_idx, const double* values);
+
+void spmv(Context& ctx, const Operator& op, const double* x_dev, double* y_dev);
+
+// make_cut_space (baselines.cpp:36-47): returns the orthonormal n x s block P on the device.
+DevPtr make_cut_space(Context& ctx, int64_t n, int s, uint64_t seed);
+// arnoldi_init (idrstab.cpp:45-87) with rng seed `rng_seed` for the padding draws.
+void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s, uint64_t rng_seed,
+                  double* U, double* V);
+// Host-visible helpers for the kernel-level C entry points.
+const double* read_scal(Context& ctx, int count);
+const CycleStatus& read_status(Context& ctx);
+void reset_status(Context& ctx);
+
+}  // namespace mstab_b200

@@ -1,0 +1,533 @@
+"""Python mirror of the reference's proj/core solver interface, over the C-ABI.
+
+Same names, argument meaning and error behaviour as the reference
+(``mstab::idrstab_solve`` / ``mstab_solve`` in proj/core/include/mstab/solvers/idrstab.hpp:88-96,
+``SolverConfig``/``SolveReport`` in report.hpp:24-58, ``RecycleData``/``FetchPolicy``/
+``validate``/``save``/``load`` in recycle.hpp:18-64, the error classes of errors.hpp), so the
+tests read like the reference's own GTest suites. Arrays are real float64 numpy vectors on the
+host, or CUDA tensors (anything with ``__cuda_array_interface__`` / ``data_ptr``) on the device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import List, Optional
+
+import numpy as np
+
+from . import _capi
+from ._capi import Lib, dptr, i64ptr
+
+
+# ---- errors (errors.hpp:9-72) -----------------------------------------------------------------
+class Error(RuntimeError):
+    pass
+
+
+class BreakdownError(Error):
+    pass
+
+
+class DimensionMismatch(Error):
+    pass
+
+
+class SingularProjection(BreakdownError):
+    pass
+
+
+class RankDeficient(BreakdownError):
+    pass
+
+
+class FingerprintMismatch(Error):
+    pass
+
+
+class StaleData(Error):
+    pass
+
+
+class ParseError(Error):
+    pass
+
+
+class IoError(Error):
+    pass
+
+
+class ConfigError(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+class NotReal(ConfigError):
+    pass
+
+
+_ERR = {-1: Error, -2: DimensionMismatch, -3: ConfigError, -4: FingerprintMismatch, -5: StaleData,
+        -6: ParseError, -7: IoError, -8: SingularProjection, -9: RankDeficient, -20: CudaError,
+        -21: NotReal}
+
+
+def _check(lib: Lib, rc: int):
+    if rc != 0:
+        raise _ERR.get(rc, Error)(lib.last_error())
+
+
+# ---- config / report (report.hpp) -------------------------------------------------------------
+@dataclass
+class SolverConfig:
+    s: int = 2
+    ell: int = 1
+    tol: float = 1e-8
+    max_mv: int = 100000
+    true_residual_each_cycle: bool = False
+    seed: int = 0
+
+    def _c(self):
+        return _capi.SolverConfigC(int(self.s), int(self.ell), float(self.tol), int(self.max_mv),
+                                   1 if self.true_residual_each_cycle else 0, 0, int(self.seed) & (2**64 - 1))
+
+
+@dataclass
+class FetchPolicy:
+    kind: int = _capi.FETCH_MANUAL
+    cycle: int = 0
+
+    @staticmethod
+    def at_cycle(k: int) -> "FetchPolicy":
+        if k < 1:
+            raise ConfigError("fetch policy: cycle >= 1 required")
+        return FetchPolicy(_capi.FETCH_AT_CYCLE, int(k))
+
+    @staticmethod
+    def at_half_tolerance() -> "FetchPolicy":
+        return FetchPolicy(_capi.FETCH_AT_HALF_TOLERANCE, 0)
+
+    @staticmethod
+    def manual() -> "FetchPolicy":
+        return FetchPolicy(_capi.FETCH_MANUAL, 0)
+
+
+CONVERGED, MAXMV, BREAKDOWN = "Converged", "MaxMV", "Breakdown"
+_STATUS = {0: CONVERGED, 1: MAXMV, 2: BREAKDOWN}
+
+
+@dataclass
+class HistoryPoint:
+    cycle: int
+    mv: int
+    level: int
+    resnorm: float
+    wall_ns: int
+
+
+@dataclass
+class SolveReport:
+    residual_history: List[HistoryPoint] = field(default_factory=list)
+    omega_history: List[np.ndarray] = field(default_factory=list)  # tau per cycle
+    h_mv: int = 0
+    h_mv_aux: int = 0
+    h_rd: int = 0
+    cycles: int = 0
+    status: str = MAXMV
+    breakdown_reason: str = ""
+    bnorm: float = 0.0
+    final_resnorm: float = 0.0
+    wall_ns_total: int = 0
+
+    def total_mv(self) -> int:
+        return self.h_mv + self.h_mv_aux
+
+
+@dataclass
+class ValidationReport:
+    max_deviation: float
+    sigma_min_ratio: float
+    low_rank_warning: bool
+
+
+# ---- context ----------------------------------------------------------------------------------
+class Context:
+    """Device + stream binding of one implementation (``mstab_context``)."""
+
+    def __init__(self, lib: Optional[Lib] = None, device: int = 0):
+        self.lib = lib if lib is not None else Lib()
+        h = C.c_void_p()
+        _check(self.lib, self.lib.dll.mstab_context_create(int(device), C.byref(h)))
+        self.h = h
+
+    def synchronize(self):
+        _check(self.lib, self.lib.dll.mstab_context_synchronize(self.h))
+
+    @property
+    def stream(self) -> int:
+        return self.lib.dll.mstab_context_stream(self.h) or 0
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.dll.mstab_context_destroy(self.h)
+            self.h = None
+
+
+_default_ctx: dict = {}
+
+
+def default_context(lib: Optional[Lib] = None) -> Context:
+    lib = lib if lib is not None else Lib()
+    if lib.path not in _default_ctx:
+        _default_ctx[lib.path] = Context(lib)
+    return _default_ctx[lib.path]
+
+
+def _f64(a) -> np.ndarray:
+    a = np.asarray(a)
+    if np.iscomplexobj(a):
+        if np.any(a.imag != 0):
+            raise NotReal("complex data: this build is the real fp64 path")
+        a = a.real
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _dev_ptr(a):
+    """(pointer, mem) for a numpy array or a CUDA tensor."""
+    if hasattr(a, "__cuda_array_interface__"):
+        return a.__cuda_array_interface__["data"][0], _capi.MEM_DEVICE
+    if hasattr(a, "is_cuda") and a.is_cuda:
+        return a.data_ptr(), _capi.MEM_DEVICE
+    return None, _capi.MEM_HOST
+
+
+# ---- matrices / operators (csr.hpp, operator.hpp) ---------------------------------------------
+class CsrMatrix:
+    """Compressed sparse row matrix (csr.hpp:17-52), real fp64 values, int64 indices."""
+
+    def __init__(self, n_rows, n_cols, row_ptr, col_idx, values):
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+        self.row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        self.col_idx = np.ascontiguousarray(col_idx, dtype=np.int64)
+        self.values = _f64(values)
+
+    def nnz(self) -> int:
+        return int(self.values.size)
+
+    @staticmethod
+    def from_triplets(n_rows, n_cols, triplets):
+        """Duplicates are summed (csr.cpp:53-79)."""
+        d = {}
+        for i, j, v in triplets:
+            if not (0 <= i < n_rows and 0 <= j < n_cols):
+                raise Error("from_triplets: index out of range")
+            d[(i, j)] = d.get((i, j), 0.0) + v
+        keys = sorted(d)
+        rp = np.zeros(n_rows + 1, dtype=np.int64)
+        for i, _ in keys:
+            rp[i + 1] += 1
+        rp = np.cumsum(rp)
+        return CsrMatrix(n_rows, n_cols, rp, [j for _, j in keys], [d[k] for k in keys])
+
+    @staticmethod
+    def identity(n):
+        return CsrMatrix(n, n, np.arange(n + 1), np.arange(n), np.ones(n))
+
+    @staticmethod
+    def tridiag(a, b, c, n):
+        """a on the sub-, b on the main, c on the super-diagonal (csr.cpp:92-101)."""
+        t = []
+        for i in range(n):
+            if i > 0:
+                t.append((i, i - 1, a))
+            t.append((i, i, b))
+            if i + 1 < n:
+                t.append((i, i + 1, c))
+        return CsrMatrix.from_triplets(n, n, t)
+
+    @staticmethod
+    def from_dense(m):
+        m = np.asarray(m, dtype=np.float64)
+        n = m.shape[0]
+        t = [(i, j, m[i, j]) for i in range(n) for j in range(m.shape[1])]
+        return CsrMatrix.from_triplets(n, m.shape[1], t)
+
+    def to_dense(self):
+        d = np.zeros((self.n_rows, self.n_cols))
+        for i in range(self.n_rows):
+            for k in range(self.row_ptr[i], self.row_ptr[i + 1]):
+                d[i, self.col_idx[k]] = self.values[k]
+        return d
+
+
+class CsrOperator:
+    """LinearOperator over a CSR matrix (operator.hpp:33-50); uploaded once, fingerprint cached."""
+
+    def __init__(self, a: CsrMatrix, ctx: Optional[Context] = None):
+        if a.n_rows != a.n_cols:
+            raise DimensionMismatch("CsrOperator: square matrix required")
+        self.ctx = ctx if ctx is not None else default_context()
+        self.lib = self.ctx.lib
+        self.matrix = a
+        h = C.c_void_p()
+        _check(self.lib, self.lib.dll.mstab_operator_create_csr(
+            self.ctx.h, a.n_rows, i64ptr(a.row_ptr), i64ptr(a.col_idx), dptr(a.values), C.byref(h)))
+        self.h = h
+
+    def size(self) -> int:
+        return int(self.lib.dll.mstab_operator_size(self.h))
+
+    def fingerprint(self) -> int:
+        return int(self.lib.dll.mstab_operator_fingerprint(self.h))
+
+    def is_real(self) -> bool:
+        return True
+
+    def apply(self, x, y=None):
+        ptr, mem = _dev_ptr(x)
+        if mem == _capi.MEM_DEVICE:
+            yptr, _ = _dev_ptr(y)
+            _check(self.lib, self.lib.dll.mstab_operator_apply(self.ctx.h, self.h, ptr, yptr, mem))
+            return y
+        x = _f64(x)
+        if x.size != self.size():
+            raise DimensionMismatch("spmv: dimension mismatch")
+        out = np.empty_like(x)
+        _check(self.lib, self.lib.dll.mstab_operator_apply(self.ctx.h, self.h, x.ctypes.data, out.ctypes.data,
+                                                           _capi.MEM_HOST))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.dll.mstab_operator_destroy(self.h)
+            self.h = None
+
+
+# ---- recycle data (recycle.hpp) ---------------------------------------------------------------
+class RecycleData:
+    """Immutable recycle state (P, U, V, omega history, level J, s, fingerprint); device-resident
+    in the B200 implementation, downloaded lazily."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx, self.lib, self.h = ctx, ctx.lib, handle
+        info = _capi.RecycleInfoC()
+        _check(self.lib, self.lib.dll.mstab_recycle_info_get(handle, C.byref(info)))
+        self.n, self.s, self.level_J = int(info.n), int(info.s), int(info.level_j)
+        self.matrix_fingerprint = int(info.fingerprint)
+        self._omega_count = int(info.omega_count)
+        self._blocks = None
+        self._omega = None
+
+    def _download(self):
+        if self._blocks is None:
+            n, s = self.n, self.s
+            p, u, v = (np.empty((s, n)) for _ in range(3))
+            om = np.empty(2 * max(self._omega_count, 1))
+            _check(self.lib, self.lib.dll.mstab_recycle_download(self.ctx.h, self.h, dptr(p), dptr(u), dptr(v),
+                                                                 dptr(om)))
+            self._blocks = (p.T, u.T, v.T)  # n x s views of the column-major data
+            self._omega = om[0:2 * self._omega_count:2] + 1j * om[1:2 * self._omega_count:2]
+        return self._blocks
+
+    @property
+    def p(self):
+        return self._download()[0]
+
+    @property
+    def u(self):
+        return self._download()[1]
+
+    @property
+    def v(self):
+        return self._download()[2]
+
+    @property
+    def omega_history(self):
+        self._download()
+        return self._omega
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.dll.mstab_recycle_destroy(self.h)
+            self.h = None
+
+
+def fetch(p, u, v, omega_history, level_j, fingerprint, ctx: Optional[Context] = None) -> RecycleData:
+    """Deep-copy constructor of RecycleData (recycle.cpp:26-38)."""
+    ctx = ctx if ctx is not None else default_context()
+    p, u, v = (np.asfortranarray(_f64(a)) for a in (p, u, v))
+    n, s = p.shape
+    om = np.asarray(omega_history, dtype=np.complex128).ravel()
+    omr = np.empty(2 * max(om.size, 1))
+    omr[0:2 * om.size:2] = om.real
+    omr[1:2 * om.size:2] = om.imag
+    h = C.c_void_p()
+    _check(ctx.lib, ctx.lib.dll.mstab_recycle_create(
+        ctx.h, n, s, p.ctypes.data, u.ctypes.data, v.ctypes.data, _capi.MEM_HOST, dptr(omr), om.size,
+        int(level_j), int(fingerprint), C.byref(h)))
+    return RecycleData(ctx, h)
+
+
+def validate(data: RecycleData, op: CsrOperator) -> ValidationReport:
+    r = _capi.ValidationReportC()
+    _check(op.lib, op.lib.dll.mstab_recycle_validate(op.ctx.h, data.h, op.h, C.byref(r)))
+    return ValidationReport(r.max_deviation, r.sigma_min_ratio, bool(r.low_rank_warning))
+
+
+def save(data: RecycleData, path) -> None:
+    _check(data.lib, data.lib.dll.mstab_recycle_save(data.ctx.h, data.h, str(path).encode()))
+
+
+def load(path, ctx: Optional[Context] = None) -> RecycleData:
+    ctx = ctx if ctx is not None else default_context()
+    h = C.c_void_p()
+    _check(ctx.lib, ctx.lib.dll.mstab_recycle_load(ctx.h, str(path).encode(), C.byref(h)))
+    return RecycleData(ctx, h)
+
+
+# ---- solve (idrstab.hpp:70-96) ----------------------------------------------------------------
+class SolveResult:
+    def __init__(self, ctx: Context, handle):
+        self.ctx, self.lib, self.h = ctx, ctx.lib, handle
+        rep = _capi.ReportC()
+        _check(self.lib, self.lib.dll.mstab_result_report(handle, C.byref(rep)))
+        self._rep = rep
+        self.n = None
+        self._x = None
+        self._report = None
+
+    @property
+    def report(self) -> SolveReport:
+        if self._report is None:
+            r = self._rep
+            hist = (_capi.HistoryPointC * max(r.history_len, 1))()
+            cnt = self.lib.dll.mstab_result_history(self.h, hist, r.history_len)
+            taus = np.empty(2 * max(r.tau_len, 1))
+            tcnt = self.lib.dll.mstab_result_taus(self.h, dptr(taus), r.tau_len)
+            t = taus[0:2 * tcnt:2] + 1j * taus[1:2 * tcnt:2]
+            ell = int(r.ell) if r.ell > 0 else 1
+            self._report = SolveReport(
+                residual_history=[HistoryPoint(h.cycle, h.mv, h.level, h.resnorm, h.wall_ns) for h in hist[:cnt]],
+                omega_history=[t[i:i + ell] for i in range(0, tcnt, ell)],
+                h_mv=r.h_mv, h_mv_aux=r.h_mv_aux, h_rd=r.h_rd, cycles=r.cycles, status=_STATUS[r.status],
+                breakdown_reason=r.breakdown_reason.decode(), bnorm=r.bnorm, final_resnorm=r.final_resnorm,
+                wall_ns_total=r.wall_ns_total)
+        return self._report
+
+    @property
+    def x(self) -> np.ndarray:
+        if self._x is None:
+            out = np.empty(self.n)
+            _check(self.lib, self.lib.dll.mstab_result_x(self.ctx.h, self.h, out.ctypes.data, _capi.MEM_HOST))
+            self._x = out
+        return self._x
+
+    def x_into(self, dst) -> None:
+        """Copy x into a CUDA tensor / host array without materialising it in Python."""
+        ptr, mem = _dev_ptr(dst)
+        if mem == _capi.MEM_HOST:
+            ptr = dst.ctypes.data
+        _check(self.lib, self.lib.dll.mstab_result_x(self.ctx.h, self.h, ptr, mem))
+
+    def _rd(self, fn) -> RecycleData:
+        h = C.c_void_p()
+        _check(self.lib, fn(self.h, C.byref(h)))
+        return RecycleData(self.ctx, h)
+
+    @property
+    def final_data(self) -> RecycleData:
+        return self._rd(self.lib.dll.mstab_result_final_data)
+
+    @property
+    def fetched(self) -> Optional[RecycleData]:
+        return self._rd(self.lib.dll.mstab_result_fetched) if self._rep.has_fetched else None
+
+    def handoff(self) -> RecycleData:
+        return self._rd(self.lib.dll.mstab_result_handoff)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.dll.mstab_result_destroy(self.h)
+            self.h = None
+
+
+def idrstab_solve(a: CsrOperator, b, x0=None, cfg: Optional[SolverConfig] = None,
+                  recycle: Optional[RecycleData] = None, fetch_policy: Optional[FetchPolicy] = None) -> SolveResult:
+    """IDR(s)stab(ell); M(s,ell)stab when `recycle` is given (idrstab.hpp:88-91)."""
+    cfg = cfg if cfg is not None else SolverConfig()
+    ctx, lib = a.ctx, a.lib
+    n = a.size()
+    bptr, mem = _dev_ptr(b)
+    keep = []
+    if mem == _capi.MEM_HOST:
+        b = _f64(b)
+        if b.size != n:
+            raise DimensionMismatch("idrstab: rhs size")
+        keep.append(b)
+        bptr = b.ctypes.data
+    xptr = None
+    if x0 is not None and (not hasattr(x0, "__len__") or len(x0) > 0):
+        if mem == _capi.MEM_HOST:
+            x0 = _f64(x0)
+            if x0.size != n:
+                raise DimensionMismatch("idrstab: guess size")
+            keep.append(x0)
+            xptr = x0.ctypes.data
+        else:
+            xptr, _ = _dev_ptr(x0)
+    c = cfg._c()
+    fp = None
+    if fetch_policy is not None:
+        fp = _capi.FetchPolicyC(fetch_policy.kind, 0, fetch_policy.cycle)
+    h = C.c_void_p()
+    _check(lib, lib.dll.mstab_solve(ctx.h, a.h, bptr, xptr, mem, C.byref(c), recycle.h if recycle else None,
+                                    C.byref(fp) if fp is not None else None, C.byref(h)))
+    res = SolveResult(ctx, h)
+    res.n = n
+    return res
+
+
+def mstab_solve(a: CsrOperator, b, x0, cfg: SolverConfig, recycle: RecycleData,
+                fetch_policy: Optional[FetchPolicy] = None) -> SolveResult:
+    """M(s,ell)stab: idrstab_solve with mandatory recycle data (idrstab.hpp:94-96)."""
+    return idrstab_solve(a, b, x0, cfg, recycle, fetch_policy)
+
+
+# ---- kernel-level helpers (include/mstab_b200_kernels.h) --------------------------------------
+def solve_small(m, rhs, ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx if ctx is not None else default_context()
+    m = np.asfortranarray(_f64(m))
+    rhs = _f64(rhs)
+    x = np.empty_like(rhs)
+    _check(ctx.lib, ctx.lib.dll.mstab_kernel_solve_small(ctx.h, m.shape[0], m.ctypes.data_as(_capi._D),
+                                                         dptr(rhs), dptr(x)))
+    return x
+
+
+def least_squares_tall(z, r, ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx if ctx is not None else default_context()
+    z = np.asfortranarray(_f64(z))
+    r = _f64(r)
+    n, ell = z.shape
+    tau = np.empty(ell)
+    _check(ctx.lib, ctx.lib.dll.mstab_kernel_least_squares(ctx.h, n, ell, z.ctypes.data_as(_capi._D), dptr(r),
+                                                           dptr(tau)))
+    return tau
+
+
+def make_cut_space(n, s, seed, ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx if ctx is not None else default_context()
+    p = np.empty((s, n))
+    _check(ctx.lib, ctx.lib.dll.mstab_kernel_cut_space(ctx.h, n, s, seed, dptr(p)))
+    return p.T
+
+
+def arnoldi_init(a: CsrOperator, r0, s, rng_seed):
+    r0 = _f64(r0)
+    n = r0.size
+    u, v = np.empty((s, n)), np.empty((s, n))
+    mv = C.c_int64(0)
+    _check(a.lib, a.lib.dll.mstab_kernel_arnoldi(a.ctx.h, a.h, dptr(r0), s, rng_seed, dptr(u), dptr(v), C.byref(mv)))
+    return u.T, v.T, int(mv.value)
