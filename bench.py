@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""bench.py — solved RHS/s over the BASELINE c2 system sequence on B200.
+
+Workload (BASELINE.json configs[1], builder-defined details in SURVEY.md §8(d) / DESIGN.md §5):
+3-D convection-diffusion 128^3 (N = 2,097,152, 7-point first-order upwind, beta = (1,.5,.25)*200,
+h^2-scaled implicit Euler, dt = 1e-2), a chained right-hand-side sequence b_{i+1} = h^2(x_i/dt + f),
+M(8,4)stab with tol 1e-8 on the true residual (true_residual_each_cycle), recycle hand-off at half
+tolerance. A STEP is one right-hand side of that sequence: the whole mstab_solve (validate, cycles,
+fetch, hand-off); a hand-off rejected by validate (StaleData, recycle.cpp:73) is re-solved fresh.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Arms:
+  b200 (default)  value: device-resident inputs (b, x in HBM), CUDA events on the solver stream;
+                  e2e:   the same sequence through the C-ABI with HOST b/x (H2D + D2H every step).
+  reference       the unmodified reference (oracle/_ref, compiled from its own sources) advancing its
+                  own solve loop on the same c2 system one level iteration per step, 1 host core.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "solved RHS/sec over a system sequence; SpMV+block-kernel HBM GB/s vs roofline"
+UNIT = "RHS/s"
+REF_LIB = ROOT / "oracle" / "_ref" / "libmstab_ref.so"
+CYCLES_FILE = ROOT / "profiles" / "sequence_cycles.json"
+NCU_FILE = ROOT / "profiles" / "ncu_traffic.json"
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def workload_desc(cfg, A):
+    return {
+        "workload": f"{cfg.name}: 3-D conv-diff {cfg.grid}^3 7-pt upwind Pe=200, implicit-Euler RHS sequence, "
+                    f"M({cfg.s},{cfg.ell})stab tol 1e-8 (true residual), fetch at half tolerance",
+        "N": int(A.n_rows), "nnz": int(A.nnz()), "s": cfg.s, "ell": cfg.ell, "sequence_len": cfg.n_rhs,
+        "l2": "working set ~80 N-vectors = 1.34 GB >> 126 MB L2 (no flush needed)",
+    }
+
+
+# ---- clocks sampling (B200_PROFILING.md) -------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---- the sequence driver (caller side of the hot path; reference harness.cpp:192-265) ----------
+class Sequence:
+    def __init__(self, m, cfg, op, ctx, seed, device_mode, torch=None):
+        self.m, self.cfg, self.op, self.ctx, self.torch = m, cfg, op, ctx, torch
+        cfg.seed = seed
+        self.x0, self.f = cfg.sources()
+        self.sc = m.SolverConfig(cfg.s, cfg.ell, cfg.tol, 100000, True, 0)
+        self.fp = m.FetchPolicy.at_half_tolerance()
+        self.device_mode = device_mode
+        self.rec = None
+        self.restarts = 0
+        self.log = []
+        N = cfg.N
+        if device_mode:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            self.f_d = torch.from_numpy(self.f).to(dev)
+            self.x_d = torch.empty(N, dtype=torch.float64, device=dev)
+            self.b_d = torch.from_numpy(cfg.first_rhs(self.x0, self.f)).to(dev)
+            torch.cuda.synchronize()
+        else:
+            self.b_h = torch.from_numpy(cfg.first_rhs(self.x0, self.f)).pin_memory().numpy()
+            self.x_h = torch.empty(N, dtype=torch.float64).pin_memory().numpy()
+
+    def step(self):
+        m, t = self.m, self.torch
+        b = self.b_d if self.device_mode else self.b_h
+        restarted = False
+        try:
+            r = m.idrstab_solve(self.op, b, None, self.sc, self.rec, self.fp)
+        except m.StaleData:
+            restarted = True
+            self.restarts += 1
+            r = m.idrstab_solve(self.op, b, None, self.sc, None, self.fp)
+        rep = r._rep
+        self.log.append({"cycles": int(rep.cycles), "status": int(rep.status), "restart": restarted,
+                         "relres": float(rep.final_resnorm / rep.bnorm) if rep.bnorm else 0.0})
+        self.rec = r.handoff()
+        c = self.cfg
+        if self.device_mode:
+            r.x_into(self.x_d)  # D2D on the solver stream (synchronised)
+            self.b_d = c.h2 * (self.x_d / c.dt + self.f_d)  # b_{i+1} = h^2 (x_i/dt + f), same rounding order
+            t.cuda.current_stream().synchronize()
+        else:
+            r.x_into(self.x_h)  # D2H into pinned host memory
+            from paper_1604_06043_b200 import problems as pb
+            self.b_h[:] = pb.euler_rhs(self.x_h, self.f, c.dt, c.h2)
+        return r
+
+
+def run_b200(args):
+    import torch
+    import paper_1604_06043_b200 as m
+    from paper_1604_06043_b200 import _capi
+    from paper_1604_06043_b200 import problems as pb
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    lib = m.Lib()
+    ctx = m.Context(lib, local)
+    cfg = pb.config(args.config, grid=args.grid)
+    A = cfg.matrix()
+    op = m.CsrOperator(A, ctx)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    N = cfg.N
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- value: device-resident inputs -------------------------------------------------------
+    seq = Sequence(m, cfg, op, ctx, seed=rank, device_mode=True, torch=torch)
+    for _ in range(args.warmup):
+        seq.step()
+    barrier()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    lib.dll.mstab_profiling_reset()
+    lib.dll.mstab_profiling_enable(1)
+    l0 = lib.dll.mstab_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            seq.step()
+        ev1.record(stream)
+        ev1.synchronize()
+    launches = int(lib.dll.mstab_launch_count() - l0)
+    lib.dll.mstab_profiling_enable(0)
+    stats = (_capi.KernelClassStatsC * 16)()
+    ncls = lib.dll.mstab_profiling_read(stats, 16)
+    ms = ev0.elapsed_time(ev1)
+    barrier()
+    ms_max = max_over_ranks(ms)
+    timed = seq.log[args.warmup:]
+    value = world * args.steps / (ms_max / 1e3)
+
+    # ---- e2e: host buffers through the C-ABI --------------------------------------------------
+    seq_h = Sequence(m, cfg, op, ctx, seed=rank, device_mode=False, torch=torch)
+    for _ in range(args.warmup):
+        seq_h.step()
+    barrier()
+    ctx.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        seq_h.step()
+    e1.record(stream)
+    e1.synchronize()
+    ems = max_over_ranks(e0.elapsed_time(e1))
+    e2e = {"value": world * args.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * N,
+           "d2h_bytes_per_step": 8 * N}
+
+    # ---- per-kernel roofline of the timed region ---------------------------------------------
+    hbm, hbm_src = peaks()
+    kernels = {}
+    total_ms = sum(stats[i].total_ms for i in range(ncls))
+    for i in range(ncls):
+        s = stats[i]
+        if s.launches == 0:
+            continue
+        avg_ms = s.total_ms / s.launches
+        gbs = (s.total_bytes / s.launches) / (avg_ms / 1e3) / 1e9 if avg_ms > 0 else 0.0
+        kernels[lib.dll.mstab_kernel_class_name(i).decode()] = {
+            "launches": int(s.launches), "avg_us": round(avg_ms * 1e3, 3),
+            "bytes_per_launch": s.total_bytes / s.launches, "achieved_gbs": round(gbs, 1),
+            "frac": round(gbs / hbm, 4), "share_of_kernel_time": round(s.total_ms / total_ms, 4)}
+    dom = "spmv_ph"
+    traffic = None
+    if NCU_FILE.exists():
+        try:
+            traffic = json.loads(NCU_FILE.read_text()).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "kernel": dom, "achieved": kernels.get(dom, {}).get("achieved_gbs"),
+            "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
+            "frac": kernels.get(dom, {}).get("frac"), "traffic": traffic,
+            "bytes_per_launch": kernels.get(dom, {}).get("bytes_per_launch")}
+
+    mean_cycles = float(np.mean([r["cycles"] for r in timed])) if timed else None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, A, mean_cycles, steps=args.cpu_levels)
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, DESIGN.md §5)",
+            "config": dict(workload_desc(cfg, A), parallelism=(f"replicas{world}: independent sequences per GPU"
+                                                              if world > 1 else "single GPU"),
+                           rhs_range=[args.warmup + 1, args.warmup + args.steps]),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "kernels": kernels,
+            "sequence": {"mean_cycles_per_rhs": mean_cycles, "restarts": seq.restarts,
+                         "max_true_relres": max(r["relres"] for r in timed) if timed else None,
+                         "per_rhs": timed},
+        }
+        print(json.dumps(out), flush=True)
+        if args.write_cycles:
+            CYCLES_FILE.write_text(json.dumps({args.config: {"mean_cycles_per_rhs": mean_cycles,
+                                                              "rhs_range": out["config"]["rhs_range"],
+                                                              "per_rhs": [r["cycles"] for r in timed]}}, indent=1))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+# ---- the reference arm ------------------------------------------------------------------------
+def ref_sampler(cfg, A):
+    import ctypes as C
+
+    import paper_1604_06043_b200 as m
+    lib = m.Lib(REF_LIB)
+    lib.dll.mstab_ref_sample_create.restype = C.c_void_p
+    lib.dll.mstab_ref_sample_create.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int64, C.c_int64, C.c_uint64]
+    lib.dll.mstab_ref_sample_step.argtypes = [C.c_void_p]
+    lib.dll.mstab_ref_sample_destroy.argtypes = [C.c_void_p]
+    ctx = m.Context(lib)
+    op = m.CsrOperator(A, ctx)
+    x0, f = cfg.sources()
+    b = cfg.first_rhs(x0, f)
+    h = lib.dll.mstab_ref_sample_create(op.h, b.ctypes.data_as(C.POINTER(C.c_double)), cfg.s, cfg.ell, 0)
+    if not h:
+        raise RuntimeError("reference sample init failed: " + lib.last_error())
+    return lib, op, h
+
+
+def workload_cycles(cfg, measured):
+    if measured:
+        return measured, "measured in this run (b200 arm, same sequence positions)"
+    try:
+        d = json.loads(CYCLES_FILE.read_text())[cfg.name]
+        return d["mean_cycles_per_rhs"], f"profiles/{CYCLES_FILE.name} (b200 arm, RHS {d['rhs_range']})"
+    except Exception:
+        return 11.0, "fresh-solve cycle count of the c2 system (no sequence record)"
+
+
+def cpu_baseline(cfg, A, mean_cycles, steps):
+    """The reference's own loop on this system, `steps` level iterations on 1 core."""
+    lib, op, h = ref_sampler(cfg, A)
+    t = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        lib.dll.mstab_ref_sample_step(h)
+        t.append(time.perf_counter() - t0)
+    lib.dll.mstab_ref_sample_destroy(h)
+    cyc, src = workload_cycles(cfg, mean_cycles)
+    per_level = sum(t) / len(t)
+    rhs_s = 1.0 / (cyc * cfg.ell * per_level)
+    return {"value": rhs_s, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"{steps} level iterations of the reference solve loop (oracle/_ref, unmodified sources) on "
+                      f"the {cfg.name} system, {per_level:.2f} s each; RHS time = cycles/RHS ({cyc:.2f}, {src}) x "
+                      f"ell ({cfg.ell}) x level time (validate/poly/true-residual MVs not charged: favours the CPU)",
+            "cpu_model": cpu_model()}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} cores)"
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args):
+    from paper_1604_06043_b200 import problems as pb
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    if not REF_LIB.exists():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmstab_ref.so not built"}))
+        return
+    cfg = pb.config(args.config, grid=args.grid)
+    A = cfg.matrix()
+    lib, op, h = ref_sampler(cfg, A)
+    for _ in range(args.warmup):
+        lib.dll.mstab_ref_sample_step(h)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        lib.dll.mstab_ref_sample_step(h)
+    dt = time.perf_counter() - t0
+    lib.dll.mstab_ref_sample_destroy(h)
+    cyc, src = workload_cycles(cfg, None)
+    value = args.steps / (cyc * cfg.ell * dt)
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded generators, DESIGN.md §5)",
+           "config": dict(workload_desc(cfg, A), parallelism="1 host core (the reference is single-threaded)"),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+                            "sample": f"each step = one level iteration of the reference solve loop on the {cfg.name} "
+                                      f"system; RHS time = cycles/RHS ({cyc:.2f}, {src}) x ell x level time",
+                            "cpu_model": cpu_model()},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--grid", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-levels", type=int, default=2)
+    ap.add_argument("--write-cycles", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -197,6 +197,20 @@ int mstab_result_final_data(const mstab_result* res, mstab_recycle** out);
 int mstab_result_fetched(const mstab_result* res, mstab_recycle** out);
 int mstab_result_handoff(const mstab_result* res, mstab_recycle** out);
 
+/* ---- evidence hooks (no reference counterpart; the reference implementation reports zeros) --- */
+/* Number of kernel launches issued by this library since load. */
+uint64_t mstab_launch_count(void);
+/* Per-launch CUDA-event timing by kernel class, tagged with ALGORITHMIC bytes. */
+typedef struct mstab_kernel_class_stats {
+  int64_t launches;
+  double total_ms;
+  double total_bytes;
+} mstab_kernel_class_stats;
+int mstab_profiling_enable(int32_t on);
+int32_t mstab_profiling_read(mstab_kernel_class_stats* out, int32_t cap); /* returns #classes */
+void mstab_profiling_reset(void);
+const char* mstab_kernel_class_name(int32_t cls);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,6 +36,8 @@ void mstab_gen_euler_rhs(int64_t n, const double* x, const double* f, double dt,
  * U[-1,1) in sorted order; diagonal = 1.1 * row abs-sum; std::mt19937_64(seed). */
 int mstab_gen_banded(int64_t n, int32_t nnz_per_row, int64_t half_width, uint64_t seed,
                      int64_t* row_ptr, int64_t* col_idx, double* values);
+/* make_rhs sinewave (harness.cpp:72-77): v[k-1] = sin(2*pi*k/N), k = 1..N (libm sin). */
+void mstab_gen_sinewave(int64_t n, double* out);
 /* g ~ N(0,1), N draws from std::mt19937_64(seed) + std::normal_distribution<double>. */
 int mstab_gen_normal(uint64_t seed, int64_t count, double* out);
 

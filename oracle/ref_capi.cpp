@@ -343,3 +343,77 @@ int mstab_kernel_arnoldi(mstab_context*, const mstab_operator* op, const double*
 }
 
 }  // extern "C"
+
+// ---- bench reference arm: the reference solve loop advanced one level iteration at a time ------
+// (idrstab.cpp:250-259 split into steps: start + level_iteration(0), level_iteration(1), ...,
+// level_iteration(ell-1) + poly_combination), so a bounded number of steps times the reference's
+// own cycle cost on the workload's real system. Initialised like a fresh solve (make_cut_space +
+// arnoldi_init), outside the timed steps.
+namespace {
+struct RefSample {
+  const mstab_operator* op = nullptr;
+  mstab::DenseMatrix p, u, v;
+  mstab::Vector x, r;
+  mstab::IterationState st;
+  mstab::SolveReport rep;
+  size_t k = 0, ell = 1;
+};
+}  // namespace
+
+extern "C" {
+void* mstab_ref_sample_create(const mstab_operator* op, const double* b, int64_t s, int64_t ell,
+                              uint64_t seed) {
+  try {
+    auto* h = new RefSample();
+    const size_t n = op->m.n_rows;
+    h->op = op;
+    h->ell = (size_t)ell;
+    h->r = to_vec(b, (int64_t)n);
+    h->x = mstab::Vector(n, Complex(0.0));
+    h->p = mstab::make_cut_space(n, (size_t)s, seed, true);
+    std::mt19937_64 rng(seed ^ 0x9e3779b97f4a7c15ull);
+    mstab::ArnoldiResult ai = mstab::arnoldi_init(*op->op, h->r, (size_t)s, rng);
+    h->u = std::move(ai.u);
+    h->v = std::move(ai.v);
+    return h;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// One step; returns 0, or MSTAB_E_* on a breakdown (the sample is then restarted from its x, r).
+int mstab_ref_sample_step(void* handle) {
+  auto* h = static_cast<RefSample*>(handle);
+  return guarded([&] {
+    if (h->k == 0) h->st = mstab::IterationState::start(h->x, h->r, h->u, h->v);
+    try {
+      mstab::level_iteration(h->st, *h->op->op, h->p, h->k, h->rep);
+      if (h->k + 1 == h->ell) {
+        mstab::PolyOut po = mstab::poly_combination(h->st, h->ell);
+        h->x = std::move(po.x);
+        h->r = std::move(po.r);
+        h->u = std::move(po.u);
+        h->v = std::move(po.v);
+        h->k = 0;
+      } else {
+        h->k++;
+      }
+    } catch (...) {
+      h->k = 0;
+      throw;
+    }
+  });
+}
+
+void mstab_ref_sample_destroy(void* handle) { delete static_cast<RefSample*>(handle); }
+}
+
+// ---- evidence hooks: the reference launches no kernels -------------------------------------
+extern "C" {
+uint64_t mstab_launch_count(void) { return 0; }
+int mstab_profiling_enable(int32_t) { return MSTAB_OK; }
+int32_t mstab_profiling_read(mstab_kernel_class_stats*, int32_t) { return 0; }
+void mstab_profiling_reset(void) {}
+const char* mstab_kernel_class_name(int32_t) { return "?"; }
+}

@@ -104,6 +104,18 @@ ABI = [
     ("mstab_result_handoff", C.c_int, [_P, C.POINTER(_P)]),
 ]
 
+class KernelClassStatsC(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("total_ms", C.c_double), ("total_bytes", C.c_double)]
+
+
+ABI += [
+    ("mstab_launch_count", C.c_uint64, []),
+    ("mstab_profiling_enable", C.c_int, [C.c_int32]),
+    ("mstab_profiling_read", C.c_int32, [C.POINTER(KernelClassStatsC), C.c_int32]),
+    ("mstab_profiling_reset", None, []),
+    ("mstab_kernel_class_name", C.c_char_p, [C.c_int32]),
+]
+
 # include/mstab_b200_kernels.h
 KERNEL_ABI = [
     ("mstab_kernel_solve_small", C.c_int, [_P, C.c_int64, _D, _D, _D]),
@@ -120,6 +132,7 @@ GEN_ABI = [
     ("mstab_gen_euler_rhs", None, [C.c_int64, _D, _D, C.c_double, C.c_double, _D]),
     ("mstab_gen_banded", C.c_int, [C.c_int64, C.c_int32, C.c_int64, C.c_uint64, _I64, _I64, _D]),
     ("mstab_gen_normal", C.c_int, [C.c_uint64, C.c_int64, _D]),
+    ("mstab_gen_sinewave", None, [C.c_int64, _D]),
 ]
 
 

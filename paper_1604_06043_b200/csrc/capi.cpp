@@ -385,3 +385,37 @@ int mstab_kernel_arnoldi(mstab_context* ctx, const mstab_operator* op, const dou
 }
 
 }  // extern "C"
+
+// ---- evidence hooks -------------------------------------------------------------------------
+extern "C" {
+
+uint64_t mstab_launch_count(void) { return launch_count(); }
+
+int mstab_profiling_enable(int32_t on) {
+  return guarded([&] {
+    prof_collect();
+    prof_enable(on != 0);
+  });
+}
+
+int32_t mstab_profiling_read(mstab_kernel_class_stats* out, int32_t cap) {
+  prof_collect();
+  KernelClassStats st[kKNumClasses];
+  prof_read(st);
+  const int32_t cnt = std::min<int32_t>(cap, kKNumClasses);
+  for (int32_t i = 0; i < cnt; ++i) out[i] = {(int64_t)st[i].launches, st[i].total_ms, st[i].total_bytes};
+  return kKNumClasses;
+}
+
+void mstab_profiling_reset(void) {
+  prof_collect();
+  prof_reset();
+}
+
+const char* mstab_kernel_class_name(int32_t cls) {
+  static const char* names[kKNumClasses] = {"spmv_ph", "level_update", "rebuild_top", "rebuild_deferred",
+                                            "ls_tsqr", "poly", "prologue", "validate", "other"};
+  return (cls >= 0 && cls < kKNumClasses) ? names[cls] : "?";
+}
+
+}  // extern "C"

@@ -1,6 +1,7 @@
 // generators.cpp — see include/mstab_gen.h. Host-only; builder-defined stand-ins for the
 // BASELINE configs (no external data set is involved).
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <random>
 #include <vector>
@@ -140,6 +141,11 @@ int mstab_gen_banded(int64_t n, int32_t nnz_per_row, int64_t half_width, uint64_
     row_ptr[i + 1] = k;
   }
   return 0;
+}
+
+void mstab_gen_sinewave(int64_t n, double* out) {
+  const double two_pi = 2.0 * 3.141592653589793238462643383279502884;
+  for (int64_t k = 1; k <= n; ++k) out[k - 1] = std::sin(two_pi * static_cast<double>(k) / static_cast<double>(n));
 }
 
 int mstab_gen_normal(uint64_t seed, int64_t count, double* out) {

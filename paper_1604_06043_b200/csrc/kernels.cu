@@ -14,7 +14,11 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <atomic>
 #include <cstdint>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
 
 #include "kernels.h"
 
@@ -837,11 +841,25 @@ __global__ void k_small_solve(int s, const double* m, const double* rhs, double*
   *ok = dev_lu_solve(s, lu, rhs, x) ? 1 : 0;
 }
 
+// Resident CTAs per SM of each kernel, queried once (the occupancy API costs tens of us per
+// call, which would starve the GPU between launches).
+std::mutex g_occ_mu;
+std::unordered_map<const void*, int> g_occ;
+
 template <typename K>
 int occupancy_grid(K kernel, int64_t n, size_t dyn_smem) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, dyn_smem);
-  if (per_sm < 1) per_sm = 1;
+  {
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    auto it = g_occ.find(reinterpret_cast<const void*>(kernel));
+    if (it != g_occ.end()) {
+      per_sm = it->second;
+    } else {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, dyn_smem);
+      if (per_sm < 1) per_sm = 1;
+      g_occ[reinterpret_cast<const void*>(kernel)] = per_sm;
+    }
+  }
   int64_t want = (n + kBlock - 1) / kBlock;
   int64_t cap = (int64_t)g_num_sms * per_sm;
   if (cap > kMaxGrid) cap = kMaxGrid;
@@ -908,6 +926,104 @@ void kernels_init(int device) {
 #undef MSTAB_SET_SMEM
 }
 
+namespace {
+
+// ---- launch accounting -------------------------------------------------------------------------
+std::atomic<uint64_t> g_launch_count{0};
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+  double bytes;
+};
+
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<ProfRec> pending;
+  KernelClassStats stats[kKNumClasses] = {};
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+};
+Profiler g_prof;
+std::mutex g_prof_mu;
+
+// Counts one launch; with profiling on, brackets it with events on its stream.
+struct LaunchScope {
+  cudaStream_t st;
+  int cls;
+  double bytes;
+  cudaEvent_t a = nullptr;
+  LaunchScope(cudaStream_t s, int c, double b) : st(s), cls(c), bytes(b) {
+    g_launch_count.fetch_add(1, std::memory_order_relaxed);
+    if (g_prof.on) {
+      std::lock_guard<std::mutex> lk(g_prof_mu);
+      a = g_prof.get();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~LaunchScope() {
+    if (!a) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t b = g_prof.get();
+    cudaEventRecord(b, st);
+    g_prof.pending.push_back({cls, a, b, bytes});
+  }
+};
+
+inline double vbytes(int64_t n, double vectors) { return 8.0 * (double)n * vectors; }
+inline double csr_bytes(const DevCsr& a) { return 12.0 * (double)a.nnz + 4.0 * (double)(a.n + 1); }
+
+}  // namespace
+
+uint64_t launch_count() { return g_launch_count.load(); }
+
+void prof_enable(bool on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof.on = on;
+  // events are created up front and only read back at prof_collect(), so the timed region pays
+  // one cudaEventRecord per launch boundary and nothing else
+  while (on && g_prof.pool.size() < 65536) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) break;
+    g_prof.pool.push_back(e);
+  }
+}
+
+void prof_collect() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (const ProfRec& r : g_prof.pending) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    KernelClassStats& s = g_prof.stats[r.cls];
+    s.launches++;
+    s.total_ms += ms;
+    s.total_bytes += r.bytes;
+    g_prof.pool.push_back(r.a);
+    g_prof.pool.push_back(r.b);
+  }
+  g_prof.pending.clear();
+}
+
+void prof_read(KernelClassStats* out) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (int i = 0; i < kKNumClasses; ++i) out[i] = g_prof.stats[i];
+}
+
+void prof_reset() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& s : g_prof.stats) s = KernelClassStats{};
+}
+
 int grid_for(int64_t n) {
   int64_t want = (n + kBlock - 1) / kBlock;
   int64_t cap = (int64_t)g_num_sms * 4;
@@ -917,6 +1033,8 @@ int grid_for(int64_t n) {
 
 void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
                     int64_t ld, int s, const double* b, const FinParams& fin, const Reducer& red) {
+  // CSR + gathered x + y + P^H epilogue (+ b for the true-residual form)
+  LaunchScope ls(st, kKSpmv, csr_bytes(a) + vbytes(a.n, 2.0 + s + (b ? 1.0 : 0.0)));
   MSTAB_DISPATCH_S(s, {
     if (b) {
       auto kfn = k_spmv_ph<S, true>;
@@ -932,6 +1050,7 @@ void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y
 
 void launch_level_update(cudaStream_t st, int64_t n, int64_t ld, int s, int k, const double* r_in,
                          double* r_out, const double* vk, DevState* ds) {
+  LaunchScope ls(st, kKLevelUpdate, vbytes(n, s + 2.0));
   MSTAB_DISPATCH_S(s, {
     auto kfn = k_level_update<S>;
     const int grid = occupancy_grid(kfn, n, 0);
@@ -941,6 +1060,7 @@ void launch_level_update(cudaStream_t st, int64_t n, int64_t ld, int s, int k, c
 
 void launch_rebuild_top(cudaStream_t st, int64_t n, int64_t ld, int s, int q, const double* rnext,
                         const double* vk_in, double* vk_out, const double* vk1, DevState* ds) {
+  LaunchScope ls(st, kKRebuildTop, vbytes(n, s + 2.0));
   MSTAB_DISPATCH_S(s, {
     auto kfn = k_rebuild_top<S>;
     const int grid = occupancy_grid(kfn, n, 0);
@@ -952,6 +1072,9 @@ void launch_rebuild_deferred(cudaStream_t st, int64_t n, int64_t ld, int s, int 
                              const double* const* lv_in, double* const* lv_out,
                              const double* const* r_in, double* const* r_out, const double* x_in,
                              double* x_out, DevState* ds) {
+  // reads x, r^(0..k), V^(-1..k); writes x, r^(0..k-1), V^(-1..k-1)
+  LaunchScope ls(st, kKRebuildDeferred,
+                 vbytes(n, (k + 1.0) + 1.0 + (k + 2.0) * s + k + 1.0 + (k + 1.0) * s));
   DeferredArgs a{};
   for (int i = 0; i <= k + 1; ++i) {
     a.lv_in[i] = lv_in[i];
@@ -973,6 +1096,7 @@ void launch_rebuild_deferred(cudaStream_t st, int64_t n, int64_t ld, int s, int 
 void launch_ls(cudaStream_t st, int64_t n, int64_t ld, int ell, int s, const double* const* r,
                const Reducer& red) {
   (void)ld;
+  LaunchScope ls(st, kKLs, vbytes(n, ell + 1.0));
   LsArgs a{};
   for (int i = 0; i <= ell; ++i) a.r[i] = r[i];
   MSTAB_DISPATCH_L(ell, {
@@ -985,6 +1109,8 @@ void launch_ls(cudaStream_t st, int64_t n, int64_t ld, int ell, int s, const dou
 void launch_poly(cudaStream_t st, int64_t n, int64_t ld, int s, int ell, const double* const* lv,
                  double* u_out, double* v_out, const double* const* r, double* r_out,
                  const double* x_in, double* x_out, const double* p, const Reducer& red) {
+  // reads x, r^(0..ell), V^(-1..ell), P; writes x, r, U, V
+  LaunchScope ls(st, kKPoly, vbytes(n, 1.0 + (ell + 1.0) + (ell + 2.0) * s + s + 2.0 + 2.0 * s));
   PolyArgs a{};
   for (int i = 0; i <= ell + 1; ++i) a.lv[i] = lv[i];
   for (int i = 0; i <= ell; ++i) a.r[i] = r[i];
@@ -1004,6 +1130,7 @@ void launch_poly(cudaStream_t st, int64_t n, int64_t ld, int s, int ell, const d
 
 void launch_prologue(cudaStream_t st, int64_t n, int64_t ld, int s, const double* p,
                      const double* v, const double* r, const Reducer& red) {
+  LaunchScope ls(st, kKPrologue, vbytes(n, 2.0 * s + 1.0));
   PolyArgs a{};
   a.lv[1] = v;
   a.r[0] = r;
@@ -1018,6 +1145,7 @@ void launch_prologue(cudaStream_t st, int64_t n, int64_t ld, int s, const double
 
 void launch_validate(cudaStream_t st, const DevCsr& a, const double* p, const double* u,
                      const double* v, int64_t ld, int s, const Reducer& red) {
+  LaunchScope ls(st, kKValidate, csr_bytes(a) + vbytes(a.n, 3.0 * s));
   MSTAB_DISPATCH_S(s, {
     auto kfn = k_validate<S>;
     const size_t sm = gram_smem<S>();
@@ -1028,45 +1156,54 @@ void launch_validate(cudaStream_t st, const DevCsr& a, const double* p, const do
 
 void launch_dots(cudaStream_t st, int64_t n, int64_t ld, const double* a, int na, const double* y,
                  bool with_norm, double* dst, const Reducer& red) {
+  LaunchScope ls(st, kKOther, vbytes(n, na + 1.0));
   const int grid = occupancy_grid(k_dots, n, 0);
   k_dots<<<grid, kBlock, 0, st>>>(n, ld, a, na, y, with_norm ? 1 : 0, dst, red);
 }
 
 void launch_axpy_neg(cudaStream_t st, int64_t n, int64_t ld, const double* a, int na,
                      const double* coef, double* y) {
+  LaunchScope ls(st, kKOther, vbytes(n, na + 2.0));
   const int grid = occupancy_grid(k_axpy_neg, n, 0);
   k_axpy_neg<<<grid, kBlock, 0, st>>>(n, ld, a, na, coef, y);
 }
 
 void launch_div_by_sqrt(cudaStream_t st, int64_t n, const double* x, const double* d2, double* y) {
+  LaunchScope ls(st, kKOther, vbytes(n, 2.0));
   k_div_by_sqrt<<<grid_for(n), kBlock, 0, st>>>(n, x, d2, y);
 }
 
 void launch_mul_inv_sqrt(cudaStream_t st, int64_t n, const double* x, const double* d2, double* y) {
+  LaunchScope ls(st, kKOther, vbytes(n, 2.0));
   k_mul_inv_sqrt<<<grid_for(n), kBlock, 0, st>>>(n, x, d2, y);
 }
 
 void launch_rsub(cudaStream_t st, int64_t n, const double* b, double* y) {
+  LaunchScope ls(st, kKOther, vbytes(n, 3.0));
   k_rsub<<<grid_for(n), kBlock, 0, st>>>(n, b, y);
 }
 
 void launch_vec_stats(cudaStream_t st, int64_t n, const double* x, double* dst, const Reducer& red) {
+  LaunchScope ls(st, kKOther, vbytes(n, 1.0));
   const int grid = occupancy_grid(k_vec_stats, n, 0);
   k_vec_stats<<<grid, kBlock, 0, st>>>(n, x, dst, red);
 }
 
 void launch_euler_rhs(cudaStream_t st, int64_t n, const double* x, const double* f, double dt,
                       double h2, double* b) {
+  LaunchScope ls(st, kKOther, vbytes(n, 3.0));
   k_euler_rhs<<<grid_for(n), kBlock, 0, st>>>(n, x, f, dt, h2, b);
 }
 
 void launch_axpby_chain(cudaStream_t st, int64_t n, const double* x, const double* g, double alpha,
                         double* b) {
+  LaunchScope ls(st, kKOther, vbytes(n, 3.0));
   k_axpby_chain<<<grid_for(n), kBlock, 0, st>>>(n, x, g, alpha, b);
 }
 
 void launch_small_solve(cudaStream_t st, int s, const double* m, const double* rhs, double* x,
                         int32_t* ok) {
+  LaunchScope ls(st, kKOther, 0.0);
   k_small_solve<<<1, 32, 0, st>>>(s, m, rhs, x, ok);
 }
 

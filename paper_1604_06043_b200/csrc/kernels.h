@@ -50,6 +50,33 @@ struct FinParams {
 int grid_for(int64_t n);
 void kernels_init(int device);
 
+// ---- launch accounting (bench evidence) ---------------------------------------------------
+// Every launcher counts its kernel launches. With profiling on, each launch is also bracketed
+// by CUDA events on its stream and tagged with its ALGORITHMIC bytes, so the
+// bench can report per-class average duration and achieved GB/s of the timed region.
+enum KernelClass : int32_t {
+  kKSpmv = 0,
+  kKLevelUpdate,
+  kKRebuildTop,
+  kKRebuildDeferred,
+  kKLs,
+  kKPoly,
+  kKPrologue,
+  kKValidate,
+  kKOther,
+  kKNumClasses
+};
+struct KernelClassStats {
+  uint64_t launches;
+  double total_ms;
+  double total_bytes;
+};
+uint64_t launch_count();
+void prof_enable(bool on);
+void prof_collect();  // folds completed events into the per-class totals (call after a sync)
+void prof_read(KernelClassStats* out);  // kKNumClasses entries
+void prof_reset();
+
 // ---- the Mstab cycle ----------------------------------------------------------------------
 // y = A x, fused partial dots P^H y (s of them) and the finaliser `fin`. When `b` != nullptr the
 // kernel instead writes y = b - A x and also reduces ||y||^2 (true residual refresh).

@@ -41,6 +41,9 @@ struct Context {
   DevPtr partials;      // reduction partials
   CycleStatus* host_status = nullptr;  // pinned
   double* host_scal = nullptr;         // pinned, 64 doubles
+  DevPtr pcache;                       // last make_cut_space result (immutable)
+  int64_t pcache_n = -1, pcache_s = -1;
+  uint64_t pcache_seed = 0;
   cudaStream_t stream() const { return sh->stream; }
   DevState* ds() const { return static_cast<DevState*>(ds_mem->ptr); }
   Reducer reducer() const { return Reducer{partials->d(), ds()}; }

@@ -63,6 +63,13 @@ def normal(seed: int, count: int) -> np.ndarray:
     return out
 
 
+def sinewave(n: int) -> np.ndarray:
+    """make_rhs(Sinewave) of the reference harness (harness.cpp:72-77)."""
+    out = np.empty(n)
+    gen_lib().mstab_gen_sinewave(n, dptr(out))
+    return out
+
+
 def euler_rhs(x: np.ndarray, f: np.ndarray, dt: float, h2: float) -> np.ndarray:
     x = np.ascontiguousarray(x, dtype=np.float64)
     out = np.empty_like(x)

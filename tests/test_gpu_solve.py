@@ -1,0 +1,293 @@
+"""The reference's own solver and recycle test suites (proj/tests/test_solvers.cpp,
+test_recycle.cpp), ported to the drop-in API and run against the B200 library, plus teacher-forced
+parity against the golden sequences written by the reference (tests/golden/seq_small.npz)."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_1604_06043_b200 as m
+from paper_1604_06043_b200 import problems as pb
+
+pytestmark = pytest.mark.gpu
+
+
+def tri(n, a=2.0, b=3.0, c=1.0):
+    return m.CsrMatrix.tridiag(a, b, c, n)
+
+
+def shifted_random(n, shift, seed):
+    """test_solvers.cpp:29-40 (dense-as-CSR); normal draws from the reference's RNG."""
+    g = pb.normal(seed, n * n).reshape(n, n) / np.sqrt(n)
+    return m.CsrMatrix.from_dense(g + shift * np.eye(n))
+
+
+def true_res(op, b, x):
+    return b - op.apply(x)
+
+
+def run_cycles(op, b, s, ell, cycles, seed):
+    """test_solvers.cpp:43-48"""
+    return m.idrstab_solve(op, b, None, m.SolverConfig(s, ell, 1e-30, s + cycles * ell * (s + 1), False, seed))
+
+
+# ---- Idrstab.* (test_solvers.cpp:254-339) ---------------------------------------------------------
+def test_identity_converges_in_one_cycle(gpu_ctx):
+    op = m.CsrOperator(m.CsrMatrix.identity(12), gpu_ctx)
+    b = pb.normal(11, 12)
+    res = m.idrstab_solve(op, b, None, m.SolverConfig(1, 1, 1e-10, 1000, False, 11))
+    assert res.report.status == m.CONVERGED and res.report.cycles == 1
+    assert np.max(np.abs(res.x - b)) <= 1e-10
+
+
+def test_finite_termination_tridiag40(gpu_ctx, golden_kat):
+    op = m.CsrOperator(tri(40), gpu_ctx)
+    for s, bound in ((2, 22), (4, 11)):
+        r = m.idrstab_solve(op, np.ones(40), None, m.SolverConfig(s, 1, 1e-8, 100000, True, 1))
+        assert r.report.status == m.CONVERGED and r.report.cycles <= bound
+        g = golden_kat[f"idr{s}_counters"]
+        assert [r.report.cycles, r.report.h_mv, r.report.h_mv_aux, r.report.h_rd] == list(g[:4])
+        assert np.linalg.norm(r.x - golden_kat[f"idr{s}_x"]) <= 1e-6 * np.linalg.norm(golden_kat[f"idr{s}_x"])
+
+
+def test_counter_law_and_overshoot_bound(gpu_ctx):
+    op = m.CsrOperator(tri(200), gpu_ctx)
+    b = np.ones(200)
+    for s in (2, 4):
+        for ell in (1, 2):
+            res = run_cycles(op, b, s, ell, 5, 3)
+            assert res.report.cycles == 5
+            assert res.report.h_mv == s + 5 * ell * (s + 1)
+            assert res.report.h_rd == 5 * ell * s
+            assert res.report.h_mv_aux == 0
+    cfg = m.SolverConfig(3, 2, 1e-30, 50, False, 3)
+    res = m.idrstab_solve(op, b, None, cfg)
+    assert res.report.status == m.MAXMV
+    assert res.report.h_mv <= cfg.max_mv + (3 + 1) * 2
+
+
+def test_breakdown_surfaces_with_partial_report(gpu_ctx):
+    op = m.CsrOperator(tri(8, 0.0, 0.0, 0.0), gpu_ctx)
+    res = m.idrstab_solve(op, np.ones(8), None, m.SolverConfig(2, 1, 1e-8, 1000, False, 1))
+    assert res.report.status == m.BREAKDOWN
+    assert res.report.breakdown_reason
+    assert len(res.report.residual_history) >= 1
+
+
+def test_deterministic_for_fixed_seed(gpu_ctx):
+    op = m.CsrOperator(shifted_random(16, 3.0, 12), gpu_ctx)
+    b = pb.normal(12, 16)
+    cfg = m.SolverConfig(2, 2, 1e-10, 1000, False, 99)
+    r1, r2 = m.idrstab_solve(op, b, None, cfg), m.idrstab_solve(op, b, None, cfg)
+    h1 = [h.resnorm for h in r1.report.residual_history]
+    h2 = [h.resnorm for h in r2.report.residual_history]
+    assert h1 == h2
+
+
+def test_recurrence_residual_tracks_true_residual(gpu_ctx):
+    op = m.CsrOperator(tri(40), gpu_ctx)
+    b = np.ones(40)
+    for cycles in (4, 10, 16):
+        res = run_cycles(op, b, 2, 1, cycles, 1)
+        truth = np.linalg.norm(true_res(op, b, res.x))
+        assert abs(truth - res.report.final_resnorm) <= 1e-6 * np.linalg.norm(b)
+
+
+def test_config_and_input_errors(gpu_ctx):
+    op = m.CsrOperator(tri(10), gpu_ctx)
+    with pytest.raises(m.ConfigError):
+        m.idrstab_solve(op, np.ones(10), None, m.SolverConfig(0, 1))
+    with pytest.raises(m.ConfigError):
+        m.idrstab_solve(op, np.ones(10), None, m.SolverConfig(2, 1, 0.0))
+    with pytest.raises(m.ConfigError):
+        m.idrstab_solve(op, np.ones(10), None, m.SolverConfig(2, 1, 1e-8, 2))
+    with pytest.raises(m.DimensionMismatch):
+        m.idrstab_solve(op, np.ones(9), None, m.SolverConfig(2, 1))
+    bad = np.ones(10)
+    bad[3] = np.nan
+    with pytest.raises(m.Error):
+        m.idrstab_solve(op, bad, None, m.SolverConfig(2, 1))
+    with pytest.raises(m.Error):  # fresh solve with a zero start vector (idrstab.cpp:50)
+        m.idrstab_solve(op, np.zeros(10), None, m.SolverConfig(2, 1))
+    with pytest.raises(m.ConfigError):
+        m.FetchPolicy.at_cycle(0)
+
+
+def test_nonzero_initial_guess_costs_one_aux_mv(gpu_ctx, ref_ctx):
+    A = tri(60)
+    b = pb.sinewave(60)
+    x0 = np.full(60, 0.1)
+    cfg = m.SolverConfig(2, 2, 1e-10, 10000, False, 5)
+    g = m.idrstab_solve(m.CsrOperator(A, gpu_ctx), b, x0, cfg)
+    r = m.idrstab_solve(m.CsrOperator(A, ref_ctx), b, x0, cfg)
+    assert g.report.h_mv_aux == r.report.h_mv_aux == 1
+    assert abs(g.report.cycles - r.report.cycles) <= 2
+    assert np.linalg.norm(g.x - r.x) <= 1e-6 * np.linalg.norm(r.x)
+
+
+# ---- Mstab.* (test_solvers.cpp:341-409) ------------------------------------------------------------
+def test_mstab_finite_termination_after_fetch(gpu_ctx):
+    op = m.CsrOperator(tri(40), gpu_ctx)
+    b1, b2 = np.ones(40), pb.sinewave(40)
+    for s, cyc, bound in ((2, 19, 12), (4, 9, 5)):
+        cfg = m.SolverConfig(s, 1, 1e-8, 100000, True, 1)
+        donor = m.idrstab_solve(op, b1, None, cfg, None, m.FetchPolicy.at_cycle(cyc))
+        assert donor.fetched is not None and donor.fetched.level_J == cyc
+        r = m.mstab_solve(op, b2, None, cfg, donor.fetched)
+        assert r.report.status == m.CONVERGED and r.report.cycles <= bound
+
+
+def test_mstab_recycle_data_is_degree_agnostic(gpu_ctx):
+    op = m.CsrOperator(tri(40), gpu_ctx)
+    b1, b2 = np.ones(40), pb.sinewave(40)
+    for dl in (1, 2):
+        donor = m.idrstab_solve(op, b1, None, m.SolverConfig(4, dl, 1e-8, 100000, False, 1), None,
+                                m.FetchPolicy.at_cycle(8 if dl == 1 else 4))
+        assert donor.fetched.level_J == 8
+        for ul in (1, 2):
+            r = m.mstab_solve(op, b2, None, m.SolverConfig(4, ul, 1e-8, 100000, False, 1), donor.fetched)
+            assert r.report.status == m.CONVERGED
+            assert r.report.residual_history[-1].level <= (13 if ul == 1 else 14)
+
+
+def test_mstab_counter_laws_with_recycle_head_start(gpu_ctx):
+    op = m.CsrOperator(tri(200), gpu_ctx)
+    b1, b2 = np.ones(200), pb.sinewave(200)
+    s, J = 2, 5
+    donor = m.idrstab_solve(op, b1, None, m.SolverConfig(s, 1, 1e-30, s + 20 * (s + 1), False, 3), None,
+                            m.FetchPolicy.at_cycle(J))
+    for j in (1, 4, 9):
+        r = m.mstab_solve(op, b2, None, m.SolverConfig(s, 1, 1e-30, j * (s + 1), False, 3), donor.fetched)
+        assert r.report.cycles == j
+        assert r.report.h_mv == j * (s + 1)
+        assert r.report.h_rd == j * s + J * (s - 1)
+
+
+# ---- Recycle.* (test_recycle.cpp) ------------------------------------------------------------------
+def donor_run(op, fetch_cycle):
+    return m.idrstab_solve(op, np.ones(op.size()), None, m.SolverConfig(2, 1, 1e-8, 100000, False, 21), None,
+                           m.FetchPolicy.at_cycle(fetch_cycle))
+
+
+def test_fetch_is_deterministic_deep_copy(gpu_ctx):
+    op = m.CsrOperator(tri(30), gpu_ctx)
+    r1, r2 = donor_run(op, 4), donor_run(op, 4)
+    assert r1.fetched.level_J == 4
+    assert np.array_equal(r1.fetched.u, r2.fetched.u) and np.array_equal(r1.fetched.v, r2.fetched.v)
+
+
+def test_fetched_data_satisfies_image_invariant(gpu_ctx):
+    op = m.CsrOperator(tri(30), gpu_ctx)
+    vr = m.validate(donor_run(op, 4).fetched, op)
+    assert vr.max_deviation <= 1e-8
+
+
+def test_half_tolerance_triggers_at_log_midpoint(gpu_ctx):
+    op = m.CsrOperator(tri(40), gpu_ctx)
+    b = np.ones(40)
+    res = m.idrstab_solve(op, b, None, m.SolverConfig(2, 1, 1e-8, 100000, False, 21), None,
+                          m.FetchPolicy.at_half_tolerance())
+    gate = 1e-4 * np.linalg.norm(b)
+    first = next(h.level for h in res.report.residual_history if h.resnorm <= gate)
+    assert res.fetched.level_J == first
+
+
+def test_validate_rejects_perturbed_and_foreign_data(gpu_ctx):
+    op = m.CsrOperator(tri(30), gpu_ctx)
+    f = donor_run(op, 4).fetched
+    v = f.v.copy()
+    v[7, 1] += 1e-3
+    pert = m.fetch(f.p, f.u, v, f.omega_history, f.level_J, f.matrix_fingerprint, gpu_ctx)
+    with pytest.raises(m.StaleData):
+        m.validate(pert, op)
+    other = m.CsrOperator(tri(30, 2.0, 3.1, 1.0), gpu_ctx)
+    with pytest.raises(m.FingerprintMismatch):
+        m.validate(f, other)
+    with pytest.raises(m.StaleData):  # omega history length disagrees with the level
+        m.validate(m.fetch(f.p, f.u, f.v, [0.5], f.level_J, f.matrix_fingerprint, gpu_ctx), op)
+
+
+def test_save_load_round_trips_bit_exact(gpu_ctx, tmp_path):
+    op = m.CsrOperator(tri(30), gpu_ctx)
+    f = donor_run(op, 4).fetched
+    path = tmp_path / "data.mrd"
+    m.save(f, path)
+    back = m.load(path, gpu_ctx)
+    assert (back.level_J, back.s, back.matrix_fingerprint) == (f.level_J, f.s, f.matrix_fingerprint)
+    assert np.array_equal(back.omega_history, f.omega_history)
+    for a, b in ((back.p, f.p), (back.u, f.u), (back.v, f.v)):
+        assert np.array_equal(a, b)
+
+
+def test_reference_mrd_interop(gpu_ctx, ref_ctx, tmp_path):
+    """A .mrd written by the reference loads here, and ours loads in the reference, byte-identical."""
+    from conftest import GOLDEN
+    src = GOLDEN / "donor_tridiag30.mrd"
+    d = m.load(src, gpu_ctx)
+    out = tmp_path / "ours.mrd"
+    m.save(d, out)
+    assert out.read_bytes() == src.read_bytes()
+    back = m.load(out, ref_ctx)
+    assert back.level_J == 4 and np.array_equal(back.u, d.u)
+
+
+def test_truncated_file_rejected(gpu_ctx, tmp_path):
+    op = m.CsrOperator(tri(30), gpu_ctx)
+    path = tmp_path / "trunc.mrd"
+    m.save(donor_run(op, 4).fetched, path)
+    os.truncate(path, path.stat().st_size - 9)
+    with pytest.raises(m.ParseError):
+        m.load(path, gpu_ctx)
+    junk = tmp_path / "junk.mrd"
+    junk.write_bytes(b"not a recycle file")
+    with pytest.raises(m.ParseError):
+        m.load(junk, gpu_ctx)
+
+
+def test_reloaded_data_reproduces_mstab_trajectory(gpu_ctx, tmp_path):
+    op = m.CsrOperator(tri(40), gpu_ctx)
+    donor = donor_run(op, 10)
+    path = tmp_path / "chain.mrd"
+    m.save(donor.fetched, path)
+    reloaded = m.load(path, gpu_ctx)
+    b2 = pb.sinewave(40)
+    cfg = m.SolverConfig(2, 1, 1e-8, 100000, False, 21)
+    a = m.mstab_solve(op, b2, None, cfg, donor.fetched)
+    b = m.mstab_solve(op, b2, None, cfg, reloaded)
+    ha = [h.resnorm for h in a.report.residual_history]
+    hb = [h.resnorm for h in b.report.residual_history]
+    assert len(ha) == len(hb)
+    for x, y in zip(ha, hb):
+        assert abs(x - y) <= 1e-12 * max(x, 1e-300)
+
+
+# ---- teacher-forced parity against the reference's golden sequences --------------------------------
+@pytest.mark.parametrize("key", ["c1_16_", "c1_32_", "c2_8_", "c3_2048_"])
+def test_golden_sequences_teacher_forced(gpu_ctx, golden_seq, key):
+    g = golden_seq
+    n = len(g[key + "rp"]) - 1
+    A = m.CsrMatrix(n, n, g[key + "rp"], g[key + "ci"], g[key + "va"])
+    op = m.CsrOperator(A, gpu_ctx)
+    cfg = pb.config(key.split("_")[0])
+    sc = m.SolverConfig(cfg.s, cfg.ell, 1e-8, 100000, False, 0)
+    for i in range(int(g[key + "count"][0])):
+        k = f"{key}{i}_"
+        b = g[k + "b"]
+        rec = None
+        if (k + "in_meta") in g:
+            rec = m.fetch(g[k + "in_p"], g[k + "in_u"], g[k + "in_v"], g[k + "in_omega"], int(g[k + "in_meta"][0]),
+                          int(g[k + "in_fp"][0]), gpu_ctx)
+            if (k + "stale") in g:
+                with pytest.raises(m.StaleData):
+                    m.validate(rec, op)
+                rec = None
+        r = m.idrstab_solve(op, b, None, sc, rec, m.FetchPolicy.at_half_tolerance())
+        cyc, hmv, hmv_aux, hrd, status = (int(v) for v in g[k + "counters"])
+        assert r.report.status == m.CONVERGED and status == 0
+        assert abs(r.report.cycles - cyc) <= 2
+        assert r.report.h_mv_aux == hmv_aux
+        xr = g[k + "x"]
+        assert np.linalg.norm(r.x - xr) <= 1e-6 * np.linalg.norm(xr)
+        tr_ref = np.linalg.norm(true_res(op, b, xr)) / np.linalg.norm(b)
+        tr = np.linalg.norm(true_res(op, b, r.x)) / np.linalg.norm(b)
+        assert tr <= max(1e-8, 1.5 * tr_ref)
