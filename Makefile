@@ -15,8 +15,9 @@ CXXFLAGS := -O3 -std=c++20 -fPIC -ffp-contract=off -Wall -Wextra -I$(CUDA_HOME)/
 
 HOST_SRCS := $(CSRC)/solver.cpp $(CSRC)/capi.cpp $(CSRC)/host_util.cpp
 HOST_OBJS := $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.o,$(HOST_SRCS))
-CU_OBJS := $(BUILD)/kernels.o
-HEADERS := $(wildcard $(CSRC)/*.h) include/mstab_b200.h
+CU_SRCS := $(CSRC)/kspmv.cu $(CSRC)/klevel.cu $(CSRC)/kls.cu $(CSRC)/kpoly.cu $(CSRC)/kmisc.cu
+CU_OBJS := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
+HEADERS := $(wildcard $(CSRC)/*.h) $(CSRC)/kcommon.cuh include/mstab_b200.h
 
 all: product gen oracle ref
 
@@ -26,7 +27,7 @@ gen: $(PKG)/libmstab_gen.so
 $(BUILD):
 	mkdir -p $(BUILD)
 
-$(BUILD)/kernels.o: $(CSRC)/kernels.cu $(HEADERS) | $(BUILD)
+$(BUILD)/%.o: $(CSRC)/%.cu $(HEADERS) | $(BUILD)
 	$(NVCC) $(NVCCFLAGS) -c $< -o $@
 
 $(BUILD)/%.o: $(CSRC)/%.cpp $(HEADERS) | $(BUILD)
@@ -44,8 +45,8 @@ oracle:
 ref:
 	@if [ -d /root/reference/proj/core/src ]; then $(MAKE) -C oracle ref; else echo "reference absent: using prebuilt oracle/_ref"; fi
 
-sass: $(BUILD)/kernels.o
-	$(CUDA_HOME)/bin/cuobjdump -sass $< > $(BUILD)/kernels.sass
+sass: $(CU_OBJS)
+	for o in $(CU_OBJS); do $(CUDA_HOME)/bin/cuobjdump -sass $$o; done > $(BUILD)/kernels.sass
 
 clean:
 	rm -rf $(BUILD) $(PKG)/*.so

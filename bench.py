@@ -129,6 +129,7 @@ class Sequence:
         m, t = self.m, self.torch
         b = self.b_d if self.device_mode else self.b_h
         restarted = False
+        t0 = time.perf_counter()
         try:
             r = m.idrstab_solve(self.op, b, None, self.sc, self.rec, self.fp)
         except m.StaleData:
@@ -137,17 +138,20 @@ class Sequence:
             r = m.idrstab_solve(self.op, b, None, self.sc, None, self.fp)
         rep = r._rep
         self.log.append({"cycles": int(rep.cycles), "status": int(rep.status), "restart": restarted,
-                         "relres": float(rep.final_resnorm / rep.bnorm) if rep.bnorm else 0.0})
+                         "relres": float(rep.final_resnorm / rep.bnorm) if rep.bnorm else 0.0,
+                         "solve_ms": round(1e3 * (time.perf_counter() - t0), 3)})
         self.rec = r.handoff()
         c = self.cfg
+        dll, h = self.ctx.lib.dll, self.ctx.h
+        # b_{i+1} = h^2 (x_i/dt + f) through the C-ABI harness helper (same rounding on both paths)
         if self.device_mode:
             r.x_into(self.x_d)  # D2D on the solver stream (synchronised)
-            self.b_d = c.h2 * (self.x_d / c.dt + self.f_d)  # b_{i+1} = h^2 (x_i/dt + f), same rounding order
-            t.cuda.current_stream().synchronize()
+            dll.mstab_harness_euler_rhs(h, c.N, self.x_d.data_ptr(), self.f_d.data_ptr(), c.dt, c.h2,
+                                        self.b_d.data_ptr(), 1)
         else:
             r.x_into(self.x_h)  # D2H into pinned host memory
-            from paper_1604_06043_b200 import problems as pb
-            self.b_h[:] = pb.euler_rhs(self.x_h, self.f, c.dt, c.h2)
+            dll.mstab_harness_euler_rhs(h, c.N, self.x_h.ctypes.data, self.f.ctypes.data, c.dt, c.h2,
+                                        self.b_h.ctypes.data, 0)
         return r
 
 
@@ -189,7 +193,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     ctx.synchronize()
     lib.dll.mstab_profiling_reset()
-    lib.dll.mstab_profiling_enable(1)
+    lib.dll.mstab_profiling_enable(1 if args.profile == "timed" else 0)
     l0 = lib.dll.mstab_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -199,13 +203,18 @@ def run_b200(args):
         ev1.record(stream)
         ev1.synchronize()
     launches = int(lib.dll.mstab_launch_count() - l0)
+    if args.profile == "after":  # per-kernel events on K more steps of the same sequence
+        lib.dll.mstab_profiling_enable(1)
+        for _ in range(args.steps):
+            seq.step()
+        ctx.synchronize()
     lib.dll.mstab_profiling_enable(0)
     stats = (_capi.KernelClassStatsC * 16)()
     ncls = lib.dll.mstab_profiling_read(stats, 16)
     ms = ev0.elapsed_time(ev1)
     barrier()
     ms_max = max_over_ranks(ms)
-    timed = seq.log[args.warmup:]
+    timed = seq.log[args.warmup:args.warmup + args.steps]
     value = world * args.steps / (ms_max / 1e3)
 
     # ---- e2e: host buffers through the C-ABI --------------------------------------------------
@@ -222,7 +231,7 @@ def run_b200(args):
     e1.synchronize()
     ems = max_over_ranks(e0.elapsed_time(e1))
     e2e = {"value": world * args.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * N,
-           "d2h_bytes_per_step": 8 * N}
+           "d2h_bytes_per_step": 8 * N, "per_rhs": seq_h.log[args.warmup:args.warmup + args.steps]}
 
     # ---- per-kernel roofline of the timed region ---------------------------------------------
     hbm, hbm_src = peaks()
@@ -380,6 +389,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-levels", type=int, default=2)
     ap.add_argument("--write-cycles", action="store_true")
+    ap.add_argument("--profile", default="timed", choices=["timed", "after", "off"],  # graphs: events are nodes
+                    help="per-kernel CUDA events inside the timed region (default) or on K extra steps")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -197,6 +197,15 @@ int mstab_result_final_data(const mstab_result* res, mstab_recycle** out);
 int mstab_result_fetched(const mstab_result* res, mstab_recycle** out);
 int mstab_result_handoff(const mstab_result* res, mstab_recycle** out);
 
+/* ---- sequence-driver helpers (the caller side of the path: run_sequence's RHS rules) ------- */
+/* b = h2 * (x / dt + f) (implicit-Euler chain of the BASELINE conv-diff configs) and
+ * b = x + alpha * g (banded-random chain). mem = DEVICE runs on the context stream (synchronised);
+ * HOST loops on the host. Both evaluate in exactly this rounding order. */
+int mstab_harness_euler_rhs(mstab_context* ctx, int64_t n, const double* x, const double* f,
+                            double dt, double h2, double* b, int32_t mem);
+int mstab_harness_axpby(mstab_context* ctx, int64_t n, const double* x, const double* g,
+                        double alpha, double* b, int32_t mem);
+
 /* ---- evidence hooks (no reference counterpart; the reference implementation reports zeros) --- */
 /* Number of kernel launches issued by this library since load. */
 uint64_t mstab_launch_count(void);

@@ -30,6 +30,14 @@ int mstab_kernel_cut_space(mstab_context* ctx, int64_t n, int64_t s, uint64_t se
 int mstab_kernel_arnoldi(mstab_context* ctx, const mstab_operator* op, const double* r0, int64_t s,
                          uint64_t rng_seed, double* u, double* v, int64_t* mv_cost);
 
+/* Micro-benchmark of one kernel class of the cycle on synthetic data shaped like `op` with
+ * (s, ell): `iters` back-to-back launches timed with CUDA events; *us = mean microseconds per
+ * launch, *bytes = algorithmic bytes per launch. kind: 0 SpMV + P^H + LU finalize, 1 top
+ * rebuild, 2 level update, 3 deferred levels (k = ell-1), 4 poly_combination, 5 least squares.
+ * (Reference implementation: MSTAB_E_CONFIG.) */
+int mstab_kernel_bench(mstab_context* ctx, const mstab_operator* op, int32_t kind, int64_t s,
+                       int64_t ell, int32_t iters, double* us, double* bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -409,6 +409,32 @@ int mstab_ref_sample_step(void* handle) {
 void mstab_ref_sample_destroy(void* handle) { delete static_cast<RefSample*>(handle); }
 }
 
+// ---- sequence-driver helpers (host only) ---------------------------------------------------------
+extern "C" {
+int mstab_harness_euler_rhs(mstab_context*, int64_t n, const double* x, const double* f, double dt,
+                            double h2, double* b, int32_t mem) {
+  return guarded([&] {
+    host_only(mem);
+    for (int64_t i = 0; i < n; ++i) {
+      const volatile double q = x[i] / dt;
+      const volatile double t = q + f[i];
+      b[i] = h2 * t;
+    }
+  });
+}
+
+int mstab_harness_axpby(mstab_context*, int64_t n, const double* x, const double* g, double alpha,
+                        double* b, int32_t mem) {
+  return guarded([&] {
+    host_only(mem);
+    for (int64_t i = 0; i < n; ++i) {
+      const volatile double t = alpha * g[i];
+      b[i] = x[i] + t;
+    }
+  });
+}
+}
+
 // ---- evidence hooks: the reference launches no kernels -------------------------------------
 extern "C" {
 uint64_t mstab_launch_count(void) { return 0; }
@@ -416,4 +442,10 @@ int mstab_profiling_enable(int32_t) { return MSTAB_OK; }
 int32_t mstab_profiling_read(mstab_kernel_class_stats*, int32_t) { return 0; }
 void mstab_profiling_reset(void) {}
 const char* mstab_kernel_class_name(int32_t) { return "?"; }
+}
+
+extern "C" int mstab_kernel_bench(mstab_context*, const mstab_operator*, int32_t, int64_t, int64_t, int32_t,
+                                  double*, double*) {
+  g_err = "reference implementation: no kernels to benchmark";
+  return MSTAB_E_CONFIG;
 }

@@ -109,6 +109,8 @@ class KernelClassStatsC(C.Structure):
 
 
 ABI += [
+    ("mstab_harness_euler_rhs", C.c_int, [_P, C.c_int64, _P, _P, C.c_double, C.c_double, _P, C.c_int32]),
+    ("mstab_harness_axpby", C.c_int, [_P, C.c_int64, _P, _P, C.c_double, _P, C.c_int32]),
     ("mstab_launch_count", C.c_uint64, []),
     ("mstab_profiling_enable", C.c_int, [C.c_int32]),
     ("mstab_profiling_read", C.c_int32, [C.POINTER(KernelClassStatsC), C.c_int32]),

@@ -386,6 +386,44 @@ int mstab_kernel_arnoldi(mstab_context* ctx, const mstab_operator* op, const dou
 
 }  // extern "C"
 
+// ---- sequence-driver helpers ------------------------------------------------------------------
+extern "C" {
+
+int mstab_harness_euler_rhs(mstab_context* ctx, int64_t n, const double* x, const double* f,
+                            double dt, double h2, double* b, int32_t mem) {
+  return guarded([&] {
+    if (mem == MSTAB_MEM_DEVICE) {
+      bind(ctx);
+      launch_euler_rhs(ctx->impl->stream(), n, x, f, dt, h2, b);
+      ctx->impl->sync();
+    } else {
+      for (int64_t i = 0; i < n; ++i) {
+        const volatile double q = x[i] / dt;
+        const volatile double t = q + f[i];
+        b[i] = h2 * t;
+      }
+    }
+  });
+}
+
+int mstab_harness_axpby(mstab_context* ctx, int64_t n, const double* x, const double* g,
+                        double alpha, double* b, int32_t mem) {
+  return guarded([&] {
+    if (mem == MSTAB_MEM_DEVICE) {
+      bind(ctx);
+      launch_axpby_chain(ctx->impl->stream(), n, x, g, alpha, b);
+      ctx->impl->sync();
+    } else {
+      for (int64_t i = 0; i < n; ++i) {
+        const volatile double t = alpha * g[i];
+        b[i] = x[i] + t;
+      }
+    }
+  });
+}
+
+}  // extern "C"
+
 // ---- evidence hooks -------------------------------------------------------------------------
 extern "C" {
 
@@ -416,6 +454,125 @@ const char* mstab_kernel_class_name(int32_t cls) {
   static const char* names[kKNumClasses] = {"spmv_ph", "level_update", "rebuild_top", "rebuild_deferred",
                                             "ls_tsqr", "poly", "prologue", "validate", "other"};
   return (cls >= 0 && cls < kKNumClasses) ? names[cls] : "?";
+}
+
+int mstab_kernel_bench(mstab_context* ctx, const mstab_operator* op, int32_t kind, int64_t s64,
+                       int64_t ell64, int32_t iters, double* us, double* bytes) {
+  return guarded([&] {
+    bind(ctx);
+    Context& c = *ctx->impl;
+    const Operator& o = *op->impl;
+    const int s = (int)s64, ell = (int)ell64;
+    if (s < 1 || s > kMaxS || ell < 1 || ell > kMaxEll) throw Error(MSTAB_E_CONFIG, "bench: bad s/ell");
+    const int64_t n = o.n, ld = padded_ld(n);
+    cudaStream_t st = c.stream();
+    uint64_t seed = 1;
+    auto vec = [&](int64_t cols) {
+      DevPtr d = c.alloc_vecs(n, cols);
+      launch_fill_hash(st, d->d(), ld * cols, seed++);
+      return d;
+    };
+    DevPtr P = vec(s), b = vec(1);
+    WSet A{vec(1), vec(1), vec(s), vec(s)}, B{vec(1), vec(1), vec(s), vec(s)};
+    std::vector<DevPtr> R(ell + 1), VL(ell + 1);
+    for (int i = 1; i <= ell; ++i) {
+      R[i] = vec(1);
+      VL[i] = vec(s);
+    }
+    // benign small-system state: identity projections, small coefficients, no breakdown
+    DevState hs{};
+    for (int i = 0; i < s; ++i) {
+      hs.Ma[i + i * s] = 1.0;
+      hs.Mn[i + i * s] = 1.0;
+      hs.rhs[i] = hs.g[i] = 1.0;
+      for (int k = 0; k < kMaxEll; ++k) hs.gamma[k * kMaxS + i] = 0.1;
+      for (int q = 0; q < s; ++q) hs.eta[q * s + i] = 0.01;
+    }
+    for (int i = 0; i < kMaxEll; ++i) hs.st.tau[i] = 0.1;
+    cudaMemcpyAsync(c.ds(), &hs, sizeof(DevState), cudaMemcpyHostToDevice, st);
+    const Reducer red = c.reducer();
+    DevState* ds = c.ds();
+    const DevCsr csr = o.csr();
+    const double* lv_in[kMaxEll + 2];
+    double* lv_out[kMaxEll + 2];
+    const double* rin[kMaxEll + 1];
+    double* rout[kMaxEll + 1];
+    const double* rr[kMaxEll + 1];
+    const double* lv[kMaxEll + 2];
+    const int k = ell - 1;
+    lv_in[0] = lv_out[0] = A.U->d();
+    lv_in[1] = lv_out[1] = A.V->d();
+    lv[0] = A.U->d();
+    lv[1] = A.V->d();
+    for (int i = 1; i <= ell; ++i) {
+      lv_in[i + 1] = lv_out[i + 1] = VL[i]->d();
+      lv[i + 1] = VL[i]->d();
+    }
+    rin[0] = rout[0] = A.r->d();
+    rr[0] = A.r->d();
+    for (int i = 1; i <= ell; ++i) {
+      rout[i] = R[i]->d();
+      rin[i] = rr[i] = R[i]->d();
+    }
+    auto launch = [&]() {
+      switch (kind) {
+        case 0: {
+          FinParams f;
+          f.op = kFinRhsEta0;
+          f.s = s;
+          f.ell = ell;
+          launch_spmv_ph(st, csr, A.r->d(), R[1]->d(), P->d(), ld, s, nullptr, f, red);
+          break;
+        }
+        case 1:
+          launch_rebuild_top(st, n, ld, s, s / 2, R[1]->d(), A.V->d(), B.V->d(), VL[1]->d(), ds);
+          break;
+        case 2:
+          launch_level_update(st, n, ld, s, 1, A.r->d(), B.r->d(), A.V->d(), ds);
+          break;
+        case 3:
+          launch_rebuild_deferred(st, n, ld, s, k, lv_in, lv_out, rin, rout, A.x->d(), B.x->d(), ds);
+          break;
+        case 4:
+          launch_poly(st, n, ld, s, ell, lv, B.U->d(), B.V->d(), rr, B.r->d(), A.x->d(), B.x->d(), P->d(), red);
+          break;
+        case 5:
+          launch_ls(st, n, ld, ell, s, rr, red);
+          break;
+        default:
+          throw Error(MSTAB_E_CONFIG, "bench: unknown kind");
+      }
+    };
+    launch();
+    launch();
+    c.sync();
+    prof_collect();
+    KernelClassStats before[kKNumClasses], after[kKNumClasses];
+    prof_read(before);
+    const bool was_on = prof_enabled();
+    prof_enable(true);  // bytes per launch come from the launchers' accounting
+    launch();
+    c.sync();
+    prof_collect();
+    prof_read(after);
+    prof_enable(was_on);
+    double b1 = 0.0;
+    for (int i = 0; i < kKNumClasses; ++i) b1 += after[i].total_bytes - before[i].total_bytes;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    for (int i = 0; i < iters; ++i) launch();
+    cudaEventRecord(e1, st);
+    c.sync();
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (cudaGetLastError() != cudaSuccess) throw Error(MSTAB_E_CUDA, "bench launch failed");
+    *us = 1e3 * ms / iters;
+    *bytes = b1;
+  });
 }
 
 }  // extern "C"

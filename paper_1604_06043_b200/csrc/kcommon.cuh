@@ -1,0 +1,305 @@
+// kcommon.cuh — device helpers and launch plumbing shared by the kernel translation units
+// (kspmv.cu, klevel.cu, kls.cu, kpoly.cu, kmisc.cu). Split per kernel family so the many
+// (s, ell)-templated instantiations compile in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
+#include "kernels.h"
+
+namespace mstab_b200 {
+
+extern int g_num_sms;
+extern std::mutex g_occ_mu;
+extern std::unordered_map<const void*, int> g_occ;
+void kpoly_init();
+
+// Counts one launch; with profiling on, brackets it with CUDA events on its stream (kmisc.cu).
+struct LaunchScope {
+  cudaStream_t st;
+  int cls;
+  double bytes;
+  cudaEvent_t a = nullptr;
+  LaunchScope(cudaStream_t s, int c, double b);
+  ~LaunchScope();
+};
+
+inline double vbytes(int64_t n, double vectors) { return 8.0 * (double)n * vectors; }
+// algorithmic bytes of streaming the matrix once: CSR (int32 col + fp64 value per entry, int32
+// row_ptr) or the DIA slots actually used
+inline double csr_bytes(const DevCsr& a) {
+  if (a.ndiag > 0) return 8.0 * (double)a.ndiag * (double)a.n;
+  return 12.0 * (double)a.nnz + 4.0 * (double)(a.n + 1);
+}
+
+namespace {
+
+constexpr int kSpmvStage = 384;  // CSR entries staged per warp (12 B each: 4.5 KB/warp, 36 KB/CTA)
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double dmax_ref(double acc, double v) {
+  // std::max(acc, v) == (acc < v) ? v : acc  (NaN keeps acc, like the reference)
+  return (acc < v) ? v : acc;
+}
+
+// Per-CTA totals of NS per-thread registers into smem `blk` (deterministic tree).
+template <int NS>
+__device__ void block_totals(const double (&v)[NS], double* blk, double* scratch /*NS*32*/) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NS; ++i) {
+    double t = warp_sum(v[i]);
+    if (lane == 0) scratch[i * 32 + w] = t;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NS; i += blockDim.x) {
+    double acc = 0.0;
+    for (int k = 0; k < nw; ++k) acc += scratch[i * 32 + k];
+    blk[i] = acc;
+  }
+  __syncthreads();
+}
+
+// Writes the CTA's `nslots` totals as partials[slot][cta]; the last CTA to arrive reduces every
+// slot over all CTAs in a fixed order into `red` (smem) and returns true.
+__device__ bool cta_commit(const double* blk, int nslots, double* partials, uint32_t* ticket,
+                           double* red) {
+  __shared__ int s_last;
+  const int G = gridDim.x;
+  for (int i = threadIdx.x; i < nslots; i += blockDim.x)
+    partials[(size_t)i * G + blockIdx.x] = blk[i];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == (uint32_t)(G - 1));
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = w; i < nslots; i += nw) {
+    const double* p = partials + (size_t)i * G;
+    double acc = 0.0;
+    int c = lane;
+    for (; c + 96 < G; c += 128) {
+      const double a0 = __ldcg(p + c), a1 = __ldcg(p + c + 32), a2 = __ldcg(p + c + 64),
+                   a3 = __ldcg(p + c + 96);
+      acc += a0;
+      acc += a1;
+      acc += a2;
+      acc += a3;
+    }
+    for (; c < G; c += 32) acc += __ldcg(p + c);
+    acc = warp_sum(acc);
+    if (lane == 0) red[i] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *ticket = 0u;
+  return true;
+}
+
+// solve_small / LuFactor (kernels.cpp:95-154): partially pivoted LU with the reference's pivot
+// rule (first strictly larger magnitude), singular test |pivot| < 1e-14 * max|M| or max|M| == 0,
+// inverse-multiply elimination and in-order substitutions. Single thread; a is s x s col-major
+// (destroyed). Returns false on a singular pivot.
+__device__ bool dev_lu_solve(int s, double* a, const double* rhs, double* x) {
+  int perm[kMaxS];
+  double scale = 0.0;
+  for (int idx = 0; idx < s * s; ++idx) scale = dmax_ref(scale, fabs(a[idx]));
+  for (int i = 0; i < s; ++i) perm[i] = i;
+  for (int k = 0; k < s; ++k) {
+    int piv = k;
+    double best = fabs(a[k + k * s]);
+    for (int i = k + 1; i < s; ++i) {
+      const double m = fabs(a[i + k * s]);
+      if (m > best) {
+        best = m;
+        piv = i;
+      }
+    }
+    if (best < 1e-14 * scale || scale == 0.0) return false;
+    if (piv != k) {
+      const int t = perm[k];
+      perm[k] = perm[piv];
+      perm[piv] = t;
+      for (int j = 0; j < s; ++j) {
+        const double u = a[k + j * s];
+        a[k + j * s] = a[piv + j * s];
+        a[piv + j * s] = u;
+      }
+    }
+    const double inv = 1.0 / a[k + k * s];
+    for (int i = k + 1; i < s; ++i) {
+      const double m = a[i + k * s] * inv;
+      a[i + k * s] = m;
+      if (m != 0.0)
+        for (int j = k + 1; j < s; ++j) a[i + j * s] = a[i + j * s] - m * a[k + j * s];
+    }
+  }
+  for (int i = 0; i < s; ++i) x[i] = rhs[perm[i]];
+  for (int i = 1; i < s; ++i)
+    for (int j = 0; j < i; ++j) x[i] = x[i] - a[i + j * s] * x[j];
+  for (int i = s - 1; i >= 0; --i) {
+    for (int j = i + 1; j < s; ++j) x[i] = x[i] - a[i + j * s] * x[j];
+    x[i] = x[i] / a[i + i * s];
+  }
+  return true;
+}
+
+__device__ void set_breakdown(DevState* ds, int code, int mv) {
+  ds->st.breakdown = code;
+  ds->st.mv_at_breakdown = mv;
+}
+
+// The dense step after an SpMV reduction, run by ALL threads of the last CTA: the s x s system
+// is staged from global memory into shared memory in parallel (one element per thread; a single
+// thread walking ds->Ma would pay ~s^2 dependent L2 round trips), thread 0 factors and solves in
+// shared memory, and the solution is written back in parallel.
+__device__ void finalize_spmv(const FinParams& f, const double* red, DevState* ds) {
+  __shared__ double lu[kMaxS * kMaxS];
+  __shared__ double vin[kMaxS], vout[kMaxS];
+  __shared__ int ok;
+  const int s = f.s, t = threadIdx.x, nt = blockDim.x;
+  if (f.op == kFinStore) {
+    if (t < s) f.dst[t] = red[t];
+    return;
+  }
+  double* dst = nullptr;
+  int mv = 0;
+  bool solve = true, pending = false;
+  if (f.op == kFinRhsEta0) {  // after step (b) of level k: rhs and eta_0 (msys_0 = P^H V^(k))
+    if (t < s) {
+      ds->rhs[t] = red[t];
+      vin[t] = red[t];
+    }
+    for (int i = t; i < s * s; i += nt) lu[i] = ds->Ma[i];
+    dst = ds->eta;
+    mv = f.k * (s + 1) + 1;
+  } else if (f.op == kFinColEta) {  // after V^(k+1)_q = A v_q^(k)
+    const int q = f.q, k = f.k;
+    if (t < s) {
+      ds->Mn[t + q * s] = red[t];
+      vin[t] = ds->rhs[t];
+    }
+    if (q + 1 < s) {
+      // msys_{q+1} = [P^H V^(k+1)_{0..q}, P^H V^(k)_{q+1..s-1}]  (idrstab.cpp:133-137)
+      for (int i = t; i < s * s; i += nt) {
+        const int c = i / s;
+        lu[i] = (c < q) ? ds->Mn[i] : (c == q ? red[i - c * s] : ds->Ma[i]);
+      }
+      dst = ds->eta + (q + 1) * s;
+      mv = k * (s + 1) + 1 + (q + 1);
+    } else {
+      // level done: Ma := P^H V^(k+1), g := P^H r^(k+1); gamma of level k+1 unless it is the last
+      for (int i = t; i < s * s; i += nt) {
+        const int c = i / s;
+        const double v = (c == q) ? red[i - c * s] : ds->Mn[i];
+        lu[i] = v;
+        ds->Ma[i] = v;
+      }
+      if (t < s) ds->g[t] = ds->rhs[t];
+      if (k + 1 < f.ell) {
+        dst = ds->gamma + (k + 1) * kMaxS;
+        mv = (k + 1) * (s + 1);
+      } else {
+        solve = false;
+      }
+    }
+  } else if (f.op == kFinTrueRes) {  // r = b - A x: resnorm, g, pending gamma_0
+    if (t == 0) ds->st.resnorm = sqrt(red[s]);
+    if (t < s) {
+      ds->g[t] = red[t];
+      vin[t] = red[t];
+    }
+    for (int i = t; i < s * s; i += nt) lu[i] = ds->Ma[i];
+    dst = ds->gamma;
+    pending = true;
+  } else {
+    return;
+  }
+  __syncthreads();
+  if (!solve) return;
+  if (t == 0) ok = dev_lu_solve(s, lu, vin, vout) ? 1 : 0;
+  __syncthreads();
+  if (t < s) dst[t] = vout[t];
+  if (t == 0) {
+    if (pending)
+      ds->st.pending_singular = ok ? 0 : 1;
+    else if (!ok)
+      set_breakdown(ds, kBreakSingular, mv);
+  }
+}
+
+// Resident CTAs per SM of each kernel, queried once (the occupancy API costs tens of us per
+// call, which would starve the GPU between launches).
+
+template <typename K>
+int occupancy_grid(K kernel, int64_t n, size_t dyn_smem) {
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    auto it = g_occ.find(reinterpret_cast<const void*>(kernel));
+    if (it != g_occ.end()) {
+      per_sm = it->second;
+    } else {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, dyn_smem);
+      if (per_sm < 1) per_sm = 1;
+      g_occ[reinterpret_cast<const void*>(kernel)] = per_sm;
+    }
+  }
+  int64_t want = (n + kBlock - 1) / kBlock;
+  int64_t cap = (int64_t)g_num_sms * per_sm;
+  if (cap > kMaxGrid) cap = kMaxGrid;
+  if (want > cap) want = cap;
+  if (want < 1) want = 1;
+  return (int)want;
+}
+
+
+}  // namespace
+
+// ---- dispatch --------------------------------------------------------------------------------
+#define MSTAB_DISPATCH_S(s, ...)                      \
+  switch (s) {                                         \
+    case 1: { constexpr int S = 1; __VA_ARGS__; } break;      \
+    case 2: { constexpr int S = 2; __VA_ARGS__; } break;      \
+    case 3: { constexpr int S = 3; __VA_ARGS__; } break;      \
+    case 4: { constexpr int S = 4; __VA_ARGS__; } break;      \
+    case 5: { constexpr int S = 5; __VA_ARGS__; } break;      \
+    case 6: { constexpr int S = 6; __VA_ARGS__; } break;      \
+    case 7: { constexpr int S = 7; __VA_ARGS__; } break;      \
+    case 8: { constexpr int S = 8; __VA_ARGS__; } break;      \
+    case 9: { constexpr int S = 9; __VA_ARGS__; } break;      \
+    case 10: { constexpr int S = 10; __VA_ARGS__; } break;    \
+    case 11: { constexpr int S = 11; __VA_ARGS__; } break;    \
+    case 12: { constexpr int S = 12; __VA_ARGS__; } break;    \
+    case 13: { constexpr int S = 13; __VA_ARGS__; } break;    \
+    case 14: { constexpr int S = 14; __VA_ARGS__; } break;    \
+    case 15: { constexpr int S = 15; __VA_ARGS__; } break;    \
+    case 16: { constexpr int S = 16; __VA_ARGS__; } break;    \
+    default: break;                                    \
+  }
+
+#define MSTAB_DISPATCH_L(l, ...)                      \
+  switch (l) {                                         \
+    case 1: { constexpr int L = 1; __VA_ARGS__; } break;      \
+    case 2: { constexpr int L = 2; __VA_ARGS__; } break;      \
+    case 3: { constexpr int L = 3; __VA_ARGS__; } break;      \
+    case 4: { constexpr int L = 4; __VA_ARGS__; } break;      \
+    case 5: { constexpr int L = 5; __VA_ARGS__; } break;      \
+    case 6: { constexpr int L = 6; __VA_ARGS__; } break;      \
+    case 7: { constexpr int L = 7; __VA_ARGS__; } break;      \
+    case 8: { constexpr int L = 8; __VA_ARGS__; } break;      \
+    default: break;                                    \
+  }
+
+}  // namespace mstab_b200

@@ -10,7 +10,10 @@
 
 #include "device_state.h"
 
+#include <vector>
+
 typedef struct CUstream_st* cudaStream_t;
+typedef struct CUevent_st* cudaEvent_t;
 
 namespace mstab_b200 {
 
@@ -20,7 +23,15 @@ struct DevCsr {
   const int32_t* row_ptr = nullptr;  // n + 1
   const int32_t* col_idx = nullptr;  // nnz (+ padding)
   const double* values = nullptr;    // nnz (+ padding)
+  // Optional diagonal (DIA) form chosen at upload when the nonzeros lie on few diagonals
+  // (stencils): dia_val[d * dia_ld + row] holds A(row, row + dia_off[d]) (0 where CSR has no
+  // entry), offsets ascending, so accumulating d = 0.. is CSR column order.
+  int32_t ndiag = 0;
+  int64_t dia_ld = 0;
+  const double* dia_val = nullptr;
+  const int32_t* dia_off = nullptr;
 };
+constexpr int kMaxDiag = 64;
 
 // Reduction workspace: `partials` holds at least kMaxGrid * max_slots doubles.
 struct Reducer {
@@ -72,6 +83,18 @@ struct KernelClassStats {
   double total_bytes;
 };
 uint64_t launch_count();
+void count_launches(uint64_t n);  // kernels executed by a CUDA-graph replay
+// Graph-captured profiling: while a capture list is set, launchers record their event pair into
+// it (event-record graph nodes); after each replay the owner folds the list into the totals.
+struct ProfEvent {
+  int32_t cls;
+  cudaEvent_t a, b;
+  double bytes;
+};
+bool prof_enabled();
+void prof_set_capture_list(std::vector<ProfEvent>* list);
+void prof_accumulate(const std::vector<ProfEvent>& list);
+void prof_release(std::vector<ProfEvent>& list);  // return a destroyed graph's events to the pool
 void prof_enable(bool on);
 void prof_collect();  // folds completed events into the per-class totals (call after a sync)
 void prof_read(KernelClassStats* out);  // kKNumClasses entries
@@ -141,6 +164,9 @@ void launch_axpby_chain(cudaStream_t st, int64_t n, const double* x, const doubl
 
 // ---- standalone kernel helpers (parity tests of the dense steps) --------------------------
 // x = solve_small(M, rhs) on the device (single-warp LU, kernels.cpp:95-154); *ok = 1 / 0.
+// Fills count doubles with hash-derived values in [-1, 1) (benchmark operands).
+void launch_fill_hash(cudaStream_t st, double* p, int64_t count, uint64_t seed);
+
 void launch_small_solve(cudaStream_t st, int s, const double* m, const double* rhs, double* x,
                         int32_t* ok);
 

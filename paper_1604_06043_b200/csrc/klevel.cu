@@ -1,0 +1,206 @@
+// klevel.cu — level-iteration kernels: step (a) update, step (c) top rebuild, deferred levels.
+//
+// Compiled with --fmad=false: every a*b+c below rounds the product and the sum separately,
+// exactly like the reference's scalar std::complex<double> loops with zero imaginary parts
+// (g++ -O3 without -mfma). Given identical small-solve inputs, the element-wise
+// kernels (SpMV, level updates, column rebuilds, poly combination) are therefore bit-identical
+// to the reference; only the length-N reductions differ (deterministic trees instead of
+// sequential sums), which is why parity is judged teacher-forced (finding 3).
+//
+// All streaming kernels are HBM-bound; they use persistent grid-stride loops
+// sized to the SM count so each CTA leaves exactly one partial per reduced value, and the last
+// CTA (ticket counter) reduces the partials in a fixed order and runs the dense step that
+// consumes them (s x s LU, Givens-TSQR least squares) without another launch.
+#include "kcommon.cuh"
+
+namespace mstab_b200 {
+
+namespace {
+
+// step (a), top level: r_out = r_in - (sum_c gamma_c V_c)  (gemv then subtract, idrstab.cpp:113-117)
+template <int S>
+__global__ void __launch_bounds__(kBlock) k_level_update(int64_t n, int64_t ld, int k,
+                                                         const double* __restrict__ r_in,
+                                                         double* __restrict__ r_out,
+                                                         const double* __restrict__ vk,
+                                                         DevState* ds) {
+  if (k == 0 && ds->st.pending_singular) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && !ds->st.breakdown) set_breakdown(ds, kBreakSingular, 0);
+    return;
+  }
+  if (ds->st.breakdown) return;
+  double gm[S];
+#pragma unroll
+  for (int c = 0; c < S; ++c) gm[c] = ds->gamma[k * kMaxS + c];
+  // two rows per thread with 16-byte loads (columns are 512-byte aligned: ld % 64 == 0)
+  const int64_t npair = (n + 1) >> 1;
+  for (int64_t pr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pr < npair;
+       pr += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = 2 * pr;
+    if (row + 1 < n) {
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < S; ++c) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(vk + c * ld + row));
+        c0 = c0 + gm[c] * v.x;
+        c1 = c1 + gm[c] * v.y;
+      }
+      const double2 r = *reinterpret_cast<const double2*>(r_in + row);
+      *reinterpret_cast<double2*>(r_out + row) = make_double2(r.x - c0, r.y - c1);
+    } else {
+      double corr = 0.0;
+#pragma unroll
+      for (int c = 0; c < S; ++c) corr = corr + gm[c] * __ldg(vk + c * ld + row);
+      r_out[row] = r_in[row] - corr;
+    }
+  }
+}
+
+// step (c), top level, column q (idrstab.cpp:140-148 at i = k)
+template <int S>
+__global__ void __launch_bounds__(kBlock) k_rebuild_top(int64_t n, int64_t ld, int q,
+                                                        const double* __restrict__ rnext,
+                                                        const double* __restrict__ vk_in,
+                                                        double* __restrict__ vk_out,
+                                                        const double* __restrict__ vk1,
+                                                        DevState* ds) {
+  if (ds->st.breakdown) return;
+  double et[S];
+#pragma unroll
+  for (int c = 0; c < S; ++c) et[c] = ds->eta[q * S + c];
+  const int64_t npair = (n + 1) >> 1;
+  for (int64_t pr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pr < npair;
+       pr += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = 2 * pr;
+    if (row + 1 < n) {
+      const double2 rn = *reinterpret_cast<const double2*>(rnext + row);
+      double n0 = rn.x, n1 = rn.y;
+#pragma unroll
+      for (int c = 0; c < S; ++c) {
+        const double* src = (c < q) ? vk1 : vk_in;
+        const double2 m = *reinterpret_cast<const double2*>(src + c * ld + row);
+        n0 = n0 + (-et[c]) * m.x;
+        n1 = n1 + (-et[c]) * m.y;
+      }
+      *reinterpret_cast<double2*>(vk_out + q * ld + row) = make_double2(n0, n1);
+    } else {
+      double nc = rnext[row];
+#pragma unroll
+      for (int c = 0; c < S; ++c) {
+        const double m = (c < q) ? vk1[c * ld + row] : vk_in[c * ld + row];
+        nc = nc + (-et[c]) * m;
+      }
+      vk_out[q * ld + row] = nc;
+    }
+  }
+}
+
+struct DeferredArgs {
+  const double* lv_in[kMaxEll + 2];
+  double* lv_out[kMaxEll + 2];
+  const double* r_in[kMaxEll + 1];
+  double* r_out[kMaxEll + 1];
+  const double* x_in;
+  double* x_out;
+};
+
+// Deferred lower levels of level k (see kernels.h). Level k is final; levels i = k-1 .. -1 are
+// rebuilt top-down, each needing only level i+1 (final) and level i (being updated in q order).
+template <int S>
+__global__ void __launch_bounds__(kBlock) k_rebuild_deferred(int64_t n, int64_t ld, int k,
+                                                             DeferredArgs a, DevState* ds) {
+  if (ds->st.breakdown) return;
+  __shared__ double et[S * S];
+  __shared__ double gm[S];
+  for (int i = threadIdx.x; i < S * S; i += blockDim.x) et[i] = ds->eta[i];
+  if (threadIdx.x < S) gm[threadIdx.x] = ds->gamma[k * kMaxS + threadIdx.x];
+  __syncthreads();
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    double ln[S], lc[S];
+    const double* top = a.lv_in[k + 1];
+#pragma unroll
+    for (int c = 0; c < S; ++c) ln[c] = top[c * ld + row];
+    double r_above = a.r_in[k][row];
+    for (int i = k - 1; i >= -1; --i) {
+      const double* cur = a.lv_in[i + 1];
+#pragma unroll
+      for (int c = 0; c < S; ++c) lc[c] = cur[c * ld + row];
+      // deferred step (a) for this level (idrstab.cpp:113-121), with the level's pre-rebuild V
+      double corr = 0.0;
+#pragma unroll
+      for (int c = 0; c < S; ++c) corr = corr + gm[c] * lc[c];
+      double ri = 0.0;
+      if (i >= 0) {
+        ri = a.r_in[i][row] - corr;
+        a.r_out[i][row] = ri;
+      } else {
+        a.x_out[row] = a.x_in[row] + corr;
+      }
+      // step (c) at level i for every column q, in q order (idrstab.cpp:140-148)
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        double nc = r_above;
+#pragma unroll
+        for (int c = 0; c < S; ++c) nc = nc + (-et[q * S + c]) * ((c < q) ? ln[c] : lc[c]);
+        lc[q] = nc;
+      }
+      double* out = a.lv_out[i + 1];
+#pragma unroll
+      for (int c = 0; c < S; ++c) {
+        out[c * ld + row] = lc[c];
+        ln[c] = lc[c];
+      }
+      r_above = ri;
+    }
+  }
+}
+
+}  // namespace
+
+void launch_level_update(cudaStream_t st, int64_t n, int64_t ld, int s, int k, const double* r_in,
+                         double* r_out, const double* vk, DevState* ds) {
+  LaunchScope ls(st, kKLevelUpdate, vbytes(n, s + 2.0));
+  MSTAB_DISPATCH_S(s, {
+    auto kfn = k_level_update<S>;
+    const int grid = occupancy_grid(kfn, n, 0);
+    kfn<<<grid, kBlock, 0, st>>>(n, ld, k, r_in, r_out, vk, ds);
+  });
+}
+
+void launch_rebuild_top(cudaStream_t st, int64_t n, int64_t ld, int s, int q, const double* rnext,
+                        const double* vk_in, double* vk_out, const double* vk1, DevState* ds) {
+  LaunchScope ls(st, kKRebuildTop, vbytes(n, s + 2.0));
+  MSTAB_DISPATCH_S(s, {
+    auto kfn = k_rebuild_top<S>;
+    const int grid = occupancy_grid(kfn, n, 0);
+    kfn<<<grid, kBlock, 0, st>>>(n, ld, q, rnext, vk_in, vk_out, vk1, ds);
+  });
+}
+
+void launch_rebuild_deferred(cudaStream_t st, int64_t n, int64_t ld, int s, int k,
+                             const double* const* lv_in, double* const* lv_out,
+                             const double* const* r_in, double* const* r_out, const double* x_in,
+                             double* x_out, DevState* ds) {
+  // reads x, r^(0..k), V^(-1..k); writes x, r^(0..k-1), V^(-1..k-1)
+  LaunchScope ls(st, kKRebuildDeferred,
+                 vbytes(n, (k + 1.0) + 1.0 + (k + 2.0) * s + k + 1.0 + (k + 1.0) * s));
+  DeferredArgs a{};
+  for (int i = 0; i <= k + 1; ++i) {
+    a.lv_in[i] = lv_in[i];
+    a.lv_out[i] = lv_out[i];
+  }
+  for (int i = 0; i <= k; ++i) {
+    a.r_in[i] = r_in[i];
+    a.r_out[i] = r_out[i];
+  }
+  a.x_in = x_in;
+  a.x_out = x_out;
+  MSTAB_DISPATCH_S(s, {
+    auto kfn = k_rebuild_deferred<S>;
+    const int grid = occupancy_grid(kfn, n, 0);
+    kfn<<<grid, kBlock, 0, st>>>(n, ld, k, a, ds);
+  });
+}
+
+}  // namespace mstab_b200

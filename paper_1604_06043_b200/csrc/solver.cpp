@@ -9,9 +9,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 
@@ -113,15 +115,6 @@ DevPtr copy_block(Context& ctx, const DevPtr& src, int64_t n, int64_t cols) {
   CUDA_OK(cudaMemcpyAsync(dst->ptr, src->ptr, sizeof(double) * (size_t)padded_ld(n) * cols,
                           cudaMemcpyDeviceToDevice, ctx.stream()));
   return dst;
-}
-
-// Upload (or device-copy) an N-vector into a fresh padded device vector.
-DevPtr to_device(Context& ctx, const double* src, int64_t n, int mem) {
-  DevPtr d = ctx.alloc_vecs(n, 1);
-  CUDA_OK(cudaMemcpyAsync(d->ptr, src, sizeof(double) * n,
-                          mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                          ctx.stream()));
-  return d;
 }
 
 // Plain SpMV through the fused kernel (s = 1, dot with x discarded).
@@ -228,11 +221,6 @@ void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s, uin
 
 namespace {
 
-struct WSet {
-  DevPtr x, r, U, V;
-  bool ro = false;  // U/V alias an immutable RecycleData
-};
-
 // One outer cycle: ell level iterations + poly_combination, S -> D (idrstab.cpp:250-259).
 void enqueue_cycle(Context& ctx, const Operator& op, const double* P, int s, int ell,
                    const WSet& S, const WSet& D, const std::vector<DevPtr>& R,
@@ -321,7 +309,9 @@ std::shared_ptr<Operator> make_operator(Context& ctx, int64_t n, const int64_t* 
     }
   }
   if (nnz >= (int64_t(1) << 31)) throw Error(MSTAB_E_CONFIG, "b200: nnz >= 2^31 not supported (int32 indices)");
+  static std::atomic<uint64_t> next_uid{1};
   auto op = std::make_shared<Operator>();
+  op->uid = next_uid.fetch_add(1);
   op->n = n;
   op->nnz = nnz;
   op->fingerprint = fnv_csr_fingerprint(n, row_ptr, col_idx, values, nnz);
@@ -336,6 +326,43 @@ std::shared_ptr<Operator> make_operator(Context& ctx, int64_t n, const int64_t* 
   CUDA_OK(cudaMemcpyAsync(op->ci->ptr, ci32.data(), sizeof(int32_t) * (nnz + 32), cudaMemcpyHostToDevice, st));
   CUDA_OK(cudaMemsetAsync(op->val->ptr, 0, sizeof(double) * (nnz + 32), st));
   CUDA_OK(cudaMemcpyAsync(op->val->ptr, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+  // DIA form when the nonzeros sit on at most kMaxDiag diagonals filled to >= 2/3: no column
+  // indices to stream and contiguous x gathers. Slots without a CSR entry hold +0.0, so the SpMV
+  // (0*x adds nothing) stays equal to the CSR-order accumulation.
+  if (n > 0 && nnz > 0 && std::getenv("MSTAB_NO_DIA") == nullptr) {
+    std::vector<int64_t> offs;
+    bool ok = true;
+    for (int64_t i = 0; i < n && ok; ++i)
+      for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+        const int64_t o = col_idx[k] - i;
+        if (std::find(offs.begin(), offs.end(), o) == offs.end()) {
+          offs.push_back(o);
+          if ((int)offs.size() > kMaxDiag) {
+            ok = false;
+            break;
+          }
+        }
+      }
+    if (ok && (double)offs.size() * (double)n <= 1.5 * (double)nnz) {
+      std::sort(offs.begin(), offs.end());
+      const int nd = (int)offs.size();
+      const int64_t ld = padded_ld(n);
+      std::vector<double> dv((size_t)nd * ld, 0.0);
+      std::vector<int32_t> off32(offs.begin(), offs.end());
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+          const int d = (int)(std::lower_bound(offs.begin(), offs.end(), col_idx[k] - i) - offs.begin());
+          dv[(size_t)d * ld + i] = values[k];
+        }
+      op->ndiag = nd;
+      op->dia_ld = ld;
+      op->dia_val = ctx.alloc(sizeof(double) * dv.size());
+      op->dia_off = ctx.alloc(sizeof(int32_t) * nd);
+      CUDA_OK(cudaMemcpyAsync(op->dia_val->ptr, dv.data(), sizeof(double) * dv.size(), cudaMemcpyHostToDevice, st));
+      CUDA_OK(cudaMemcpyAsync(op->dia_off->ptr, off32.data(), sizeof(int32_t) * nd, cudaMemcpyHostToDevice, st));
+      ctx.sync();
+    }
+  }
   ctx.sync();
   return op;
 }
@@ -379,6 +406,105 @@ mstab_validation_report validate(Context& ctx, const Recycle& rd, const Operator
   return rep;
 }
 
+void CycleGraph::reset() {
+  if (exec) cudaGraphExecDestroy(exec);
+  exec = nullptr;
+  kernels = 0;
+  if (!prof.empty()) prof_release(prof);
+}
+
+namespace {
+
+Workspace& workspace(Context& ctx, const Operator& op, int s, int ell, bool tres) {
+  auto& w = ctx.ws;
+  if (w && w->op_uid == op.uid && w->n == op.n && w->s == s && w->ell == ell && w->tres == tres) return *w;
+  ctx.sync();
+  w = std::make_unique<Workspace>();
+  w->op_uid = op.uid;
+  w->n = op.n;
+  w->s = s;
+  w->ell = ell;
+  w->tres = tres;
+  const int64_t n = op.n;
+  for (auto& set : w->set) {
+    set.x = ctx.alloc_vecs(n, 1);
+    set.r = ctx.alloc_vecs(n, 1);
+    set.U = ctx.alloc_vecs(n, s);
+    set.V = ctx.alloc_vecs(n, s);
+  }
+  w->R.resize(ell + 1);
+  w->VL.resize(ell + 1);
+  for (int i = 1; i <= ell; ++i) {
+    w->R[i] = ctx.alloc_vecs(n, 1);
+    w->VL[i] = ctx.alloc_vecs(n, s);
+  }
+  w->b = ctx.alloc_vecs(n, 1);
+  w->P = ctx.alloc_vecs(n, s);
+  return *w;
+}
+
+// Everything one cycle enqueues (idrstab.cpp:250-273), set[p] -> set[1-p].
+void enqueue_full_cycle(Context& ctx, const Operator& op, Workspace& w, int p) {
+  const WSet& S = w.set[p];
+  const WSet& D = w.set[1 - p];
+  enqueue_cycle(ctx, op, w.P->d(), w.s, w.ell, S, D, w.R, w.VL);
+  if (w.tres) {  // r = b - A x (idrstab.cpp:268-273)
+    FinParams ft;
+    ft.op = kFinTrueRes;
+    ft.s = w.s;
+    ft.ell = w.ell;
+    launch_spmv_ph(ctx.stream(), op.csr(), D.x->d(), D.r->d(), w.P->d(), padded_ld(op.n), w.s, w.b->d(), ft,
+                   ctx.reducer());
+    check_launch();
+  }
+}
+
+// Runs one cycle: replays the captured graph of parity p (capturing it on first use), or
+// launches the kernels directly when graphs are off.
+void run_cycle(Context& ctx, const Operator& op, Workspace& w, int p) {
+  cudaStream_t st = ctx.stream();
+  if (!ctx.use_graphs) {
+    enqueue_full_cycle(ctx, op, w, p);
+    return;
+  }
+  CycleGraph& g = w.graph[p];
+  const bool prof = prof_enabled();
+  if (g.exec && g.profiled != prof) g.reset();
+  if (!g.exec) {
+    cudaGraph_t graph = nullptr;
+    const uint64_t l0 = launch_count();
+    CUDA_OK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    prof_set_capture_list(prof ? &g.prof : nullptr);
+    try {
+      enqueue_full_cycle(ctx, op, w, p);
+    } catch (...) {
+      prof_set_capture_list(nullptr);
+      cudaStreamEndCapture(st, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    prof_set_capture_list(nullptr);
+    CUDA_OK(cudaStreamEndCapture(st, &graph));
+    g.kernels = launch_count() - l0;
+    cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) throw Error(MSTAB_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    g.profiled = prof;
+    // capture counted the launches once; replays count them below
+    count_launches((uint64_t)0 - g.kernels);
+  }
+  CUDA_OK(cudaGraphLaunch(g.exec, st));
+  count_launches(g.kernels);
+}
+
+DevPtr copy_vec(Context& ctx, const DevPtr& src, int64_t n) {
+  DevPtr d = ctx.alloc_vecs(n, 1);
+  CUDA_OK(cudaMemcpyAsync(d->ptr, src->ptr, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx.stream()));
+  return d;
+}
+
+}  // namespace
+
 std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const double* b_in,
                                        const double* x0_in, int mem, const mstab_solver_config& cfg,
                                        const Recycle* recycle, const mstab_fetch_policy* fetch) {
@@ -394,11 +520,14 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   const int s = (int)cfg.s, ell = (int)cfg.ell;
   const int64_t n = op.n, ld = padded_ld(n);
   cudaStream_t st = ctx.stream();
+  const bool tres = cfg.true_residual_each_cycle != 0;
+  Workspace& w = workspace(ctx, op, s, ell, tres);
   reset_status(ctx);
 
   // b: ensure_finite + bnorm (idrstab.cpp:200, :205)
-  DevPtr b = to_device(ctx, b_in, n, mem);
-  launch_vec_stats(st, n, b->d(), scal(ctx, 0), ctx.reducer());
+  CUDA_OK(cudaMemcpyAsync(w.b->ptr, b_in, sizeof(double) * n,
+                          mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  launch_vec_stats(st, n, w.b->d(), scal(ctx, 0), ctx.reducer());
   check_launch();
   const double* h = read_scal(ctx, 3);
   if (h[1] > 0.0) throw Error(MSTAB_E_ERROR, "idrstab rhs: non-finite entries");
@@ -410,26 +539,25 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   rep.ell = ell;
   rep.bnorm = std::sqrt(h[0]);
 
-  WSet cur, alt;
-  cur.x = ctx.alloc_vecs(n, 1);
-  cur.r = ctx.alloc_vecs(n, 1);
+  int p = 0;  // the current state lives in w.set[p]
+  WSet& c0 = w.set[0];
   bool x_zero = true;
   if (x0_in) {
-    CUDA_OK(cudaMemcpyAsync(cur.x->ptr, x0_in, sizeof(double) * n,
+    CUDA_OK(cudaMemcpyAsync(c0.x->ptr, x0_in, sizeof(double) * n,
                             mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
-    launch_vec_stats(st, n, cur.x->d(), scal(ctx, 0), ctx.reducer());
+    launch_vec_stats(st, n, c0.x->d(), scal(ctx, 0), ctx.reducer());
     check_launch();
     const double* hx = read_scal(ctx, 3);
     x_zero = hx[2] == 0.0;
     if (!x_zero && hx[1] > 0.0) throw Error(MSTAB_E_ERROR, "idrstab guess: non-finite entries");
   } else {
-    CUDA_OK(cudaMemsetAsync(cur.x->ptr, 0, sizeof(double) * n, st));
+    CUDA_OK(cudaMemsetAsync(c0.x->ptr, 0, sizeof(double) * ld, st));
   }
   if (x_zero) {
-    CUDA_OK(cudaMemcpyAsync(cur.r->ptr, b->ptr, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(c0.r->ptr, w.b->ptr, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   } else {  // r = b - A x0, one auxiliary MV (idrstab.cpp:210-216)
-    spmv_dev(ctx, op, cur.x->d(), cur.r->d());
-    launch_rsub(st, n, b->d(), cur.r->d());
+    spmv_dev(ctx, op, c0.x->d(), c0.r->d());
+    launch_rsub(st, n, w.b->d(), c0.r->d());
     check_launch();
     rep.h_mv_aux++;
   }
@@ -443,9 +571,9 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
     rep.h_mv_aux += recycle->s;
     if (recycle->s != cfg.s) throw Error(MSTAB_E_CONFIG, "idrstab: recycle s != config s");
     P = recycle->p;
-    cur.U = recycle->u;
-    cur.V = recycle->v;
-    cur.ro = true;
+    // the solve works on copies (idrstab.cpp:227-231): the recycle data stays immutable
+    CUDA_OK(cudaMemcpyAsync(c0.U->ptr, recycle->u->ptr, sizeof(double) * ld * s, cudaMemcpyDeviceToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(c0.V->ptr, recycle->v->ptr, sizeof(double) * ld * s, cudaMemcpyDeviceToDevice, st));
     base_level = recycle->level_j;
     omega_levels = recycle->omega;
     omegas_complete = (int64_t)omega_levels.size() == base_level;
@@ -462,48 +590,28 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
       ctx.pcache_s = s;
       ctx.pcache_seed = cfg.seed;
     }
-    cur.U = ctx.alloc_vecs(n, s);
-    cur.V = ctx.alloc_vecs(n, s);
-    arnoldi_init(ctx, op, cur.r->d(), s, cfg.seed ^ 0x9e3779b97f4a7c15ull, cur.U->d(), cur.V->d());
+    arnoldi_init(ctx, op, c0.r->d(), s, cfg.seed ^ 0x9e3779b97f4a7c15ull, c0.U->d(), c0.V->d());
     rep.h_mv += s;
+  }
+  if (w.p_src != P->ptr) {  // the graphs read P from the workspace copy
+    CUDA_OK(cudaMemcpyAsync(w.P->ptr, P->ptr, sizeof(double) * ld * s, cudaMemcpyDeviceToDevice, st));
+    w.p_src = P->ptr;
   }
 
   // P^H V, P^H r, ||r|| and gamma_0 of the first cycle
   reset_status(ctx);
-  launch_prologue(st, n, ld, s, P->d(), cur.V->d(), cur.r->d(), ctx.reducer());
+  launch_prologue(st, n, ld, s, w.P->d(), c0.V->d(), c0.r->d(), ctx.reducer());
   check_launch();
   double resnorm = read_status(ctx).resnorm;
   int64_t level = 0;
   res->history.push_back({0, rep.h_mv + rep.h_mv_aux, base_level, resnorm, ns_since(t0)});
   const double threshold = cfg.tol * rep.bnorm;
 
-  std::vector<DevPtr> R(ell + 1), VL(ell + 1);
-  for (int i = 1; i <= ell; ++i) {
-    R[i] = ctx.alloc_vecs(n, 1);
-    VL[i] = ctx.alloc_vecs(n, s);
-  }
-  alt.x = ctx.alloc_vecs(n, 1);
-  alt.r = ctx.alloc_vecs(n, 1);
-  alt.U = ctx.alloc_vecs(n, s);
-  alt.V = ctx.alloc_vecs(n, s);
-
   bool broke = false;
   while (resnorm > threshold && rep.h_mv < cfg.max_mv) {
-    if (alt.ro) {  // never write into the caller's immutable recycle blocks
-      alt.U = ctx.alloc_vecs(n, s);
-      alt.V = ctx.alloc_vecs(n, s);
-      alt.ro = false;
-    }
-    enqueue_cycle(ctx, op, P->d(), s, ell, cur, alt, R, VL);
-    if (cfg.true_residual_each_cycle) {  // r = b - A x (idrstab.cpp:268-273)
-      FinParams ft;
-      ft.op = kFinTrueRes;
-      ft.s = s;
-      ft.ell = ell;
-      launch_spmv_ph(st, op.csr(), alt.x->d(), alt.r->d(), P->d(), ld, s, b->d(), ft, ctx.reducer());
-      check_launch();
-    }
+    run_cycle(ctx, op, w, p);
     const CycleStatus& cs = read_status(ctx);
+    if (w.graph[p].profiled) prof_accumulate(w.graph[p].prof);
     if (cs.breakdown) {  // BreakdownError: keep the last completed cycle (idrstab.cpp:290-293)
       rep.h_mv += cs.mv_at_breakdown;
       rep.status = MSTAB_STATUS_BREAKDOWN;
@@ -513,7 +621,7 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
       broke = true;
       break;
     }
-    std::swap(cur, alt);
+    p = 1 - p;
     rep.cycles++;
     level += ell;
     rep.h_mv += (int64_t)ell * (s + 1);
@@ -521,7 +629,7 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
     std::vector<double> tau(cs.tau, cs.tau + ell);
     if (omegas_complete) omegas_complete = extract_omegas(tau, omega_levels);
     res->taus.insert(res->taus.end(), tau.begin(), tau.end());
-    if (cfg.true_residual_each_cycle) rep.h_mv_aux++;
+    if (tres) rep.h_mv_aux++;
     resnorm = cs.resnorm;
     res->history.push_back({(int64_t)rep.cycles, rep.h_mv + rep.h_mv_aux, base_level + level, resnorm,
                             ns_since(t0)});
@@ -529,15 +637,15 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
       const bool hit = (fetch->kind == MSTAB_FETCH_AT_CYCLE && rep.cycles == fetch->cycle) ||
                        (fetch->kind == MSTAB_FETCH_AT_HALF_TOLERANCE &&
                         resnorm <= std::sqrt(cfg.tol) * rep.bnorm);
-      if (hit) {
+      if (hit) {  // fetch(): deep copy (recycle.cpp:26-38)
         auto f = std::make_shared<Recycle>();
         f->n = n;
         f->s = s;
         f->level_j = base_level + level;
         f->fingerprint = op.fingerprint;
         f->p = P;
-        f->u = copy_block(ctx, cur.U, n, s);
-        f->v = copy_block(ctx, cur.V, n, s);
+        f->u = copy_block(ctx, w.set[p].U, n, s);
+        f->v = copy_block(ctx, w.set[p].V, n, s);
         if (omegas_complete) f->omega = omega_levels;
         res->fetched = f;
       }
@@ -545,15 +653,16 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   }
   if (!broke) rep.status = resnorm <= threshold ? MSTAB_STATUS_CONVERGED : MSTAB_STATUS_MAXMV;
   rep.final_resnorm = resnorm;
-  res->x = cur.x;
+  const WSet& cur = w.set[p];
+  res->x = copy_vec(ctx, cur.x, n);
   auto fin = std::make_shared<Recycle>();
   fin->n = n;
   fin->s = s;
   fin->level_j = base_level + level;
   fin->fingerprint = op.fingerprint;
   fin->p = P;
-  fin->u = cur.U;  // handed over: the working set is not reused after the solve
-  fin->v = cur.V;
+  fin->u = copy_block(ctx, cur.U, n, s);
+  fin->v = copy_block(ctx, cur.V, n, s);
   if (omegas_complete) fin->omega = omega_levels;
   res->final_data = fin;
   rep.has_fetched = res->fetched ? 1 : 0;

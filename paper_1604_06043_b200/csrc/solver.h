@@ -11,6 +11,8 @@
 #include "host_util.h"
 #include "kernels.h"
 
+typedef struct CUgraphExec_st* cudaGraphExec_t;
+
 namespace mstab_b200 {
 
 // Device allocation freed stream-ordered on the owning stream (cudaMallocAsync pool).
@@ -34,6 +36,36 @@ struct StreamHolder {
 
 int64_t padded_ld(int64_t n);
 
+// One source/destination buffer set of the cycle ping-pong (x, r^(0), U = V^(-1), V = V^(0)).
+struct WSet {
+  DevPtr x, r, U, V;
+};
+
+// An instantiated CUDA graph of one whole cycle (ell level iterations + poly [+ true residual]).
+struct CycleGraph {
+  cudaGraphExec_t exec = nullptr;
+  uint64_t kernels = 0;
+  bool profiled = false;
+  std::vector<ProfEvent> prof;  // event pairs captured into the graph (profiling mode)
+  void reset();
+  ~CycleGraph() { reset(); }
+};
+
+// Per-context solve workspace, persistent across solves with the same (operator, s, ell,
+// true-residual) so the two cycle graphs (A->B, B->A) are captured once and replayed for every
+// cycle of every right-hand side of a sequence.
+struct Workspace {
+  uint64_t op_uid = 0;
+  int64_t n = -1;
+  int s = 0, ell = 0;
+  bool tres = false;
+  WSet set[2];
+  std::vector<DevPtr> R, VL;  // r^(1..ell), V^(1..ell)
+  DevPtr b, P;
+  const void* p_src = nullptr;  // device buffer P was last copied from
+  CycleGraph graph[2];          // graph[p]: set[p] -> set[1-p]
+};
+
 struct Context {
   std::shared_ptr<StreamHolder> sh;
   int device = 0;
@@ -41,6 +73,8 @@ struct Context {
   DevPtr partials;      // reduction partials
   CycleStatus* host_status = nullptr;  // pinned
   double* host_scal = nullptr;         // pinned, 64 doubles
+  std::unique_ptr<Workspace> ws;       // cycle buffers + captured cycle graphs
+  bool use_graphs = true;
   DevPtr pcache;                       // last make_cut_space result (immutable)
   int64_t pcache_n = -1, pcache_s = -1;
   uint64_t pcache_seed = 0;
@@ -57,6 +91,7 @@ struct Context {
 };
 
 struct Operator {
+  uint64_t uid = 0;  // unique per created operator (workspace/graph cache key)
   int64_t n = 0, nnz = 0;
   uint64_t fingerprint = 0;
   DevPtr rp, ci, val;
@@ -67,8 +102,19 @@ struct Operator {
     c.row_ptr = static_cast<const int32_t*>(rp->ptr);
     c.col_idx = static_cast<const int32_t*>(ci->ptr);
     c.values = val->d();
+    if (ndiag > 0 && use_dia) {
+      c.ndiag = ndiag;
+      c.dia_ld = dia_ld;
+      c.dia_val = dia_val->d();
+      c.dia_off = static_cast<const int32_t*>(dia_off->ptr);
+    }
     return c;
   }
+  // DIA form of the same matrix (kernels.h DevCsr), built at upload when it pays off
+  int32_t ndiag = 0;
+  int64_t dia_ld = 0;
+  DevPtr dia_val, dia_off;
+  bool use_dia = true;
 };
 
 struct Recycle {
