@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ph(DevCsr a, const double* __re
 constexpr int kDiaChunk = 8;  // diagonals whose loads are issued together
 
 template <int S, bool TRUE_RES>
-__global__ void __launch_bounds__(kBlock) k_spmv_dia(DevCsr a, const double* __restrict__ x,
+__global__ void __launch_bounds__(kBlock, 2) k_spmv_dia(DevCsr a, const double* __restrict__ x,
                                                      double* __restrict__ y,
                                                      const double* __restrict__ p, int64_t ld,
                                                      const double* __restrict__ b, FinParams fin,
