@@ -40,7 +40,7 @@ struct DevState {
   double scal[64];             // misc reduced scalars (norms, dots for init/validate)
   double gram[2 * kMaxS * kMaxS];  // validate: P^H P then V^H V
   uint32_t ticket;             // last-CTA-done counter (reset by the finaliser)
-  uint32_t _pad;
+  uint32_t tile_next;          // dynamic tile scheduler counter (reset by the finaliser)
 };
 
 }  // namespace mstab_b200

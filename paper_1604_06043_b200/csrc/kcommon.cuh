@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
@@ -107,6 +108,43 @@ __device__ bool cta_commit(const double* blk, int nslots, double* partials, uint
   return true;
 }
 
+// Dynamic tile scheduling with deterministic reductions: CTAs claim row tiles from a global
+// counter (no SM idles while a slow one finishes a static share) and store each tile's partials
+// at partials[slot * ntiles + tile]; the last CTA to finish sums every slot over tiles
+// 0..ntiles-1 in a fixed order, so the result does not depend on which CTA ran which tile.
+__device__ bool tiles_commit(int nslots, int64_t ntiles, const double* partials, uint32_t* ticket,
+                             uint32_t* tile_next, double* red) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = w; i < nslots; i += nw) {
+    const double* p = partials + (size_t)i * ntiles;
+    double acc = 0.0;
+    int64_t c = lane;
+    for (; c + 224 < ntiles; c += 256) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + c + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; c < ntiles; c += 32) acc += __ldcg(p + c);
+    acc = warp_sum(acc);
+    if (lane == 0) red[i] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *ticket = 0u;
+    *tile_next = 0u;
+  }
+  return true;
+}
+
 // solve_small / LuFactor (kernels.cpp:95-154): partially pivoted LU with the reference's pivot
 // rule (first strictly larger magnitude), singular test |pivot| < 1e-14 * max|M| or max|M| == 0,
 // inverse-multiply elimination and in-order substitutions. Single thread; a is s x s col-major
@@ -155,7 +193,96 @@ __device__ bool dev_lu_solve(int s, double* a, const double* rhs, double* x) {
   return true;
 }
 
+// The same LU + solve, by one warp: lane i holds row i of the s x s system in registers
+// (MAXS >= s). Every element sees exactly the reference's operations in the reference's order
+// (pivot = first strictly larger magnitude, elimination with the pivot inverse, forward and
+// backward substitution with ascending j), so the result is bit-identical to dev_lu_solve; the
+// dependent chain shrinks from ~s^3/3 scalar steps to ~s^2 warp steps. Call with all 32 lanes;
+// a (col-major), rhs, x live in shared memory. Returns the (warp-uniform) non-singular flag.
+template <int MAXS>
+__device__ bool warp_lu_solve(int s, const double* a, const double* rhs, double* x) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const bool mine = lane < s;
+  double row[MAXS];
+#pragma unroll
+  for (int j = 0; j < MAXS; ++j) row[j] = (mine && j < s) ? a[lane + j * s] : 0.0;
+  int perm = lane;
+  double mx = 0.0;  // max |M| (std::max semantics: NaN entries never win)
+#pragma unroll
+  for (int j = 0; j < MAXS; ++j) mx = dmax_ref(mx, fabs(row[j]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = dmax_ref(mx, __shfl_xor_sync(FULL, mx, o));
+  const double scale = mx;
+#pragma unroll
+  for (int k = 0; k < MAXS; ++k) {
+    if (k >= s) break;
+    const double akk_abs = __shfl_sync(FULL, fabs(row[k]), k);
+    int piv = k;
+    double best = akk_abs;
+    if (!isnan(akk_abs)) {  // first index with the largest magnitude among rows k.. (NaN never wins)
+      double m = (lane >= k && mine) ? fabs(row[k]) : -1.0;
+      if (isnan(m)) m = -1.0;
+      int idx = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double mo = __shfl_xor_sync(FULL, m, o);
+        const int io = __shfl_xor_sync(FULL, idx, o);
+        if (mo > m || (mo == m && io < idx)) {
+          m = mo;
+          idx = io;
+        }
+      }
+      piv = idx;
+      best = m;
+    }
+    if (best < 1e-14 * scale || scale == 0.0) return false;
+    if (piv != k) {
+      const int src = (lane == k) ? piv : ((lane == piv) ? k : lane);
+#pragma unroll
+      for (int j = 0; j < MAXS; ++j) row[j] = __shfl_sync(FULL, row[j], src);
+      perm = __shfl_sync(FULL, perm, src);
+    }
+    const double inv = 1.0 / __shfl_sync(FULL, row[k], k);
+    double rk[MAXS];
+#pragma unroll
+    for (int j = 0; j < MAXS; ++j) rk[j] = __shfl_sync(FULL, row[j], k);
+    if (lane > k && mine) {
+      const double mm = row[k] * inv;
+      row[k] = mm;
+      if (mm != 0.0) {
+#pragma unroll
+        for (int j = 0; j < MAXS; ++j)
+          if (j > k && j < s) row[j] = row[j] - mm * rk[j];
+      }
+    }
+  }
+  double xv = mine ? rhs[perm] : 0.0;
+#pragma unroll
+  for (int j = 0; j < MAXS; ++j) {  // forward: lane i subtracts L(i,j) x_j for j = 0..i-1 in order
+    if (j >= s - 1) break;
+    const double xj = __shfl_sync(FULL, xv, j);
+    if (lane > j && mine) xv = xv - row[j] * xj;
+  }
+#pragma unroll
+  for (int i = MAXS - 1; i >= 0; --i) {  // backward: x_i -= U(i,j) x_j for j = i+1.. ascending
+    if (i >= s) continue;
+    double t = xv;
+#pragma unroll
+    for (int j = i + 1; j < MAXS; ++j) {
+      if (j >= s) break;
+      const double xj = __shfl_sync(FULL, xv, j);
+      t = t - row[j] * xj;
+    }
+    t = t / row[i];
+    if (lane == i) xv = t;
+  }
+  if (mine) x[lane] = xv;
+  return true;
+}
+
 __device__ void set_breakdown(DevState* ds, int code, int mv) {
+  if (ds->st.breakdown) return;  // the first breakdown of the cycle is the one the reference raises
   ds->st.breakdown = code;
   ds->st.mv_at_breakdown = mv;
 }
@@ -163,7 +290,8 @@ __device__ void set_breakdown(DevState* ds, int code, int mv) {
 // The dense step after an SpMV reduction, run by ALL threads of the last CTA: the s x s system
 // is staged from global memory into shared memory in parallel (one element per thread; a single
 // thread walking ds->Ma would pay ~s^2 dependent L2 round trips), thread 0 factors and solves in
-// shared memory, and the solution is written back in parallel.
+// shared memory (warp 0, warp_lu_solve), and the solution is written back in parallel.
+template <int MAXS>
 __device__ void finalize_spmv(const FinParams& f, const double* red, DevState* ds) {
   __shared__ double lu[kMaxS * kMaxS];
   __shared__ double vin[kMaxS], vout[kMaxS];
@@ -228,7 +356,10 @@ __device__ void finalize_spmv(const FinParams& f, const double* red, DevState* d
   }
   __syncthreads();
   if (!solve) return;
-  if (t == 0) ok = dev_lu_solve(s, lu, vin, vout) ? 1 : 0;
+  if (t < 32) {
+    const bool r = warp_lu_solve<MAXS>(s, lu, vin, vout);
+    if (t == 0) ok = r ? 1 : 0;
+  }
   __syncthreads();
   if (t < s) dst[t] = vout[t];
   if (t == 0) {

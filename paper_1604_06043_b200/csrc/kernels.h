@@ -30,6 +30,7 @@ struct DevCsr {
   int64_t dia_ld = 0;
   const double* dia_val = nullptr;
   const int32_t* dia_off = nullptr;
+  int32_t off[64] = {};  // the offsets again, by value: kernels read them from the parameter bank
 };
 constexpr int kMaxDiag = 64;
 

@@ -28,7 +28,6 @@ __global__ void __launch_bounds__(kBlock) k_level_update(int64_t n, int64_t ld, 
     if (blockIdx.x == 0 && threadIdx.x == 0 && !ds->st.breakdown) set_breakdown(ds, kBreakSingular, 0);
     return;
   }
-  if (ds->st.breakdown) return;
   double gm[S];
 #pragma unroll
   for (int c = 0; c < S; ++c) gm[c] = ds->gamma[k * kMaxS + c];
@@ -64,7 +63,6 @@ __global__ void __launch_bounds__(kBlock) k_rebuild_top(int64_t n, int64_t ld, i
                                                         double* __restrict__ vk_out,
                                                         const double* __restrict__ vk1,
                                                         DevState* ds) {
-  if (ds->st.breakdown) return;
   double et[S];
 #pragma unroll
   for (int c = 0; c < S; ++c) et[c] = ds->eta[q * S + c];
@@ -109,7 +107,6 @@ struct DeferredArgs {
 template <int S>
 __global__ void __launch_bounds__(kBlock) k_rebuild_deferred(int64_t n, int64_t ld, int k,
                                                              DeferredArgs a, DevState* ds) {
-  if (ds->st.breakdown) return;
   __shared__ double et[S * S];
   __shared__ double gm[S];
   for (int i = threadIdx.x; i < S * S; i += blockDim.x) et[i] = ds->eta[i];

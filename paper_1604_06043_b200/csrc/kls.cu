@@ -102,7 +102,6 @@ struct LsArgs {
 template <int L>
 __global__ void __launch_bounds__(kBlock) k_ls_tsqr(int64_t n, int s, LsArgs a, Reducer red) {
   DevState* ds = red.ds;
-  if (ds->st.breakdown) return;
   constexpr int NR = Tri<L>::NR;
   double R[NR];
   double cn[L];

@@ -123,10 +123,15 @@ __global__ void k_axpby_chain(int64_t n, const double* __restrict__ x, const dou
 }
 
 __global__ void k_small_solve(int s, const double* m, const double* rhs, double* x, int32_t* ok) {
-  __shared__ double lu[kMaxS * kMaxS];
-  if (threadIdx.x != 0) return;
-  for (int i = 0; i < s * s; ++i) lu[i] = m[i];
-  *ok = dev_lu_solve(s, lu, rhs, x) ? 1 : 0;
+  // the warp LU the finalizers run (bit-identical to the scalar dev_lu_solve)
+  __shared__ double lu[kMaxS * kMaxS], vin[kMaxS], vout[kMaxS];
+  for (int i = threadIdx.x; i < s * s; i += blockDim.x) lu[i] = m[i];
+  if ((int)threadIdx.x < s) vin[threadIdx.x] = rhs[threadIdx.x];
+  __syncwarp();
+  const bool r = warp_lu_solve<kMaxS>(s, lu, vin, vout);
+  __syncwarp();
+  if ((int)threadIdx.x < s) x[threadIdx.x] = vout[threadIdx.x];
+  if (threadIdx.x == 0) *ok = r ? 1 : 0;
 }
 
 // ---- launch accounting -------------------------------------------------------------------------

@@ -69,7 +69,6 @@ template <int S, bool POLY>
 __global__ void __launch_bounds__(kBlock) k_poly(int64_t n, int64_t ld, int ell, PolyArgs a,
                                                  Reducer red) {
   DevState* ds = red.ds;
-  if (ds->st.breakdown) return;
   using GM = GramMap<S>;
   extern __shared__ double dsm[];
   double* Vs = dsm;                  // S x LDT
@@ -174,7 +173,10 @@ __global__ void __launch_bounds__(kBlock) k_poly(int64_t n, int64_t ld, int ell,
     lu[i] = redv[1 + S + i];
   }
   __syncthreads();
-  if (t == 0) ok = dev_lu_solve(S, lu, vin, vout) ? 1 : 0;
+  if (t < 32) {
+    const bool r2 = warp_lu_solve<S>(S, lu, vin, vout);
+    if (t == 0) ok = r2 ? 1 : 0;
+  }
   __syncthreads();
   if (t < S) ds->gamma[t] = vout[t];
   if (t == 0) ds->st.pending_singular = ok ? 0 : 1;

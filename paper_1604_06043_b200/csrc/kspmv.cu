@@ -26,7 +26,6 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ph(DevCsr a, const double* __re
                                                     const double* __restrict__ b, FinParams fin,
                                                     Reducer red) {
   DevState* ds = red.ds;
-  if (ds->st.breakdown) return;
   constexpr int NS = S + (TRUE_RES ? 1 : 0);
   double part[NS];
 #pragma unroll
@@ -83,7 +82,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ph(DevCsr a, const double* __re
   __shared__ double redv[NS];
   block_totals<NS>(part, blk, scratch);
   if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv)) return;
-  finalize_spmv(fin, redv, ds);
+  finalize_spmv<S>(fin, redv, ds);
 }
 
 // SpMV on the DIA form (kernels.h DevCsr): two rows per thread; every load of the row pair
@@ -99,13 +98,13 @@ __global__ void __launch_bounds__(kBlock, 2) k_spmv_dia(DevCsr a, const double* 
                                                      const double* __restrict__ p, int64_t ld,
                                                      const double* __restrict__ b, FinParams fin,
                                                      Reducer red) {
+  // No breakdown check before streaming: after a breakdown the rest of the cycle computes
+  // discarded values (the host keeps the source set) and the finalizers keep the first
+  // breakdown; skipping the check removes a dependent L2 round trip from every launch.
   DevState* ds = red.ds;
-  if (ds->st.breakdown) return;
   constexpr int NS = S + (TRUE_RES ? 1 : 0);
-  __shared__ int32_t s_off[kMaxDiag];
   const int nd = a.ndiag;
-  for (int d = threadIdx.x; d < kMaxDiag; d += blockDim.x) s_off[d] = d < nd ? a.dia_off[d] : 0;
-  __syncthreads();
+  const int32_t* s_off = a.off;  // parameter bank: no global load, no barrier
   double part[NS];
 #pragma unroll
   for (int i = 0; i < NS; ++i) part[i] = 0.0;
@@ -169,7 +168,150 @@ __global__ void __launch_bounds__(kBlock, 2) k_spmv_dia(DevCsr a, const double* 
   __shared__ double redv[NS];
   block_totals<NS>(part, blk, scratch);
   if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv)) return;
-  finalize_spmv(fin, redv, ds);
+  finalize_spmv<S>(fin, redv, ds);
+}
+
+// ---- TMA-pipelined DIA SpMV -----------------------------------------------------------------------
+// The streamed operands of a row tile (the S columns of P, the nd diagonals, b) are contiguous
+// T-row slices: one elected thread moves them into shared memory with 1-D bulk async copies
+// (cp.async.bulk, the TMA engine) completing on an mbarrier, double-buffered across tiles, so the
+// bytes in flight no longer depend on per-thread registers. Threads compute each row from shared
+// memory, gathering x (L2-resident) directly; accumulation order is unchanged (d = 0.., CSR order).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kTmaStages = 2;
+
+template <int S, bool TRUE_RES>
+__global__ void __launch_bounds__(kBlock) k_spmv_dia_tma(DevCsr a, const double* __restrict__ x,
+                                                         double* __restrict__ y,
+                                                         const double* __restrict__ p, int64_t ld,
+                                                         const double* __restrict__ b, int T,
+                                                         FinParams fin, Reducer red) {
+  DevState* ds = red.ds;
+  if (ds->st.breakdown) return;
+  constexpr int NS = S + (TRUE_RES ? 1 : 0);
+  extern __shared__ __align__(128) double tma_smem[];
+  __shared__ __align__(8) uint64_t bars[kTmaStages];
+  __shared__ int32_t s_off[kMaxDiag];
+  const int nd = a.ndiag;
+  const int nstream = S + nd + (TRUE_RES ? 1 : 0);  // slices per tile: P cols, diagonals, b
+  const int64_t n = a.n;
+  const int64_t dld = a.dia_ld;
+  const int64_t ntiles = (n + T - 1) / T;
+  for (int d = threadIdx.x; d < kMaxDiag; d += blockDim.x) s_off[d] = d < nd ? a.dia_off[d] : 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTmaStages; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t tile, int buf) {
+    const int64_t t0 = tile * T;
+    const int64_t rows = (t0 + T <= ld) ? T : (ld - t0);  // ld is a multiple of 64: 16-byte sizes
+    const uint32_t bytes = (uint32_t)(rows * sizeof(double));
+    double* base = tma_smem + (size_t)buf * nstream * T;
+    mbar_expect_tx(&bars[buf], bytes * (uint32_t)nstream);
+    for (int c = 0; c < S; ++c) bulk_g2s(base + (size_t)c * T, p + c * ld + t0, bytes, &bars[buf]);
+    for (int d = 0; d < nd; ++d) bulk_g2s(base + (size_t)(S + d) * T, a.dia_val + d * dld + t0, bytes, &bars[buf]);
+    if (TRUE_RES) bulk_g2s(base + (size_t)(S + nd) * T, b + t0, bytes, &bars[buf]);
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kTmaStages; ++i) {
+      const int64_t tile = blockIdx.x + (int64_t)i * gridDim.x;
+      if (tile < ntiles) issue(tile, i);
+    }
+  double part[NS];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) part[i] = 0.0;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int buf = it % kTmaStages;
+    mbar_wait(&bars[buf], (uint32_t)((it / kTmaStages) & 1));
+    const double* base = tma_smem + (size_t)buf * nstream * T;
+    const int64_t t0 = tile * T;
+    for (int lr = threadIdx.x; lr < T; lr += blockDim.x) {
+      const int64_t row = t0 + lr;
+      if (row >= n) break;
+      double xv[16];
+#pragma unroll
+      for (int d = 0; d < 16; ++d) {
+        if (d < nd) {
+          int64_t col = row + s_off[d];
+          col = col < 0 ? 0 : (col >= n ? n - 1 : col);  // out-of-range slots hold 0.0
+          xv[d] = __ldg(x + col);
+        }
+      }
+      double acc = 0.0;
+#pragma unroll
+      for (int d = 0; d < 16; ++d)
+        if (d < nd) acc = acc + base[(size_t)(S + d) * T + lr] * xv[d];
+      if (TRUE_RES) acc = base[(size_t)(S + nd) * T + lr] - acc;
+      y[row] = acc;
+#pragma unroll
+      for (int c = 0; c < S; ++c) part[c] = part[c] + base[(size_t)c * T + lr] * acc;
+      if (TRUE_RES) part[S] = part[S] + acc * acc;
+    }
+    __syncthreads();  // every thread is done with this buffer
+    if (threadIdx.x == 0) {
+      const int64_t next = tile + (int64_t)kTmaStages * gridDim.x;
+      if (next < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async writes
+        issue(next, buf);
+      }
+    }
+  }
+  __shared__ double scratch[NS * 32];
+  __shared__ double blk[NS];
+  __shared__ double redv[NS];
+  block_totals<NS>(part, blk, scratch);
+  if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv)) return;
+  finalize_spmv<S>(fin, redv, ds);
+}
+
+template <int S, bool TRUE_RES>
+void launch_dia_tma(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
+                    int64_t ld, const double* b, const FinParams& fin, const Reducer& red) {
+  const int nstream = S + a.ndiag + (TRUE_RES ? 1 : 0);
+  int T = 512;
+  while (T > 64 && (size_t)kTmaStages * nstream * T * sizeof(double) > 100 * 1024) T >>= 1;
+  const size_t smem = (size_t)kTmaStages * nstream * T * sizeof(double);
+  auto kfn = k_spmv_dia_tma<S, TRUE_RES>;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  const int64_t ntiles = (a.n + T - 1) / T;
+  const int grid = occupancy_grid(kfn, ntiles * kBlock, smem);
+  kfn<<<grid, kBlock, smem, st>>>(a, x, y, p, ld, b, T, fin, red);
 }
 
 }  // namespace
@@ -178,6 +320,16 @@ void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y
                     int64_t ld, int s, const double* b, const FinParams& fin, const Reducer& red) {
   // CSR + gathered x + y + P^H epilogue (+ b for the true-residual form)
   LaunchScope ls(st, kKSpmv, csr_bytes(a) + vbytes(a.n, 2.0 + s + (b ? 1.0 : 0.0)));
+  static const bool use_tma = std::getenv("MSTAB_TMA") != nullptr;  // experimental, off by default
+  if (a.ndiag > 0 && a.ndiag <= 16 && use_tma) {
+    MSTAB_DISPATCH_S(s, {
+      if (b)
+        launch_dia_tma<S, true>(st, a, x, y, p, ld, b, fin, red);
+      else
+        launch_dia_tma<S, false>(st, a, x, y, p, ld, b, fin, red);
+    });
+    return;
+  }
   if (a.ndiag > 0) {
     MSTAB_DISPATCH_S(s, {
       if (b) {

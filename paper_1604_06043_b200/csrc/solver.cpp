@@ -349,6 +349,7 @@ std::shared_ptr<Operator> make_operator(Context& ctx, int64_t n, const int64_t* 
       const int64_t ld = padded_ld(n);
       std::vector<double> dv((size_t)nd * ld, 0.0);
       std::vector<int32_t> off32(offs.begin(), offs.end());
+      op->offsets = off32;
       for (int64_t i = 0; i < n; ++i)
         for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
           const int d = (int)(std::lower_bound(offs.begin(), offs.end(), col_idx[k] - i) - offs.begin());

@@ -107,9 +107,11 @@ struct Operator {
       c.dia_ld = dia_ld;
       c.dia_val = dia_val->d();
       c.dia_off = static_cast<const int32_t*>(dia_off->ptr);
+      for (int d = 0; d < ndiag && d < 64; ++d) c.off[d] = offsets[d];
     }
     return c;
   }
+  std::vector<int32_t> offsets;  // DIA offsets (host copy)
   // DIA form of the same matrix (kernels.h DevCsr), built at upload when it pays off
   int32_t ndiag = 0;
   int64_t dia_ld = 0;
