@@ -112,6 +112,9 @@ __global__ void __launch_bounds__(kBlock) k_rebuild_deferred(int64_t n, int64_t 
   for (int i = threadIdx.x; i < S * S; i += blockDim.x) et[i] = ds->eta[i];
   if (threadIdx.x < S) gm[threadIdx.x] = ds->gamma[k * kMaxS + threadIdx.x];
   __syncthreads();
+  // eta is re-read from shared memory (broadcast) at every use: hoisting its S*S values into
+  // registers would cap the kernel at one CTA per SM
+  const volatile double* etv = et;
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
        row += (int64_t)gridDim.x * blockDim.x) {
     double ln[S], lc[S];
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(kBlock) k_rebuild_deferred(int64_t n, int64_t 
       for (int q = 0; q < S; ++q) {
         double nc = r_above;
 #pragma unroll
-        for (int c = 0; c < S; ++c) nc = nc + (-et[q * S + c]) * ((c < q) ? ln[c] : lc[c]);
+        for (int c = 0; c < S; ++c) nc = nc + (-etv[q * S + c]) * ((c < q) ? ln[c] : lc[c]);
         lc[q] = nc;
       }
       double* out = a.lv_out[i + 1];

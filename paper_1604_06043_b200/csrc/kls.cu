@@ -36,8 +36,9 @@ __device__ __forceinline__ void givens_absorb(double (&R)[Tri<L>::NR], double (&
     const double bj = w[j];
     if (bj == 0.0) continue;
     const double aj = R[Tri<L>::at(j, j)];
-    const double r = sqrt(aj * aj + bj * bj);
-    const double inv = 1.0 / r;
+    const double h2 = aj * aj + bj * bj;
+    const double inv = rsqrt(h2);  // one reciprocal square root instead of sqrt + divide
+    const double r = h2 * inv;
     const double c = aj * inv, sn = bj * inv;
     R[Tri<L>::at(j, j)] = r;
 #pragma unroll
