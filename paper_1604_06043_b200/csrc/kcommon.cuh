@@ -39,6 +39,34 @@ inline double csr_bytes(const DevCsr& a) {
   return 12.0 * (double)a.nnz + 4.0 * (double)(a.n + 1);
 }
 
+// ---- programmatic dependent launch (PDL) ------------------------------------------------------
+// Every kernel of the cycle is launched with programmatic stream serialisation: it may be
+// scheduled while its predecessor is still in its reduction tail, waits (pdl_wait, before its
+// first access to anything a predecessor wrote) until the predecessor has completed and flushed,
+// and signals (pdl_trigger, once its own streaming phase is done) that its successor may launch.
+// This hides the launch gap behind the tails; correctness is unchanged because pdl_wait is the
+// full grid dependency. Without a programmatic predecessor both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 namespace {
 
 constexpr int kSpmvStage = 384;  // CSR entries staged per warp (12 B each: 4.5 KB/warp, 36 KB/CTA)

@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(kBlock) k_level_update(int64_t n, int64_t ld, 
                                                          double* __restrict__ r_out,
                                                          const double* __restrict__ vk,
                                                          DevState* ds) {
+  pdl_wait();
   if (k == 0 && ds->st.pending_singular) {
     if (blockIdx.x == 0 && threadIdx.x == 0 && !ds->st.breakdown) set_breakdown(ds, kBreakSingular, 0);
     return;
@@ -63,6 +64,7 @@ __global__ void __launch_bounds__(kBlock) k_rebuild_top(int64_t n, int64_t ld, i
                                                         double* __restrict__ vk_out,
                                                         const double* __restrict__ vk1,
                                                         DevState* ds) {
+  pdl_wait();
   double et[S];
 #pragma unroll
   for (int c = 0; c < S; ++c) et[c] = ds->eta[q * S + c];
@@ -107,6 +109,7 @@ struct DeferredArgs {
 template <int S>
 __global__ void __launch_bounds__(kBlock) k_rebuild_deferred(int64_t n, int64_t ld, int k,
                                                              DeferredArgs a, DevState* ds) {
+  pdl_wait();
   __shared__ double et[S * S];
   __shared__ double gm[S];
   for (int i = threadIdx.x; i < S * S; i += blockDim.x) et[i] = ds->eta[i];
@@ -164,7 +167,7 @@ void launch_level_update(cudaStream_t st, int64_t n, int64_t ld, int s, int k, c
   MSTAB_DISPATCH_S(s, {
     auto kfn = k_level_update<S>;
     const int grid = occupancy_grid(kfn, n, 0);
-    kfn<<<grid, kBlock, 0, st>>>(n, ld, k, r_in, r_out, vk, ds);
+    launch_pdl(kfn, grid, kBlock, 0, st, n, ld, k, r_in, r_out, vk, ds);
   });
 }
 
@@ -174,7 +177,7 @@ void launch_rebuild_top(cudaStream_t st, int64_t n, int64_t ld, int s, int q, co
   MSTAB_DISPATCH_S(s, {
     auto kfn = k_rebuild_top<S>;
     const int grid = occupancy_grid(kfn, n, 0);
-    kfn<<<grid, kBlock, 0, st>>>(n, ld, q, rnext, vk_in, vk_out, vk1, ds);
+    launch_pdl(kfn, grid, kBlock, 0, st, n, ld, q, rnext, vk_in, vk_out, vk1, ds);
   });
 }
 
@@ -199,7 +202,7 @@ void launch_rebuild_deferred(cudaStream_t st, int64_t n, int64_t ld, int s, int 
   MSTAB_DISPATCH_S(s, {
     auto kfn = k_rebuild_deferred<S>;
     const int grid = occupancy_grid(kfn, n, 0);
-    kfn<<<grid, kBlock, 0, st>>>(n, ld, k, a, ds);
+    launch_pdl(kfn, grid, kBlock, 0, st, n, ld, k, a, ds);
   });
 }
 

@@ -103,6 +103,7 @@ struct LsArgs {
 template <int L>
 __global__ void __launch_bounds__(kBlock) k_ls_tsqr(int64_t n, int s, LsArgs a, Reducer red) {
   DevState* ds = red.ds;
+  pdl_wait();
   constexpr int NR = Tri<L>::NR;
   double R[NR];
   double cn[L];
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(kBlock) k_ls_tsqr(int64_t n, int s, LsArgs a, 
     w[L] = a.r[0][row];
     givens_absorb<L>(R, w, 0);
   }
+  pdl_trigger();
   // warp tree merge (lane absorbs lane + off)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
@@ -225,7 +227,7 @@ void launch_ls(cudaStream_t st, int64_t n, int64_t ld, int ell, int s, const dou
   MSTAB_DISPATCH_L(ell, {
     auto kfn = k_ls_tsqr<L>;
     const int grid = occupancy_grid(kfn, n, 0);
-    kfn<<<grid, kBlock, 0, st>>>(n, s, a, red);
+    launch_pdl(kfn, grid, kBlock, 0, st, n, s, a, red);
   });
 }
 

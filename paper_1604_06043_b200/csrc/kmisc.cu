@@ -198,6 +198,11 @@ LaunchScope::~LaunchScope() {
 uint64_t launch_count() { return g_launch_count.load(); }
 void count_launches(uint64_t n) { g_launch_count.fetch_add(n, std::memory_order_relaxed); }
 
+bool pdl_enabled() {
+  static const bool on = std::getenv("MSTAB_NO_PDL") == nullptr;
+  return on;
+}
+
 bool prof_enabled() {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   return g_prof.on;

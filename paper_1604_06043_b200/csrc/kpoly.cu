@@ -69,6 +69,7 @@ template <int S, bool POLY>
 __global__ void __launch_bounds__(kBlock) k_poly(int64_t n, int64_t ld, int ell, PolyArgs a,
                                                  Reducer red) {
   DevState* ds = red.ds;
+  pdl_wait();
   using GM = GramMap<S>;
   extern __shared__ double dsm[];
   double* Vs = dsm;                  // S x LDT
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__(kBlock) k_poly(int64_t n, int64_t ld, int ell,
     gram_tile<S>(Ps, Vs, gacc);
     __syncthreads();
   }
+  pdl_trigger();
   constexpr int NSL = 1 + S + S * S;
   __shared__ double blk[NSL];
   __shared__ double redv[NSL];
@@ -281,7 +283,7 @@ void launch_poly(cudaStream_t st, int64_t n, int64_t ld, int s, int ell, const d
     auto kfn = k_poly<S, true>;
     const size_t sm = gram_smem<S>();
     const int grid = occupancy_grid(kfn, n, sm);
-    kfn<<<grid, kBlock, sm, st>>>(n, ld, ell, a, red);
+    launch_pdl(kfn, grid, kBlock, sm, st, n, ld, ell, a, red);
   });
 }
 

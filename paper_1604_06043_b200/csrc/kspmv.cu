@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ph(DevCsr a, const double* __re
 #pragma unroll
   for (int i = 0; i < NS; ++i) part[i] = 0.0;
   const int64_t n = a.n;
+  pdl_wait();
   {
   const int32_t* __restrict__ rp = a.row_ptr;
   const int32_t* __restrict__ ci = a.col_idx;
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ph(DevCsr a, const double* __re
     }
   }
   }  // CSR path
+  pdl_trigger();
   __shared__ double scratch[NS * 32];
   __shared__ double blk[NS];
   __shared__ double redv[NS];
@@ -105,6 +107,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_spmv_dia(DevCsr a, const double* 
   constexpr int NS = S + (TRUE_RES ? 1 : 0);
   const int nd = a.ndiag;
   const int32_t* s_off = a.off;  // parameter bank: no global load, no barrier
+  pdl_wait();
   double part[NS];
 #pragma unroll
   for (int i = 0; i < NS; ++i) part[i] = 0.0;
@@ -163,6 +166,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_spmv_dia(DevCsr a, const double* 
       if (TRUE_RES) part[S] = part[S] + acc0 * acc0;
     }
   }
+  pdl_trigger();
   __shared__ double scratch[NS * 32];
   __shared__ double blk[NS];
   __shared__ double redv[NS];
@@ -335,11 +339,11 @@ void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y
       if (b) {
         auto kfn = k_spmv_dia<S, true>;
         const int grid = occupancy_grid(kfn, (a.n + 1) / 2, 0);
-        kfn<<<grid, kBlock, 0, st>>>(a, x, y, p, ld, b, fin, red);
+        launch_pdl(kfn, grid, kBlock, 0, st, a, x, y, p, ld, b, fin, red);
       } else {
         auto kfn = k_spmv_dia<S, false>;
         const int grid = occupancy_grid(kfn, (a.n + 1) / 2, 0);
-        kfn<<<grid, kBlock, 0, st>>>(a, x, y, p, ld, b, fin, red);
+        launch_pdl(kfn, grid, kBlock, 0, st, a, x, y, p, ld, b, fin, red);
       }
     });
     return;
@@ -348,11 +352,11 @@ void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y
     if (b) {
       auto kfn = k_spmv_ph<S, true>;
       const int grid = occupancy_grid(kfn, a.n, 0);
-      kfn<<<grid, kBlock, 0, st>>>(a, x, y, p, ld, b, fin, red);
+      launch_pdl(kfn, grid, kBlock, 0, st, a, x, y, p, ld, b, fin, red);
     } else {
       auto kfn = k_spmv_ph<S, false>;
       const int grid = occupancy_grid(kfn, a.n, 0);
-      kfn<<<grid, kBlock, 0, st>>>(a, x, y, p, ld, b, fin, red);
+      launch_pdl(kfn, grid, kBlock, 0, st, a, x, y, p, ld, b, fin, red);
     }
   });
 }
