@@ -1,7 +1,8 @@
 # Build recipe for the B200 product library, the generators and the oracles.
 #   make            -> product + generators + C restatement oracle (+ oracle/_ref when /root/reference exists)
 #   make product    -> paper_1604_06043_b200/libmstab_b200.so (sm_100a)
-#   make ref        -> oracle/_ref/libmstab_ref.so (the unmodified reference, see oracle/Makefile)
+#   make ref        -> oracle/_ref/libmstab_ref.so (the unmodified reference, see oracle/Makefile) and the
+#                      reference's own GTest suites built against it and against the B200 shim
 NVCC ?= /usr/local/cuda/bin/nvcc
 CXX ?= g++
 CUDA_HOME ?= /usr/local/cuda
@@ -42,8 +43,8 @@ $(PKG)/libmstab_gen.so: $(CSRC)/generators.cpp include/mstab_gen.h
 oracle:
 	$(MAKE) -C oracle restatement
 
-ref:
-	@if [ -d /root/reference/proj/core/src ]; then $(MAKE) -C oracle ref; else echo "reference absent: using prebuilt oracle/_ref"; fi
+ref: product
+	@if [ -d /root/reference/proj/core/src ]; then $(MAKE) -C oracle ref refsuite shimtests; else echo "reference absent: using prebuilt oracle/_ref"; fi
 
 sass: $(CU_OBJS)
 	for o in $(CU_OBJS); do $(CUDA_HOME)/bin/cuobjdump -sass $$o; done > $(BUILD)/kernels.sass

@@ -389,8 +389,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-levels", type=int, default=2)
     ap.add_argument("--write-cycles", action="store_true")
-    ap.add_argument("--profile", default="timed", choices=["timed", "after", "off"],  # graphs: events are nodes
-                    help="per-kernel CUDA events inside the timed region (default) or on K extra steps")
+    ap.add_argument("--profile", default="after", choices=["timed", "after", "off"],  # graphs: events are nodes
+                    help="per-kernel CUDA events on K extra steps after the timed region (default), or inside it")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -1,0 +1,259 @@
+// idrstab_b200.cpp — C++ drop-in shim: the reference's solve entry points
+//
+//   mstab::idrstab_solve(const LinearOperator&, const Vector& b, const Vector& x0,
+//                        const SolverConfig&, const RecycleData*, const FetchPolicy*)
+//   mstab::mstab_solve  (..., const RecycleData&, const FetchPolicy*)
+//
+// (proj/core/include/mstab/solvers/idrstab.hpp:88-96) defined on top of the B200 C-ABI
+// (include/mstab_b200.h), so a reference build that compiles this file instead of the two entry
+// points of src/idrstab.cpp runs every solve on the GPU. Everything else of
+// the reference library (CsrMatrix, CsrOperator, RecycleData, fetch/validate/save/load, the
+// harness, SRIDR and the level_iteration/poly_combination helpers) stays the reference's own.
+//
+// Behaviour kept from idrstab.cpp:193-307:
+//   * check order: SolverConfig::validate (report.cpp:16-22) -> DimensionMismatch for b / x0
+//     (:198-199) -> ensure_finite(b) (:200) -> (recycle) validate / s mismatch;
+//   * exceptions escaping to the caller are the reference's classes (errors.hpp:9-72), mapped 1:1
+//     from the C-ABI codes; breakdowns are a status with the reason string (:290-293);
+//   * SolveResult owns deep copies of x, the report (histories, per-cycle tau), final_data and
+//     the fetched snapshot (recycle.cpp:26-38).
+// B200 restrictions (no CPU fallback): the operator must be a CsrOperator and all data real
+// (imaginary parts exactly 0); anything else is rejected with ConfigError.
+#include <complex>
+#include <cstdint>
+#include <list>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mstab/csr.hpp"
+#include "mstab/errors.hpp"
+#include "mstab/operator.hpp"
+#include "mstab/recycle.hpp"
+#include "mstab/solvers/idrstab.hpp"
+#include "mstab/solvers/report.hpp"
+#include "mstab/types.hpp"
+#include "mstab_b200.h"
+
+namespace mstab {
+
+namespace {
+
+[[noreturn]] void rethrow(int code) {
+  const std::string msg = std::string("b200: ") + mstab_last_error();
+  switch (code) {
+    case MSTAB_E_DIMENSION: throw DimensionMismatch(msg);
+    case MSTAB_E_CONFIG: throw ConfigError(msg);
+    case MSTAB_E_FINGERPRINT: throw FingerprintMismatch(msg);
+    case MSTAB_E_STALE: throw StaleData(msg);
+    case MSTAB_E_PARSE: throw ParseError(msg);
+    case MSTAB_E_IO: throw IoError(msg);
+    case MSTAB_E_SINGULAR: throw SingularProjection(msg);
+    case MSTAB_E_RANK: throw RankDeficient(msg);
+    case MSTAB_E_NOTREAL: throw ConfigError(msg);
+    default: throw Error(msg);
+  }
+}
+
+void check(int code) {
+  if (code != MSTAB_OK) rethrow(code);
+}
+
+// One B200 context per host thread (a solve is single-threaded and owns its state, like the
+// reference's; operators are shared read-only).
+struct Session {
+  mstab_context* ctx = nullptr;
+  struct CachedOp {
+    const CsrMatrix* m = nullptr;
+    uint64_t fp = 0;
+    size_t nnz = 0;
+    mstab_operator* op = nullptr;
+  };
+  std::list<CachedOp> ops;  // most recent first
+  Session() { check(mstab_context_create(-1, &ctx)); }
+  ~Session() {
+    for (auto& c : ops) mstab_operator_destroy(c.op);
+    if (ctx) mstab_context_destroy(ctx);
+  }
+};
+
+Session& session() {
+  thread_local Session s;
+  return s;
+}
+
+std::vector<double> real_parts(std::span<const Complex> v, const char* what) {
+  std::vector<double> out(v.size());
+  for (size_t i = 0; i < v.size(); ++i) {
+    if (v[i].imag() != 0.0)
+      throw ConfigError(std::string("b200: complex ") + what + " not supported (real fp64 path)");
+    out[i] = v[i].real();
+  }
+  return out;
+}
+
+// Uploads the CSR matrix once per content (keyed by address, re-checked by the reference's own
+// fingerprint, csr.cpp:28-43, which the reference recomputes on every solve anyway).
+mstab_operator* device_operator(Session& ss, const LinearOperator& a) {
+  const auto* csr = dynamic_cast<const CsrOperator*>(&a);
+  if (!csr) throw ConfigError("b200: only CsrOperator is supported on the device path");
+  const CsrMatrix& m = csr->matrix();
+  const uint64_t fp = a.fingerprint();
+  for (auto it = ss.ops.begin(); it != ss.ops.end(); ++it)
+    if (it->m == &m && it->fp == fp && it->nnz == m.nnz()) {
+      ss.ops.splice(ss.ops.begin(), ss.ops, it);
+      return it->op;
+    }
+  if (!m.is_real()) throw ConfigError("b200: complex operator not supported (real fp64 path)");
+  const int64_t n = (int64_t)m.n_rows;
+  std::vector<int64_t> rp(m.row_ptr.begin(), m.row_ptr.end());
+  std::vector<int64_t> ci(m.col_idx.begin(), m.col_idx.end());
+  std::vector<double> va = real_parts(m.values, "operator");
+  mstab_operator* op = nullptr;
+  check(mstab_operator_create_csr(ss.ctx, n, rp.data(), ci.data(), va.data(), &op));
+  ss.ops.push_front({&m, fp, m.nnz(), op});
+  while (ss.ops.size() > 8) {
+    mstab_operator_destroy(ss.ops.back().op);
+    ss.ops.pop_back();
+  }
+  return op;
+}
+
+struct RecycleHandle {
+  mstab_recycle* h = nullptr;
+  ~RecycleHandle() {
+    if (h) mstab_recycle_destroy(h);
+  }
+};
+
+void upload_recycle(Session& ss, const RecycleData& rd, RecycleHandle& out) {
+  const int64_t n = (int64_t)rd.p.rows(), s = (int64_t)rd.s;
+  if ((int64_t)rd.p.cols() != s || (int64_t)rd.u.rows() != n || (int64_t)rd.u.cols() != s ||
+      (int64_t)rd.v.rows() != n || (int64_t)rd.v.cols() != s)
+    throw DimensionMismatch("recycle data has inconsistent shapes");
+  const auto p = real_parts(rd.p.data(), "recycle P");
+  const auto u = real_parts(rd.u.data(), "recycle U");
+  const auto v = real_parts(rd.v.data(), "recycle V");
+  std::vector<double> om(2 * rd.omega_history.size());
+  for (size_t i = 0; i < rd.omega_history.size(); ++i) {
+    om[2 * i] = rd.omega_history[i].real();
+    om[2 * i + 1] = rd.omega_history[i].imag();
+  }
+  check(mstab_recycle_create(ss.ctx, n, s, p.data(), u.data(), v.data(), MSTAB_MEM_HOST,
+                             om.empty() ? nullptr : om.data(), (int64_t)rd.omega_history.size(),
+                             (int64_t)rd.level_J, rd.matrix_fingerprint, &out.h));
+}
+
+RecycleData download_recycle(Session& ss, mstab_recycle* h) {
+  mstab_recycle_info info{};
+  check(mstab_recycle_info_get(h, &info));
+  const size_t n = (size_t)info.n, s = (size_t)info.s;
+  std::vector<double> p(n * s), u(n * s), v(n * s), om(2 * (size_t)info.omega_count);
+  check(mstab_recycle_download(ss.ctx, h, p.data(), u.data(), v.data(), om.empty() ? nullptr : om.data()));
+  RecycleData rd;
+  rd.p = DenseMatrix(n, s);
+  rd.u = DenseMatrix(n, s);
+  rd.v = DenseMatrix(n, s);
+  for (size_t i = 0; i < n * s; ++i) {
+    rd.p.data()[i] = Complex(p[i]);
+    rd.u.data()[i] = Complex(u[i]);
+    rd.v.data()[i] = Complex(v[i]);
+  }
+  for (int64_t i = 0; i < info.omega_count; ++i) rd.omega_history.emplace_back(om[2 * i], om[2 * i + 1]);
+  rd.level_J = (size_t)info.level_j;
+  rd.s = s;
+  rd.matrix_fingerprint = info.fingerprint;
+  return rd;
+}
+
+}  // namespace
+
+SolveResult idrstab_solve(const LinearOperator& a, const Vector& b, const Vector& x0,
+                          const SolverConfig& cfg, const RecycleData* recycle,
+                          const FetchPolicy* fetch_policy) {
+  cfg.validate();
+  const std::size_t n = a.size();
+  if (b.size() != n) throw DimensionMismatch("idrstab: rhs size");
+  if (!x0.empty() && x0.size() != n) throw DimensionMismatch("idrstab: guess size");
+  ensure_finite(b, "idrstab rhs");
+  if (!x0.empty()) ensure_finite(x0, "idrstab guess");
+
+  Session& ss = session();
+  mstab_operator* op = device_operator(ss, a);
+  const std::vector<double> bh = real_parts(b, "rhs");
+  const std::vector<double> xh = real_parts(x0, "guess");
+  RecycleHandle rh;
+  if (recycle) upload_recycle(ss, *recycle, rh);
+
+  mstab_solver_config c{};
+  c.s = (int64_t)cfg.s;
+  c.ell = (int64_t)cfg.ell;
+  c.tol = cfg.tol;
+  c.max_mv = cfg.max_mv;
+  c.true_residual_each_cycle = cfg.true_residual_each_cycle ? 1 : 0;
+  c.seed = cfg.seed;
+  mstab_fetch_policy fp{};
+  if (fetch_policy) {
+    fp.kind = fetch_policy->kind == FetchPolicy::Kind::AtCycle          ? MSTAB_FETCH_AT_CYCLE
+              : fetch_policy->kind == FetchPolicy::Kind::AtHalfTolerance ? MSTAB_FETCH_AT_HALF_TOLERANCE
+                                                                         : MSTAB_FETCH_MANUAL;
+    fp.cycle = (int64_t)fetch_policy->cycle;
+  }
+  mstab_result* res = nullptr;
+  check(::mstab_solve(ss.ctx, op, bh.data(), x0.empty() ? nullptr : xh.data(), MSTAB_MEM_HOST, &c, rh.h,
+                    fetch_policy ? &fp : nullptr, &res));
+  std::unique_ptr<mstab_result, void (*)(mstab_result*)> guard(res, mstab_result_destroy);
+
+  SolveResult out;
+  mstab_report r{};
+  check(mstab_result_report(res, &r));
+  std::vector<double> x(n);
+  check(mstab_result_x(ss.ctx, res, x.data(), MSTAB_MEM_HOST));
+  out.x.resize(n);
+  for (size_t i = 0; i < n; ++i) out.x[i] = Complex(x[i]);
+
+  SolveReport& rep = out.report;
+  rep.h_mv = r.h_mv;
+  rep.h_mv_aux = r.h_mv_aux;
+  rep.h_rd = r.h_rd;
+  rep.cycles = (size_t)r.cycles;
+  rep.status = r.status == MSTAB_STATUS_CONVERGED ? SolveStatus::Converged
+               : r.status == MSTAB_STATUS_MAXMV   ? SolveStatus::MaxMV
+                                                  : SolveStatus::Breakdown;
+  rep.breakdown_reason = r.breakdown_reason;
+  rep.bnorm = r.bnorm;
+  rep.final_resnorm = r.final_resnorm;
+  rep.wall_ns_total = r.wall_ns_total;
+  std::vector<mstab_history_point> hist((size_t)r.history_len);
+  if (r.history_len > 0 && mstab_result_history(res, hist.data(), r.history_len) != r.history_len)
+    throw Error("b200: history read failed");
+  for (const auto& h : hist)
+    rep.residual_history.push_back({(size_t)h.cycle, h.mv, (size_t)h.level, h.resnorm, h.wall_ns});
+  std::vector<double> taus(2 * (size_t)r.tau_len);
+  if (r.tau_len > 0 && mstab_result_taus(res, taus.data(), r.tau_len) != r.tau_len)
+    throw Error("b200: tau read failed");
+  const int64_t ell = r.ell > 0 ? r.ell : (int64_t)cfg.ell;
+  for (int64_t c0 = 0; c0 + ell <= r.tau_len; c0 += ell) {
+    std::vector<Complex> t;
+    for (int64_t j = 0; j < ell; ++j) t.emplace_back(taus[2 * (c0 + j)], taus[2 * (c0 + j) + 1]);
+    rep.omega_history.push_back(std::move(t));
+  }
+
+  RecycleHandle fin;
+  check(mstab_result_final_data(res, &fin.h));
+  out.final_data = download_recycle(ss, fin.h);
+  if (r.has_fetched) {
+    RecycleHandle fh;
+    check(mstab_result_fetched(res, &fh.h));
+    out.fetched = download_recycle(ss, fh.h);
+  }
+  return out;
+}
+
+SolveResult mstab_solve(const LinearOperator& a, const Vector& b, const Vector& x0,
+                        const SolverConfig& cfg, const RecycleData& recycle,
+                        const FetchPolicy* fetch_policy) {
+  return idrstab_solve(a, b, x0, cfg, &recycle, fetch_policy);
+}
+
+}  // namespace mstab

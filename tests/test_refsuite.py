@@ -1,0 +1,43 @@
+"""The reference's OWN GTest suites (proj/tests/test_solvers.cpp, test_recycle.cpp,
+test_harness.cpp), compiled unmodified by oracle/Makefile against a minimal GTest-compatible
+header (oracle/gtest_mini):
+
+* ref_<suite>  — linked with the reference library: pins gtest_mini (every assertion passes on the
+  code the suites were written for);
+* b200_<suite> — linked with the C++ drop-in shim (paper_1604_06043_b200/shim/idrstab_b200.cpp):
+  every mstab::idrstab_solve / mstab::mstab_solve the suites make, directly or through
+  run_sequence (harness.cpp), runs on the B200 through libmstab_b200.so.
+
+The binaries are built in the container that has /root/reference (build() / `make ref`) and travel
+to the GPU box with the rest of oracle/_ref (git-ignored, not gpurun-ignored)."""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+SUITE_DIR = ROOT / "oracle" / "_ref" / "suite"
+SUITES = ["test_solvers", "test_recycle", "test_harness"]
+
+
+def run_suite(path):
+    if not path.exists():
+        pytest.fail(f"{path.relative_to(ROOT)} missing: run `make ref` where /root/reference exists")
+    p = subprocess.run([str(path)], capture_output=True, text=True, timeout=900)
+    ran = [ln for ln in p.stdout.splitlines() if ln.startswith("[ RUN")]
+    failed = [ln for ln in p.stdout.splitlines() if ln.startswith("[  FAILED  ]")]
+    assert p.returncode == 0 and not failed, (p.stdout[-4000:], p.stderr[-4000:])
+    return len(ran)
+
+
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_suite_on_reference(suite):
+    """gtest_mini pinned: the suites pass against the reference library they were written for."""
+    assert run_suite(SUITE_DIR / f"ref_{suite}") > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_suite_on_b200_shim(suite):
+    """The reference's assertions hold with every solve routed through the B200 shim."""
+    assert run_suite(SUITE_DIR / f"b200_{suite}") > 0
