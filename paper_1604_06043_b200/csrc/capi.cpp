@@ -99,16 +99,22 @@ int mstab_operator_apply(mstab_context* ctx, const mstab_operator* op, const dou
     bind(ctx);
     Context& c = *ctx->impl;
     const int64_t n = op->impl->n;
-    if (mem == MSTAB_MEM_DEVICE) {
+    // The SpMV kernels move row pairs with 16-byte accesses: caller buffers are used in place
+    // only when 16-byte aligned and of even length, otherwise staged through padded buffers.
+    const bool direct = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15u) == 0 &&
+                        (n % 2) == 0;
+    if (mem == MSTAB_MEM_DEVICE && direct) {
       spmv(c, *op->impl, x, y);
       c.sync();
       return;
     }
+    const cudaMemcpyKind in = mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const cudaMemcpyKind out = mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     DevPtr dx = c.alloc_vecs(n, 1), dy = c.alloc_vecs(n, 1);
-    if (cudaMemcpyAsync(dx->ptr, x, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream()) != cudaSuccess)
+    if (cudaMemcpyAsync(dx->ptr, x, sizeof(double) * n, in, c.stream()) != cudaSuccess)
       throw Error(MSTAB_E_CUDA, "upload x");
     spmv(c, *op->impl, dx->d(), dy->d());
-    if (cudaMemcpyAsync(y, dy->ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream()) != cudaSuccess)
+    if (cudaMemcpyAsync(y, dy->ptr, sizeof(double) * n, out, c.stream()) != cudaSuccess)
       throw Error(MSTAB_E_CUDA, "download y");
     c.sync();
   });
@@ -538,6 +544,17 @@ int mstab_kernel_bench(mstab_context* ctx, const mstab_operator* op, int32_t kin
           break;
         case 5:
           launch_ls(st, n, ld, ell, s, rr, red);
+          break;
+        case 6: {  // the SpMV alone: reduced P^H y stored, no dense step in the tail
+          FinParams f;
+          f.op = kFinStore;
+          f.s = s;
+          f.dst = ds->scal;
+          launch_spmv_ph(st, csr, A.r->d(), R[1]->d(), P->d(), ld, s, nullptr, f, red);
+          break;
+        }
+        case 7:  // the s x s LU solve alone (one warp): latency of the finalizers' dense step
+          launch_small_solve(st, s, ds->Ma, ds->rhs, ds->scal, reinterpret_cast<int32_t*>(ds->scal + 32));
           break;
         default:
           throw Error(MSTAB_E_CONFIG, "bench: unknown kind");

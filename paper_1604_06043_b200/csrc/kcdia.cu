@@ -1,0 +1,133 @@
+// kcdia.cu — SpMV on the constant-diagonal (stencil) operator form with the fused P^H epilogue.
+// Split from kspmv.cu so the 96 instantiations (S x true-residual x mask width) build in parallel.
+// Compiled with --fmad=false like every kernel of the cycle (bit-exact element-wise arithmetic).
+#include <type_traits>
+
+#include "kcommon.cuh"
+
+namespace mstab_b200 {
+
+namespace {
+
+// SpMV on the constant-diagonal form (kernels.h DevCsr::cval / dia_mask): the only matrix
+// bytes streamed are the per-row presence masks (mask_bytes per row instead of 8 per diagonal),
+// the diagonal values come from the parameter bank. A term is taken only where its presence
+// bit is set — exactly the CSR terms in CSR order (offsets ascend) — so the result is
+// bit-identical to csr.cpp:103-113: an absent term's gather is predicated off and contributes
+// cval * (+0.0) = ±0.0, which leaves the accumulator unchanged (it starts at +0.0 and a
+// round-to-nearest sum never produces -0.0 from it; the upload requires finite cval).
+//
+// ncu on the first versions (c5, s=1): DRAM 24%, issue slots 63% busy, ~250 warp instructions
+// per row — instruction-bound, not memory-bound. So the stencil width ND is a template
+// parameter: the diagonal loop unrolls completely, each coefficient is a constant-bank operand
+// of its DMUL, the presence bits become predicates, and a gather is one 32-bit add, one wide
+// address multiply and one predicated load. ND = 0 is the generic (runtime nd) fallback.
+template <int ND>
+struct MaskOf {
+  using T = typename std::conditional<(ND <= 8), uint8_t,
+                                      typename std::conditional<(ND <= 16), uint16_t, uint32_t>::type>::type;
+};
+
+template <int S, bool TRUE_RES, int ND>
+__global__ void __launch_bounds__(kBlock, S <= 8 ? 4 : 2)
+    k_spmv_cdia(DevCsr a, const double* __restrict__ x, double* __restrict__ y,
+                const double* __restrict__ p, int64_t ld, const double* __restrict__ b,
+                FinParams fin, Reducer red) {
+  DevState* ds = red.ds;
+  constexpr int NS = S + (TRUE_RES ? 1 : 0);
+  const int64_t n = a.n;
+  const int nd = ND > 0 ? ND : a.ndiag;
+  const int mb = a.mask_bytes;
+  pdl_wait();
+  double part[NS];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) part[i] = 0.0;
+  // The gathers of a row are predicated on its mask, so the mask is loaded one iteration ahead
+  // (the first measured version waited for it: two dependent memory latencies per row).
+  auto load_mask = [&](int32_t r) -> uint32_t {
+    if (r >= (int32_t)n) return 0u;
+    if (ND > 0) return (uint32_t)__ldg(static_cast<const typename MaskOf<ND>::T*>(a.dia_mask) + r);
+    return mb == 1 ? (uint32_t)__ldg(static_cast<const uint8_t*>(a.dia_mask) + r)
+                   : (mb == 2 ? (uint32_t)__ldg(static_cast<const uint16_t*>(a.dia_mask) + r)
+                              : __ldg(static_cast<const uint32_t*>(a.dia_mask) + r));
+  };
+  const int32_t rstride = gridDim.x * blockDim.x;
+  uint32_t mnext = load_mask(blockIdx.x * blockDim.x + threadIdx.x);
+  for (int32_t row = blockIdx.x * blockDim.x + threadIdx.x; row < (int32_t)n; row += rstride) {
+    const uint32_t m = mnext;
+    mnext = load_mask(row + rstride);
+    double pv[S];
+#pragma unroll
+    for (int c = 0; c < S; ++c) pv[c] = __ldg(p + c * ld + row);
+    const double bv = TRUE_RES ? __ldg(b + row) : 0.0;
+    double acc = 0.0;
+    if (ND > 0) {
+      double xv[ND > 0 ? ND : 1];
+#pragma unroll
+      for (int d = 0; d < ND; ++d) xv[d] = ((m >> d) & 1u) ? __ldg(x + (row + a.off[d])) : 0.0;
+#pragma unroll
+      for (int d = 0; d < ND; ++d) acc = acc + a.cval[d] * xv[d];
+    } else {
+      for (int d0 = 0; d0 < nd; d0 += 8) {
+        double xv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int d = d0 + j;
+          xv[j] = (d < nd && ((m >> d) & 1u)) ? __ldg(x + (row + a.off[d])) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (d0 + j < nd) acc = acc + a.cval[d0 + j] * xv[j];
+      }
+    }
+    if (TRUE_RES) acc = bv - acc;
+    y[row] = acc;
+#pragma unroll
+    for (int c = 0; c < S; ++c) part[c] = part[c] + pv[c] * acc;
+    if (TRUE_RES) part[S] = part[S] + acc * acc;
+  }
+  pdl_trigger();
+  __shared__ double scratch[NS * 32];
+  __shared__ double blk[NS];
+  __shared__ double redv[NS];
+  block_totals<NS>(part, blk, scratch);
+  if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv)) return;
+  finalize_spmv<S>(fin, redv, ds);
+}
+
+template <int S, bool TRUE_RES, int ND>
+void launch_cdia_nd(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
+                    int64_t ld, const double* b, const FinParams& fin, const Reducer& red) {
+  auto kfn = k_spmv_cdia<S, TRUE_RES, ND>;
+  launch_pdl(kfn, occupancy_grid(kfn, a.n, 0), kBlock, 0, st, a, x, y, p, ld, b, fin, red);
+}
+
+// Specialised stencil widths: 5 (2-D 5-point: c1), 7 (3-D 7-point: c2, c5), 27 (27-point: c4).
+template <int S, bool TRUE_RES>
+void launch_cdia_b(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
+                   int64_t ld, const double* b, const FinParams& fin, const Reducer& red) {
+  switch (a.ndiag) {
+    case 5: launch_cdia_nd<S, TRUE_RES, 5>(st, a, x, y, p, ld, b, fin, red); break;
+    case 7: launch_cdia_nd<S, TRUE_RES, 7>(st, a, x, y, p, ld, b, fin, red); break;
+    case 27: launch_cdia_nd<S, TRUE_RES, 27>(st, a, x, y, p, ld, b, fin, red); break;
+    default: launch_cdia_nd<S, TRUE_RES, 0>(st, a, x, y, p, ld, b, fin, red); break;
+  }
+}
+
+template <int S>
+void launch_cdia(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
+                 int64_t ld, const double* b, const FinParams& fin, const Reducer& red) {
+  if (b)
+    launch_cdia_b<S, true>(st, a, x, y, p, ld, b, fin, red);
+  else
+    launch_cdia_b<S, false>(st, a, x, y, p, ld, b, fin, red);
+}
+
+}  // namespace
+
+void launch_spmv_cdia(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
+                      int64_t ld, int s, const double* b, const FinParams& fin, const Reducer& red) {
+  MSTAB_DISPATCH_S(s, { launch_cdia<S>(st, a, x, y, p, ld, b, fin, red); });
+}
+
+}  // namespace mstab_b200

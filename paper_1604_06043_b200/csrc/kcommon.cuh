@@ -33,8 +33,9 @@ struct LaunchScope {
 
 inline double vbytes(int64_t n, double vectors) { return 8.0 * (double)n * vectors; }
 // algorithmic bytes of streaming the matrix once: CSR (int32 col + fp64 value per entry, int32
-// row_ptr) or the DIA slots actually used
+// row_ptr), the DIA slots actually used, or the presence masks of the constant-diagonal form
 inline double csr_bytes(const DevCsr& a) {
+  if (a.ndiag > 0 && a.mask_bytes > 0) return (double)a.mask_bytes * (double)a.n;
   if (a.ndiag > 0) return 8.0 * (double)a.ndiag * (double)a.n;
   return 12.0 * (double)a.nnz + 4.0 * (double)(a.n + 1);
 }

@@ -31,8 +31,17 @@ struct DevCsr {
   const double* dia_val = nullptr;
   const int32_t* dia_off = nullptr;
   int32_t off[64] = {};  // the offsets again, by value: kernels read them from the parameter bank
+  // Constant-diagonal (stencil) form, chosen at upload when every diagonal holds ONE value
+  // (constant-coefficient stencils: c1, c2, c4, c5): cval[d] is that value and dia_mask holds one
+  // presence bit per diagonal per row (mask_bytes = 1, 2 or 4 bytes per row, rows padded to
+  // dia_ld). A cleared bit means CSR has no entry there (dropped boundary neighbour), so the row
+  // accumulates exactly the CSR terms in CSR order. dia_val is unused (nullptr) in this form.
+  int32_t mask_bytes = 0;
+  const void* dia_mask = nullptr;
+  double cval[32] = {};
 };
 constexpr int kMaxDiag = 64;
+constexpr int kMaxConstDiag = 32;
 
 // Reduction workspace: `partials` holds at least kMaxGrid * max_slots doubles.
 struct Reducer {
@@ -106,6 +115,10 @@ void prof_reset();
 // kernel instead writes y = b - A x and also reduces ||y||^2 (true residual refresh).
 void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
                     int64_t ld, int s, const double* b, const FinParams& fin, const Reducer& red);
+
+// The same on the constant-diagonal operator form (a.mask_bytes > 0); called by launch_spmv_ph.
+void launch_spmv_cdia(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
+                      int64_t ld, int s, const double* b, const FinParams& fin, const Reducer& red);
 
 // step (a), top level only: r_out = r_in - V^(k) gamma (gemv + subtract, idrstab.cpp:113-117).
 // At k == 0 the kernel first raises a pending singular gamma_0 as a breakdown.

@@ -325,6 +325,10 @@ void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y
   // CSR + gathered x + y + P^H epilogue (+ b for the true-residual form)
   LaunchScope ls(st, kKSpmv, csr_bytes(a) + vbytes(a.n, 2.0 + s + (b ? 1.0 : 0.0)));
   static const bool use_tma = std::getenv("MSTAB_TMA") != nullptr;  // experimental, off by default
+  if (a.ndiag > 0 && a.mask_bytes > 0) {
+    launch_spmv_cdia(st, a, x, y, p, ld, s, b, fin, red);  // kcdia.cu
+    return;
+  }
   if (a.ndiag > 0 && a.ndiag <= 16 && use_tma) {
     MSTAB_DISPATCH_S(s, {
       if (b)

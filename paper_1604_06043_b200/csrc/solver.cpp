@@ -347,20 +347,58 @@ std::shared_ptr<Operator> make_operator(Context& ctx, int64_t n, const int64_t* 
       std::sort(offs.begin(), offs.end());
       const int nd = (int)offs.size();
       const int64_t ld = padded_ld(n);
-      std::vector<double> dv((size_t)nd * ld, 0.0);
       std::vector<int32_t> off32(offs.begin(), offs.end());
       op->offsets = off32;
-      for (int64_t i = 0; i < n; ++i)
-        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
-          const int d = (int)(std::lower_bound(offs.begin(), offs.end(), col_idx[k] - i) - offs.begin());
-          dv[(size_t)d * ld + i] = values[k];
-        }
       op->ndiag = nd;
       op->dia_ld = ld;
-      op->dia_val = ctx.alloc(sizeof(double) * dv.size());
+      // Constant-diagonal form: every entry of diagonal d bit-equal to one value (constant-
+      // coefficient stencils). Then only a presence mask per row streams from HBM.
+      std::vector<uint64_t> cbits(nd, 0);
+      std::vector<char> seen(nd, 0);
+      bool constant = nd <= kMaxConstDiag && n < (int64_t(1) << 30) && std::getenv("MSTAB_NO_CDIA") == nullptr;
+      std::vector<uint32_t> mask;
+      if (constant) mask.assign((size_t)ld, 0u);
+      for (int64_t i = 0; i < n && constant; ++i)
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+          const int d = (int)(std::lower_bound(offs.begin(), offs.end(), col_idx[k] - i) - offs.begin());
+          uint64_t bits;
+          std::memcpy(&bits, &values[k], sizeof bits);
+          if (!seen[d]) {
+            seen[d] = 1;
+            cbits[d] = bits;
+          } else if (bits != cbits[d]) {
+            constant = false;
+            break;
+          }
+          mask[(size_t)i] |= 1u << d;
+        }
       op->dia_off = ctx.alloc(sizeof(int32_t) * nd);
-      CUDA_OK(cudaMemcpyAsync(op->dia_val->ptr, dv.data(), sizeof(double) * dv.size(), cudaMemcpyHostToDevice, st));
       CUDA_OK(cudaMemcpyAsync(op->dia_off->ptr, off32.data(), sizeof(int32_t) * nd, cudaMemcpyHostToDevice, st));
+      for (int d = 0; d < nd && constant; ++d) {  // absent terms add cval * (+0.0): needs finite cval
+        double v;
+        std::memcpy(&v, &cbits[d], sizeof v);
+        if (!std::isfinite(v)) constant = false;
+      }
+      if (constant) {
+        const int mb = nd <= 8 ? 1 : (nd <= 16 ? 2 : 4);
+        op->mask_bytes = mb;
+        op->cvals.resize(nd);
+        for (int d = 0; d < nd; ++d) std::memcpy(&op->cvals[d], &cbits[d], sizeof(double));
+        std::vector<uint8_t> packed((size_t)ld * mb);
+        for (size_t i = 0; i < (size_t)ld; ++i)
+          for (int byte = 0; byte < mb; ++byte) packed[i * mb + byte] = (uint8_t)(mask[i] >> (8 * byte));
+        op->dia_mask = ctx.alloc(packed.size());
+        CUDA_OK(cudaMemcpyAsync(op->dia_mask->ptr, packed.data(), packed.size(), cudaMemcpyHostToDevice, st));
+      } else {
+        std::vector<double> dv((size_t)nd * ld, 0.0);
+        for (int64_t i = 0; i < n; ++i)
+          for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+            const int d = (int)(std::lower_bound(offs.begin(), offs.end(), col_idx[k] - i) - offs.begin());
+            dv[(size_t)d * ld + i] = values[k];
+          }
+        op->dia_val = ctx.alloc(sizeof(double) * dv.size());
+        CUDA_OK(cudaMemcpyAsync(op->dia_val->ptr, dv.data(), sizeof(double) * dv.size(), cudaMemcpyHostToDevice, st));
+      }
       ctx.sync();
     }
   }

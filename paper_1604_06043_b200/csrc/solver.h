@@ -105,9 +105,14 @@ struct Operator {
     if (ndiag > 0 && use_dia) {
       c.ndiag = ndiag;
       c.dia_ld = dia_ld;
-      c.dia_val = dia_val->d();
+      c.dia_val = dia_val ? dia_val->d() : nullptr;
       c.dia_off = static_cast<const int32_t*>(dia_off->ptr);
       for (int d = 0; d < ndiag && d < 64; ++d) c.off[d] = offsets[d];
+      if (mask_bytes > 0) {
+        c.mask_bytes = mask_bytes;
+        c.dia_mask = dia_mask->ptr;
+        for (int d = 0; d < ndiag && d < kMaxConstDiag; ++d) c.cval[d] = cvals[d];
+      }
     }
     return c;
   }
@@ -117,6 +122,10 @@ struct Operator {
   int64_t dia_ld = 0;
   DevPtr dia_val, dia_off;
   bool use_dia = true;
+  // constant-diagonal form (kernels.h DevCsr::cval / dia_mask); mask_bytes == 0 when not used
+  int32_t mask_bytes = 0;
+  std::vector<double> cvals;
+  DevPtr dia_mask;
 };
 
 struct Recycle {

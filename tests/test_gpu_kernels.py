@@ -18,6 +18,17 @@ def matrices():
     yield "c1_64", pb.config("c1", grid=64).matrix()
     yield "c2_24", pb.config("c2", grid=24).matrix()
     yield "c4_12_27pt", pb.config("c4", grid=12).matrix()
+    # one perturbed entry: not constant-diagonal any more -> the value-streaming DIA form
+    c2p = pb.config("c2", grid=24).matrix()
+    c2p.values = c2p.values.copy()
+    c2p.values[777] *= 1.0 + 2.0 ** -30
+    yield "c2_24_perturbed", c2p
+    # variable coefficients on a stencil pattern (DIA form) and an explicit stored zero
+    c1v = pb.config("c1", grid=32).matrix()
+    c1v.values = c1v.values * (1.0 + 0.01 * np.sin(np.arange(c1v.values.size)))
+    yield "c1_32_varcoef", c1v
+    yield "explicit_zero", m.CsrMatrix.from_triplets(
+        4, 4, [(0, 0, 2.0), (0, 1, 0.0), (1, 1, 2.0), (1, 2, 0.0), (2, 2, 2.0), (2, 3, 0.0), (3, 3, 2.0)])
     c3 = pb.config("c3", grid=20000)
     c3.half_width = 512
     yield "c3_20000", c3.matrix()

@@ -17,7 +17,7 @@ lib.dll.mstab_kernel_bench.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_in
 ctx = m.Context(lib)
 op = m.CsrOperator(cfg.matrix(), ctx)
 hbm = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6538.6
-names = ["spmv+ph+lu", "rebuild_top", "level_update", "deferred(k=ell-1)", "poly", "ls"]
+names = ["spmv+ph+lu", "rebuild_top", "level_update", "deferred(k=ell-1)", "poly", "ls", "spmv+ph(store)", "lu(s x s)"]
 for kind in kinds:
     us, by = C.c_double(), C.c_double()
     rc = lib.dll.mstab_kernel_bench(ctx.h, op.h, kind, s, ell, iters, C.byref(us), C.byref(by))
