@@ -14,7 +14,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVCCFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC -Xptxas -O3
 CXXFLAGS := -O3 -std=c++20 -fPIC -ffp-contract=off -Wall -Wextra -I$(CUDA_HOME)/include
 
-HOST_SRCS := $(CSRC)/solver.cpp $(CSRC)/capi.cpp $(CSRC)/host_util.cpp
+HOST_SRCS := $(CSRC)/solver.cpp $(CSRC)/capi.cpp $(CSRC)/host_util.cpp $(CSRC)/comm.cpp
 HOST_OBJS := $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.o,$(HOST_SRCS))
 CU_SRCS := $(CSRC)/kspmv.cu $(CSRC)/kcdia.cu $(CSRC)/klevel.cu $(CSRC)/kls.cu $(CSRC)/kpoly.cu $(CSRC)/kmisc.cu
 CU_OBJS := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))

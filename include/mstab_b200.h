@@ -206,6 +206,50 @@ int mstab_harness_euler_rhs(mstab_context* ctx, int64_t n, const double* x, cons
 int mstab_harness_axpby(mstab_context* ctx, int64_t n, const double* x, const double* g,
                         double alpha, double* b, int32_t mem);
 
+/* ---- row-sharded solves across the GPUs of one node -----------------------
+ * One process (one context) per GPU owns a contiguous row slab of A and of every N-vector (x, b,
+ * r, P, U, V); the SpMV exchanges halo rows with the neighbouring slabs and every length-N
+ * reduction is summed over the ranks (the replicated s x s / least-squares steps then see
+ * bit-identical inputs on every rank). The reference is single-process; this is the
+ * B200 extension of its solve loop, with the same results up to reduction order.
+ *
+ * Protocol: rank 0 calls mstab_nccl_unique_id and distributes the 128 bytes; every rank calls
+ * mstab_context_set_comm_nccl, then mstab_operator_create_csr_slab with the FULL host CSR and the
+ * slab boundaries. From then on every N-length argument of this context (b, x0, x, recycle
+ * P/U/V) holds the rank's own rows only, and mstab_solve / validate are collective calls.
+ * mstab_context_set_comm_host plugs in a host runtime instead (MPI, gloo...): device buffers are
+ * staged through pinned host memory and the callbacks move them (not CUDA-graph capturable). */
+typedef struct mstab_host_comm {
+  void* user;
+  /* in-place sum over the ranks of `count` doubles (host memory); return 0 on success */
+  int32_t (*allreduce_sum)(void* user, double* buf, int64_t count);
+  /* rank-major concatenation: out[r * count ..] = rank r's in[0 .. count) */
+  int32_t (*allgather)(void* user, const double* in, double* out, int64_t count);
+  /* send send_bufs[i] (send_counts[i] doubles) to send_peers[i] and receive recv_counts[j]
+   * doubles from recv_peers[j] into recv_bufs[j], all concurrently (deadlock-free) */
+  int32_t (*halo_exchange)(void* user, int32_t nsend, const int32_t* send_peers,
+                           const double* const* send_bufs, const int64_t* send_counts, int32_t nrecv,
+                           const int32_t* recv_peers, double* const* recv_bufs,
+                           const int64_t* recv_counts);
+} mstab_host_comm;
+
+int mstab_nccl_unique_id(uint8_t out[128]);
+int mstab_context_set_comm_nccl(mstab_context* ctx, int32_t rank, int32_t world, const uint8_t id[128]);
+int mstab_context_set_comm_host(mstab_context* ctx, int32_t rank, int32_t world,
+                                const mstab_host_comm* fns);
+/* rank / world of the context (0 / 1 without a communicator) */
+int mstab_context_comm_info(mstab_context* ctx, int32_t* rank, int32_t* world);
+/* Row slab [slab_starts[rank], slab_starts[rank+1]) of the n x n CSR matrix. slab_starts has
+ * world + 1 ascending entries (0 .. n). Validation and the FNV fingerprint cover the whole
+ * matrix (csr.cpp:11-43), so every rank's operator carries the reference's fingerprint. */
+int mstab_operator_create_csr_slab(mstab_context* ctx, int64_t n, const int64_t* row_ptr,
+                                   const int64_t* col_idx, const double* values,
+                                   const int64_t* slab_starts, mstab_operator** out);
+/* First global row of the operator's slab (0 for a whole-matrix operator); size() is the
+ * number of local rows. */
+int64_t mstab_operator_row_begin(const mstab_operator* op);
+int64_t mstab_operator_global_size(const mstab_operator* op);
+
 /* ---- evidence hooks (no reference counterpart; the reference implementation reports zeros) --- */
 /* Number of kernel launches issued by this library since load. */
 uint64_t mstab_launch_count(void);

@@ -141,6 +141,28 @@ int mstab_operator_create_csr(mstab_context*, int64_t n, const int64_t* row_ptr,
     *out = o.release();
   });
 }
+// Row-sharded solves are a B200 extension (the reference is single-process): the
+// reference implementation of the ABI reports one rank and rejects communicators and slabs.
+int mstab_nccl_unique_id(uint8_t*) {
+  g_err = "reference: row-sharded solves are not part of the reference";
+  return MSTAB_E_CONFIG;
+}
+int mstab_context_set_comm_nccl(mstab_context*, int32_t, int32_t, const uint8_t*) { return mstab_nccl_unique_id(nullptr); }
+int mstab_context_set_comm_host(mstab_context*, int32_t, int32_t, const mstab_host_comm*) {
+  return mstab_nccl_unique_id(nullptr);
+}
+int mstab_context_comm_info(mstab_context*, int32_t* rank, int32_t* world) {
+  if (rank) *rank = 0;
+  if (world) *world = 1;
+  return MSTAB_OK;
+}
+int mstab_operator_create_csr_slab(mstab_context*, int64_t, const int64_t*, const int64_t*, const double*,
+                                   const int64_t*, mstab_operator**) {
+  return mstab_nccl_unique_id(nullptr);
+}
+int64_t mstab_operator_row_begin(const mstab_operator*) { return 0; }
+int64_t mstab_operator_global_size(const mstab_operator* op) { return (int64_t)op->m.n_rows; }
+
 void mstab_operator_destroy(mstab_operator* op) { delete op; }
 int64_t mstab_operator_size(const mstab_operator* op) { return (int64_t)op->m.n_rows; }
 int64_t mstab_operator_nnz(const mstab_operator* op) { return (int64_t)op->m.nnz(); }

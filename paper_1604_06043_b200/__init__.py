@@ -4,6 +4,6 @@ from .mstab import (  # noqa: F401
     BREAKDOWN, CONVERGED, MAXMV, BreakdownError, ConfigError, Context, CsrMatrix, CsrOperator, CudaError,
     DimensionMismatch, Error, FetchPolicy, FingerprintMismatch, HistoryPoint, IoError, NotReal, ParseError,
     RankDeficient, RecycleData, SingularProjection, SolveReport, SolveResult, SolverConfig, StaleData,
-    ValidationReport, arnoldi_init, default_context, fetch, idrstab_solve, least_squares_tall, load,
+    TorchHostComm, ValidationReport, arnoldi_init, default_context, fetch, idrstab_solve, least_squares_tall, load,
     make_cut_space, mstab_solve, save, solve_small, validate)
 from ._capi import Lib, PRODUCT_LIB  # noqa: F401

@@ -104,6 +104,27 @@ ABI = [
     ("mstab_result_handoff", C.c_int, [_P, C.POINTER(_P)]),
 ]
 
+class HostCommC(C.Structure):
+    """mstab_host_comm (include/mstab_b200.h): host callbacks of a row-sharded solve."""
+    ALLREDUCE = C.CFUNCTYPE(C.c_int32, C.c_void_p, _D, C.c_int64)
+    ALLGATHER = C.CFUNCTYPE(C.c_int32, C.c_void_p, _D, _D, C.c_int64)
+    HALO = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(_D), _I64,
+                       C.c_int32, C.POINTER(C.c_int32), C.POINTER(_D), _I64)
+    _fields_ = [("user", C.c_void_p), ("allreduce_sum", ALLREDUCE), ("allgather", ALLGATHER),
+                ("halo_exchange", HALO)]
+
+
+ABI += [
+    ("mstab_nccl_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
+    ("mstab_context_set_comm_nccl", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_uint8)]),
+    ("mstab_context_set_comm_host", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(HostCommC)]),
+    ("mstab_context_comm_info", C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    ("mstab_operator_create_csr_slab", C.c_int, [_P, C.c_int64, _I64, _I64, _D, _I64, C.POINTER(_P)]),
+    ("mstab_operator_row_begin", C.c_int64, [_P]),
+    ("mstab_operator_global_size", C.c_int64, [_P]),
+]
+
+
 class KernelClassStatsC(C.Structure):
     _fields_ = [("launches", C.c_int64), ("total_ms", C.c_double), ("total_bytes", C.c_double)]
 

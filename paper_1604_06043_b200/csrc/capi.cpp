@@ -88,6 +88,50 @@ int mstab_operator_create_csr(mstab_context* ctx, int64_t n, const int64_t* row_
   });
 }
 
+int mstab_nccl_unique_id(uint8_t out[128]) {
+  return guarded([&] { nccl_unique_id(out); });
+}
+
+int mstab_context_set_comm_nccl(mstab_context* ctx, int32_t rank, int32_t world, const uint8_t id[128]) {
+  return guarded([&] {
+    bind(ctx);
+    if (world < 1 || rank < 0 || rank >= world) throw Error(MSTAB_E_CONFIG, "comm: bad rank/world");
+    ctx->impl->sync();
+    ctx->impl->comm = make_nccl_comm(rank, world, id, ctx->impl->device);
+  });
+}
+
+int mstab_context_set_comm_host(mstab_context* ctx, int32_t rank, int32_t world, const mstab_host_comm* fns) {
+  return guarded([&] {
+    bind(ctx);
+    if (world < 1 || rank < 0 || rank >= world || !fns) throw Error(MSTAB_E_CONFIG, "comm: bad rank/world");
+    ctx->impl->sync();
+    ctx->impl->comm = make_host_comm(rank, world, *fns);
+  });
+}
+
+int mstab_context_comm_info(mstab_context* ctx, int32_t* rank, int32_t* world) {
+  return guarded([&] {
+    const Context& c = *ctx->impl;
+    if (rank) *rank = c.comm ? c.comm->rank() : 0;
+    if (world) *world = c.comm ? c.comm->world() : 1;
+  });
+}
+
+int mstab_operator_create_csr_slab(mstab_context* ctx, int64_t n, const int64_t* row_ptr,
+                                   const int64_t* col_idx, const double* values,
+                                   const int64_t* slab_starts, mstab_operator** out) {
+  return guarded([&] {
+    bind(ctx);
+    auto o = std::make_unique<mstab_operator>();
+    o->impl = make_operator_slab(*ctx->impl, n, row_ptr, col_idx, values, slab_starts);
+    *out = o.release();
+  });
+}
+
+int64_t mstab_operator_row_begin(const mstab_operator* op) { return op->impl->row0; }
+int64_t mstab_operator_global_size(const mstab_operator* op) { return op->impl->n_global; }
+
 void mstab_operator_destroy(mstab_operator* op) { delete op; }
 int64_t mstab_operator_size(const mstab_operator* op) { return op->impl->n; }
 int64_t mstab_operator_nnz(const mstab_operator* op) { return op->impl->nnz; }
@@ -101,7 +145,7 @@ int mstab_operator_apply(mstab_context* ctx, const mstab_operator* op, const dou
     const int64_t n = op->impl->n;
     // The SpMV kernels move row pairs with 16-byte accesses: caller buffers are used in place
     // only when 16-byte aligned and of even length, otherwise staged through padded buffers.
-    const bool direct = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15u) == 0 &&
+    const bool direct = !c.sharded() && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15u) == 0 &&
                         (n % 2) == 0;
     if (mem == MSTAB_MEM_DEVICE && direct) {
       spmv(c, *op->impl, x, y);
@@ -111,10 +155,10 @@ int mstab_operator_apply(mstab_context* ctx, const mstab_operator* op, const dou
     const cudaMemcpyKind in = mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     const cudaMemcpyKind out = mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     DevPtr dx = c.alloc_vecs(n, 1), dy = c.alloc_vecs(n, 1);
-    if (cudaMemcpyAsync(dx->ptr, x, sizeof(double) * n, in, c.stream()) != cudaSuccess)
+    if (cudaMemcpyAsync(dx->d(), x, sizeof(double) * n, in, c.stream()) != cudaSuccess)
       throw Error(MSTAB_E_CUDA, "upload x");
     spmv(c, *op->impl, dx->d(), dy->d());
-    if (cudaMemcpyAsync(y, dy->ptr, sizeof(double) * n, out, c.stream()) != cudaSuccess)
+    if (cudaMemcpyAsync(y, dy->d(), sizeof(double) * n, out, c.stream()) != cudaSuccess)
       throw Error(MSTAB_E_CUDA, "download y");
     c.sync();
   });
@@ -133,11 +177,11 @@ int mstab_recycle_create(mstab_context* ctx, int64_t n, int64_t s, const double*
     r->s = s;
     r->level_j = level_j;
     r->fingerprint = fingerprint;
-    const int64_t ld = padded_ld(n);
+    const int64_t ld = c.ld(n);
     const auto kind = mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     auto up = [&](const double* src) {
       DevPtr d = c.alloc_vecs(n, s);
-      if (cudaMemcpy2DAsync(d->ptr, sizeof(double) * ld, src, sizeof(double) * n, sizeof(double) * n, s,
+      if (cudaMemcpy2DAsync(d->d(), sizeof(double) * ld, src, sizeof(double) * n, sizeof(double) * n, s,
                             kind, c.stream()) != cudaSuccess)
         throw Error(MSTAB_E_CUDA, "recycle upload");
       return d;
@@ -172,10 +216,10 @@ int mstab_recycle_download(mstab_context* ctx, const mstab_recycle* rd, double* 
     bind(ctx);
     Context& c = *ctx->impl;
     const Recycle& r = *rd->impl;
-    const int64_t ld = padded_ld(r.n);
+    const int64_t ld = c.ld(r.n);
     auto down = [&](const DevPtr& src, double* dst) {
       if (!dst) return;
-      if (cudaMemcpy2DAsync(dst, sizeof(double) * r.n, src->ptr, sizeof(double) * ld, sizeof(double) * r.n,
+      if (cudaMemcpy2DAsync(dst, sizeof(double) * r.n, src->d(), sizeof(double) * ld, sizeof(double) * r.n,
                             r.s, cudaMemcpyDeviceToHost, c.stream()) != cudaSuccess)
         throw Error(MSTAB_E_CUDA, "recycle download");
     };
@@ -203,6 +247,8 @@ int mstab_recycle_validate(mstab_context* ctx, const mstab_recycle* rd, const ms
 int mstab_recycle_save(mstab_context* ctx, const mstab_recycle* rd, const char* path) {
   return guarded([&] {
     bind(ctx);
+    if (ctx->impl->sharded())
+      throw Error(MSTAB_E_CONFIG, "recycle save: a row-sharded context holds a slab; gather P/U/V on the host");
     const Recycle& r = *rd->impl;
     MrdData d;
     d.n = r.n;
@@ -222,6 +268,8 @@ int mstab_recycle_save(mstab_context* ctx, const mstab_recycle* rd, const char* 
 int mstab_recycle_load(mstab_context* ctx, const char* path, mstab_recycle** out) {
   return guarded([&] {
     bind(ctx);
+    if (ctx->impl->sharded())
+      throw Error(MSTAB_E_CONFIG, "recycle load: a row-sharded context holds a slab; scatter P/U/V on the host");
     MrdData d = mrd_read(path);
     std::vector<double> om(2 * d.omega.size());
     for (size_t i = 0; i < d.omega.size(); ++i) {
@@ -256,7 +304,7 @@ int mstab_result_x(mstab_context* ctx, const mstab_result* res, double* x, int32
   return guarded([&] {
     bind(ctx);
     Context& c = *ctx->impl;
-    if (cudaMemcpyAsync(x, res->impl->x->ptr, sizeof(double) * res->impl->n,
+    if (cudaMemcpyAsync(x, res->impl->x->d(), sizeof(double) * res->impl->n,
                         mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                         c.stream()) != cudaSuccess)
       throw Error(MSTAB_E_CUDA, "download x");
@@ -342,7 +390,7 @@ int mstab_kernel_least_squares(mstab_context* ctx, int64_t n, int64_t ell, const
     Context& c = *ctx->impl;
     if (ell < 1 || n < ell) throw Error(MSTAB_E_DIMENSION, "least_squares_tall: need N >= ell >= 1");
     if (ell > kMaxEll) throw Error(MSTAB_E_CONFIG, "b200: least squares supports ell <= 8");
-    const int64_t ld = padded_ld(n);
+    const int64_t ld = c.ld(n);
     DevPtr zr = c.alloc_vecs(n, ell + 1);
     cudaMemcpyAsync(zr->d(), r, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream());
     cudaMemcpy2DAsync(zr->d() + ld, sizeof(double) * ld, z, sizeof(double) * n, sizeof(double) * n, ell,
@@ -364,7 +412,7 @@ int mstab_kernel_cut_space(mstab_context* ctx, int64_t n, int64_t s, uint64_t se
     Context& c = *ctx->impl;
     if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: 1 <= s <= 16");
     DevPtr P = make_cut_space(c, n, (int)s, seed);
-    cudaMemcpy2DAsync(p, sizeof(double) * n, P->ptr, sizeof(double) * padded_ld(n), sizeof(double) * n, s,
+    cudaMemcpy2DAsync(p, sizeof(double) * n, P->d(), sizeof(double) * c.ld(n), sizeof(double) * n, s,
                       cudaMemcpyDeviceToHost, c.stream());
     c.sync();
   });
@@ -376,14 +424,14 @@ int mstab_kernel_arnoldi(mstab_context* ctx, const mstab_operator* op, const dou
     bind(ctx);
     Context& c = *ctx->impl;
     if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: 1 <= s <= 16");
-    const int64_t n = op->impl->n, ld = padded_ld(n);
+    const int64_t n = op->impl->n, ld = c.ld(n);
     DevPtr r = c.alloc_vecs(n, 1), U = c.alloc_vecs(n, s), V = c.alloc_vecs(n, s);
-    cudaMemcpyAsync(r->ptr, r0, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream());
+    cudaMemcpyAsync(r->d(), r0, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream());
     reset_status(c);
     arnoldi_init(c, *op->impl, r->d(), (int)s, rng_seed, U->d(), V->d());
-    cudaMemcpy2DAsync(u, sizeof(double) * n, U->ptr, sizeof(double) * ld, sizeof(double) * n, s,
+    cudaMemcpy2DAsync(u, sizeof(double) * n, U->d(), sizeof(double) * ld, sizeof(double) * n, s,
                       cudaMemcpyDeviceToHost, c.stream());
-    cudaMemcpy2DAsync(v, sizeof(double) * n, V->ptr, sizeof(double) * ld, sizeof(double) * n, s,
+    cudaMemcpy2DAsync(v, sizeof(double) * n, V->d(), sizeof(double) * ld, sizeof(double) * n, s,
                       cudaMemcpyDeviceToHost, c.stream());
     c.sync();
     if (mv_cost) *mv_cost = s;
@@ -470,7 +518,7 @@ int mstab_kernel_bench(mstab_context* ctx, const mstab_operator* op, int32_t kin
     const Operator& o = *op->impl;
     const int s = (int)s64, ell = (int)ell64;
     if (s < 1 || s > kMaxS || ell < 1 || ell > kMaxEll) throw Error(MSTAB_E_CONFIG, "bench: bad s/ell");
-    const int64_t n = o.n, ld = padded_ld(n);
+    const int64_t n = o.n, ld = c.ld(n);
     cudaStream_t st = c.stream();
     uint64_t seed = 1;
     auto vec = [&](int64_t cols) {

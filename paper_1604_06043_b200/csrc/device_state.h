@@ -14,6 +14,7 @@ constexpr int kMaxS = 16;    // s in {1..16} (BASELINE c5 sweep tops at 16)
 constexpr int kMaxEll = 8;   // ell in {1..8}
 constexpr int kBlock = 256;  // threads per CTA for every streaming kernel
 constexpr int kMaxGrid = 148 * 8;
+constexpr int kMaxXred = 2 + 2 * kMaxS * kMaxS + 6;  // largest split payload (validate)
 
 // Breakdown codes written by the device finalizers (idrstab.cpp:290-293 reasons).
 enum : int32_t { kBreakNone = 0, kBreakSingular = 1, kBreakRank = 2 };
@@ -39,6 +40,10 @@ struct DevState {
   double eta[kMaxS * kMaxS];   // eta_q of the current level, row q = eta for column q
   double scal[64];             // misc reduced scalars (norms, dots for init/validate)
   double gram[2 * kMaxS * kMaxS];  // validate: P^H P then V^H V
+  // Row-sharded solves (comm world > 1): the last CTA of a reduction kernel leaves its rank-local
+  // totals here instead of running the dense step; the host allreduces (or allgathers) them over
+  // the ranks and launches the matching finaliser kernel (kernels.h launch_fin_*).
+  double xred[kMaxXred];
   uint32_t ticket;             // last-CTA-done counter (reset by the finaliser)
   uint32_t tile_next;          // dynamic tile scheduler counter (reset by the finaliser)
 };

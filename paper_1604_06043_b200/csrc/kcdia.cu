@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kBlock, S <= 8 ? 4 : 2)
   __shared__ double blk[NS];
   __shared__ double redv[NS];
   block_totals<NS>(part, blk, scratch);
-  if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv)) return;
+  if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv, red.xred)) return;
   finalize_spmv<S>(fin, redv, ds);
 }
 

@@ -104,7 +104,7 @@ __device__ void block_totals(const double (&v)[NS], double* blk, double* scratch
 // Writes the CTA's `nslots` totals as partials[slot][cta]; the last CTA to arrive reduces every
 // slot over all CTAs in a fixed order into `red` (smem) and returns true.
 __device__ bool cta_commit(const double* blk, int nslots, double* partials, uint32_t* ticket,
-                           double* red) {
+                           double* red, double* xred = nullptr) {
   __shared__ int s_last;
   const int G = gridDim.x;
   for (int i = threadIdx.x; i < nslots; i += blockDim.x)
@@ -134,6 +134,10 @@ __device__ bool cta_commit(const double* blk, int nslots, double* partials, uint
   }
   __syncthreads();
   if (threadIdx.x == 0) *ticket = 0u;
+  if (xred) {  // row-sharded: hand the rank-local totals to the cross-rank reduction
+    for (int i = threadIdx.x; i < nslots; i += blockDim.x) xred[i] = red[i];
+    return false;
+  }
   return true;
 }
 

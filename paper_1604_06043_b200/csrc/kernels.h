@@ -39,6 +39,9 @@ struct DevCsr {
   int32_t mask_bytes = 0;
   const void* dia_mask = nullptr;
   double cval[32] = {};
+  // Valid index range [xlo, xhi) of the x vector the SpMV reads: [0, n) on one GPU; in a
+  // row-sharded solve the owned rows plus the halo on either side (negative xlo).
+  int64_t xlo = 0, xhi = 0;
 };
 constexpr int kMaxDiag = 64;
 constexpr int kMaxConstDiag = 32;
@@ -47,6 +50,9 @@ constexpr int kMaxConstDiag = 32;
 struct Reducer {
   double* partials = nullptr;
   DevState* ds = nullptr;
+  // Non-null in row-sharded solves: the last CTA writes its rank-local totals here (ds->xred)
+  // and skips the fused dense step (cta_commit), which then runs after the cross-rank reduction.
+  double* xred = nullptr;
 };
 
 // What the last CTA does with the reduced vector of an SpMV (see kernels.cu, finalize_spmv).
@@ -119,6 +125,17 @@ void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y
 // The same on the constant-diagonal operator form (a.mask_bytes > 0); called by launch_spmv_ph.
 void launch_spmv_cdia(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
                       int64_t ld, int s, const double* b, const FinParams& fin, const Reducer& red);
+
+// ---- row-sharded solves: finalisers run after the cross-rank reduction of ds->xred ---------
+// Each replays exactly the dense tail the fused kernel runs in its last CTA (same code), from
+// the reduced totals in ds->xred (allreduced) or `gath` (allgathered, rank-major).
+void launch_fin_spmv(cudaStream_t st, int s, const FinParams& fin, DevState* ds);
+void launch_fin_poly(cudaStream_t st, int s, DevState* ds);
+// dots / stats / validate: copy the reduced totals where the fused kernel would have stored them
+void launch_fin_copy(cudaStream_t st, const double* src, double* dst, int count);
+// LS: merge `world` rank-local R factors (+ column sums of squares) in rank order, then solve.
+void launch_fin_ls(cudaStream_t st, int ell, int s, int world, const double* gath, DevState* ds);
+constexpr int ls_split_count(int ell) { return (ell + 1) * (ell + 2) / 2 + ell; }
 
 // step (a), top level only: r_out = r_in - V^(k) gamma (gemv + subtract, idrstab.cpp:113-117).
 // At k == 0 the kernel first raises a pending singular gamma_0 as a breakdown.

@@ -211,12 +211,46 @@ __global__ void __launch_bounds__(kBlock) k_ls_tsqr(int64_t n, int s, LsArgs a, 
       for (int i = 0; i < NR; ++i) B[i] = wR[w2 * NR + i];
       absorb_tri<L>(Rc, B);
     }
-    ls_finalize<L>(Rc, cnt, s, ds);
     ds->ticket = 0u;
+    if (red.xred) {  // row-sharded: this rank's R factor and column sums go to the allgather
+#pragma unroll
+      for (int i = 0; i < NR; ++i) red.xred[i] = Rc[i];
+      for (int j = 0; j < L; ++j) red.xred[NR + j] = cnt[j];
+      return;
+    }
+    ls_finalize<L>(Rc, cnt, s, ds);
   }
 }
 
+// Row-sharded finaliser: `gath` holds every rank's (R, column sums) back to back, rank-major.
+// The factors are merged in rank order by the same Givens absorption as the in-kernel tree and
+// the column sums added in rank order, so every rank solves the identical least-squares system.
+template <int L>
+__global__ void k_fin_ls(int s, int world, const double* __restrict__ gath, DevState* ds) {
+  constexpr int NR = Tri<L>::NR;
+  if (threadIdx.x != 0) return;
+  double Rc[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) Rc[i] = gath[i];
+  double cnt[L];
+  for (int j = 0; j < L; ++j) cnt[j] = gath[NR + j];
+  for (int w = 1; w < world; ++w) {
+    const double* g = gath + (size_t)w * (NR + L);
+    double B[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) B[i] = g[i];
+    absorb_tri<L>(Rc, B);
+    for (int j = 0; j < L; ++j) cnt[j] = cnt[j] + g[NR + j];
+  }
+  ls_finalize<L>(Rc, cnt, s, ds);
+}
+
 }  // namespace
+
+void launch_fin_ls(cudaStream_t st, int ell, int s, int world, const double* gath, DevState* ds) {
+  static_assert(ls_split_count(8) <= kMaxXred, "LS split payload exceeds xred");
+  MSTAB_DISPATCH_L(ell, { k_fin_ls<L><<<1, 32, 0, st>>>(s, world, gath, ds); });
+}
 
 void launch_ls(cudaStream_t st, int64_t n, int64_t ld, int ell, int s, const double* const* r,
                const Reducer& red) {

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kBlock) k_dots(int64_t n, int64_t ld, const do
   __shared__ double blk[kMaxDots];
   __shared__ double redv[kMaxDots];
   block_totals<kMaxDots>(acc, blk, scratch);
-  if (!cta_commit(blk, kMaxDots, red.partials, &ds->ticket, redv)) return;
+  if (!cta_commit(blk, kMaxDots, red.partials, &ds->ticket, redv, red.xred)) return;
   if (threadIdx.x == 0) {
     for (int j = 0; j < na; ++j) dst[j] = redv[j];
     if (with_norm) dst[na] = redv[kMaxS];
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kBlock) k_vec_stats(int64_t n, const double* _
   __shared__ double blk[3];
   __shared__ double redv[3];
   block_totals<3>(acc, blk, scratch);
-  if (!cta_commit(blk, 3, red.partials, &ds->ticket, redv)) return;
+  if (!cta_commit(blk, 3, red.partials, &ds->ticket, redv, red.xred)) return;
   if (threadIdx.x == 0)
     for (int j = 0; j < 3; ++j) dst[j] = redv[j];
 }
@@ -321,6 +321,16 @@ void launch_axpby_chain(cudaStream_t st, int64_t n, const double* x, const doubl
                         double* b) {
   LaunchScope ls(st, kKOther, vbytes(n, 3.0));
   k_axpby_chain<<<grid_for(n), kBlock, 0, st>>>(n, x, g, alpha, b);
+}
+
+namespace {
+__global__ void k_fin_copy(const double* __restrict__ src, double* __restrict__ dst, int count) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = src[i];
+}
+}  // namespace
+
+void launch_fin_copy(cudaStream_t st, const double* src, double* dst, int count) {
+  k_fin_copy<<<1, kBlock, 0, st>>>(src, dst, count);
 }
 
 void launch_small_solve(cudaStream_t st, int s, const double* m, const double* rhs, double* x,

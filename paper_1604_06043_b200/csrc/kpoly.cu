@@ -62,6 +62,34 @@ struct PolyArgs {
   const double* p;
 };
 
+// The dense tail of poly / prologue (run by every thread of one CTA): ||r||, g = P^H r,
+// Ma = P^H V and the next cycle's gamma_0 = (P^H V)^-1 P^H r, staged in parallel and solved by
+// one warp in shared memory.
+template <int S>
+__device__ void poly_tail(const double* redv, DevState* ds) {
+  __shared__ double lu[kMaxS * kMaxS];
+  __shared__ double vin[kMaxS], vout[kMaxS];
+  __shared__ int ok;
+  const int t = threadIdx.x;
+  if (t == 0) ds->st.resnorm = sqrt(redv[0]);
+  if (t < S) {
+    ds->g[t] = redv[1 + t];
+    vin[t] = redv[1 + t];
+  }
+  for (int i = t; i < S * S; i += blockDim.x) {
+    ds->Ma[i] = redv[1 + S + i];
+    lu[i] = redv[1 + S + i];
+  }
+  __syncthreads();
+  if (t < 32) {
+    const bool r2 = warp_lu_solve<S>(S, lu, vin, vout);
+    if (t == 0) ok = r2 ? 1 : 0;
+  }
+  __syncthreads();
+  if (t < S) ds->gamma[t] = vout[t];
+  if (t == 0) ds->st.pending_singular = ok ? 0 : 1;
+}
+
 // POLY = true: poly_combination (idrstab.cpp:154-191) + fused reductions.
 // POLY = false: prologue (reductions of the given V and r only).
 // Slots: [0] ||r||^2, [1..S] P^H r, [1+S ..] P^H V (col-major s x s).
@@ -159,29 +187,18 @@ __global__ void __launch_bounds__(kBlock) k_poly(int64_t n, int64_t ld, int ell,
     if (threadIdx.x < S) blk[1 + threadIdx.x] = blk0[threadIdx.x];
     gram_combine<S>(gacc, gsc, blk + 1 + S);
   }
-  if (!cta_commit(blk, NSL, red.partials, &ds->ticket, redv)) return;
-  // next cycle's gamma_0 = (P^H V)^-1 P^H r, staged in parallel, solved by one thread in smem
-  __shared__ double lu[kMaxS * kMaxS];
-  __shared__ double vin[kMaxS], vout[kMaxS];
-  __shared__ int ok;
-  const int t = threadIdx.x;
-  if (t == 0) ds->st.resnorm = sqrt(redv[0]);
-  if (t < S) {
-    ds->g[t] = redv[1 + t];
-    vin[t] = redv[1 + t];
-  }
-  for (int i = t; i < S * S; i += blockDim.x) {
-    ds->Ma[i] = redv[1 + S + i];
-    lu[i] = redv[1 + S + i];
-  }
+  if (!cta_commit(blk, NSL, red.partials, &ds->ticket, redv, red.xred)) return;
+  poly_tail<S>(redv, ds);
+}
+
+// Row-sharded finaliser of poly / prologue: the allreduced slots through the same tail.
+template <int S>
+__global__ void __launch_bounds__(kBlock) k_fin_poly(DevState* ds) {
+  constexpr int NSL = 1 + S + S * S;
+  __shared__ double redv[NSL];
+  for (int i = threadIdx.x; i < NSL; i += blockDim.x) redv[i] = ds->xred[i];
   __syncthreads();
-  if (t < 32) {
-    const bool r2 = warp_lu_solve<S>(S, lu, vin, vout);
-    if (t == 0) ok = r2 ? 1 : 0;
-  }
-  __syncthreads();
-  if (t < S) ds->gamma[t] = vout[t];
-  if (t == 0) ds->st.pending_singular = ok ? 0 : 1;
+  poly_tail<S>(redv, ds);
 }
 
 // validate(): ||V - A U||^2, sum ||V_q||^2, P^H P, V^H V in one pass.
@@ -240,7 +257,7 @@ __global__ void __launch_bounds__(kBlock) k_validate(DevCsr a, const double* __r
   block_totals<2>(dn, blk, scratch);
   gram_combine<S>(g1, gsc, blk + 2);
   gram_combine<S>(g2, gsc, blk + 2 + S * S);
-  if (!cta_commit(blk, NSL, red.partials, &ds->ticket, redv)) return;
+  if (!cta_commit(blk, NSL, red.partials, &ds->ticket, redv, red.xred)) return;
   if (threadIdx.x < 2) ds->scal[threadIdx.x] = redv[threadIdx.x];
   for (int i = threadIdx.x; i < 2 * S * S; i += blockDim.x) ds->gram[i] = redv[2 + i];
 }
@@ -251,6 +268,10 @@ size_t gram_smem() {
 }
 
 }  // namespace
+
+void launch_fin_poly(cudaStream_t st, int s, DevState* ds) {
+  MSTAB_DISPATCH_S(s, { launch_pdl(k_fin_poly<S>, 1, kBlock, 0, st, ds); });
+}
 
 void kpoly_init() {
   // opt in to > 48 KB dynamic shared memory for the Gram tiles (s up to 16)

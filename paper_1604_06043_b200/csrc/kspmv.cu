@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ph(DevCsr a, const double* __re
   __shared__ double blk[NS];
   __shared__ double redv[NS];
   block_totals<NS>(part, blk, scratch);
-  if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv)) return;
+  if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv, red.xred)) return;
   finalize_spmv<S>(fin, redv, ds);
 }
 
@@ -134,8 +134,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_spmv_dia(DevCsr a, const double* 
         if (d < nd) {
           vv[j] = __ldg(reinterpret_cast<const double2*>(dv + d * dld + r0));  // dia_ld padding is 0
           int64_t c0 = r0 + s_off[d], c1 = c0 + 1;
-          c0 = c0 < 0 ? 0 : (c0 >= n ? n - 1 : c0);  // out-of-range slots hold 0.0
-          c1 = c1 < 0 ? 0 : (c1 >= n ? n - 1 : c1);
+          c0 = c0 < a.xlo ? a.xlo : (c0 >= a.xhi ? a.xhi - 1 : c0);  // out-of-range slots hold 0.0
+          c1 = c1 < a.xlo ? a.xlo : (c1 >= a.xhi ? a.xhi - 1 : c1);
           x0[j] = __ldg(x + c0);
           x1[j] = __ldg(x + c1);
         }
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_spmv_dia(DevCsr a, const double* 
   __shared__ double blk[NS];
   __shared__ double redv[NS];
   block_totals<NS>(part, blk, scratch);
-  if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv)) return;
+  if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv, red.xred)) return;
   finalize_spmv<S>(fin, redv, ds);
 }
 
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_dia_tma(DevCsr a, const double*
       for (int d = 0; d < 16; ++d) {
         if (d < nd) {
           int64_t col = row + s_off[d];
-          col = col < 0 ? 0 : (col >= n ? n - 1 : col);  // out-of-range slots hold 0.0
+          col = col < a.xlo ? a.xlo : (col >= a.xhi ? a.xhi - 1 : col);  // out-of-range slots hold 0.0
           xv[d] = __ldg(x + col);
         }
       }
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_dia_tma(DevCsr a, const double*
   __shared__ double blk[NS];
   __shared__ double redv[NS];
   block_totals<NS>(part, blk, scratch);
-  if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv)) return;
+  if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv, red.xred)) return;
   finalize_spmv<S>(fin, redv, ds);
 }
 
@@ -318,7 +318,21 @@ void launch_dia_tma(cudaStream_t st, const DevCsr& a, const double* x, double* y
   kfn<<<grid, kBlock, smem, st>>>(a, x, y, p, ld, b, T, fin, red);
 }
 
+// Row-sharded finaliser of an SpMV reduction: the allreduced totals (ds->xred) run through the
+// same finalize_spmv tail the fused kernels run in their last CTA.
+template <int S>
+__global__ void __launch_bounds__(kBlock) k_fin_spmv(FinParams fin, DevState* ds) {
+  __shared__ double redv[S + 1];
+  if (threadIdx.x <= S) redv[threadIdx.x] = ds->xred[threadIdx.x];
+  __syncthreads();
+  finalize_spmv<S>(fin, redv, ds);
+}
+
 }  // namespace
+
+void launch_fin_spmv(cudaStream_t st, int s, const FinParams& fin, DevState* ds) {
+  MSTAB_DISPATCH_S(s, { launch_pdl(k_fin_spmv<S>, 1, kBlock, 0, st, fin, ds); });
+}
 
 void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
                     int64_t ld, int s, const double* b, const FinParams& fin, const Reducer& red) {

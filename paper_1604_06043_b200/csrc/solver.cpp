@@ -42,6 +42,11 @@ void check_launch() {
 
 int64_t padded_ld(int64_t n) { return std::max<int64_t>(64, (n + 63) & ~int64_t(63)); }
 
+uint64_t next_operator_uid() {
+  static std::atomic<uint64_t> next{1};
+  return next.fetch_add(1);
+}
+
 StreamHolder::~StreamHolder() {
   if (stream) {
     cudaStreamSynchronize(stream);
@@ -85,6 +90,15 @@ Context::~Context() {
 
 void Context::sync() { CUDA_OK(cudaStreamSynchronize(stream())); }
 
+DevPtr Context::alloc_vecs(int64_t n, int64_t cols) {
+  DevPtr d = alloc(sizeof(double) * (size_t)ld(n) * (size_t)std::max<int64_t>(cols, 1));
+  if (n == lay_n) {  // slab vector: owned rows after lay_lo halo rows; halos start out zero
+    d->off = lay_lo;
+    CUDA_OK(cudaMemsetAsync(d->ptr, 0, d->bytes, stream()));
+  }
+  return d;
+}
+
 // ---- small device<->host helpers ----------------------------------------------------------
 void reset_status(Context& ctx) {
   CUDA_OK(cudaMemsetAsync(ctx.ds(), 0, sizeof(CycleStatus), ctx.stream()));
@@ -112,9 +126,52 @@ namespace {
 
 DevPtr copy_block(Context& ctx, const DevPtr& src, int64_t n, int64_t cols) {
   DevPtr dst = ctx.alloc_vecs(n, cols);
-  CUDA_OK(cudaMemcpyAsync(dst->ptr, src->ptr, sizeof(double) * (size_t)padded_ld(n) * cols,
+  CUDA_OK(cudaMemcpyAsync(dst->ptr, src->ptr, sizeof(double) * (size_t)ctx.ld(n) * cols,
                           cudaMemcpyDeviceToDevice, ctx.stream()));
   return dst;
+}
+
+// ---- row-sharded solves: what follows a reduction kernel / precedes an SpMV -------------------
+// On one GPU (no communicator) the kernels finish their reductions themselves and these are
+// no-ops. Sharded, the kernels leave rank-local totals in ds->xred; these sum them over the
+// ranks and run the dense tail the fused kernel would have run.
+double* xred(Context& ctx) { return ctx.ds()->xred; }
+
+void halo(Context& ctx, const Operator& op, const double* x) {
+  if (ctx.sharded()) ctx.comm->halo(const_cast<double*>(x), op.halo, ctx.stream());
+}
+void after_spmv(Context& ctx, int s, bool tres, const FinParams& f) {
+  if (!ctx.sharded()) return;
+  ctx.comm->allreduce_sum(xred(ctx), s + (tres ? 1 : 0), ctx.stream());
+  launch_fin_spmv(ctx.stream(), s, f, ctx.ds());
+  check_launch();
+}
+void after_poly(Context& ctx, int s) {
+  if (!ctx.sharded()) return;
+  ctx.comm->allreduce_sum(xred(ctx), 1 + s + s * s, ctx.stream());
+  launch_fin_poly(ctx.stream(), s, ctx.ds());
+  check_launch();
+}
+void after_ls(Context& ctx, int ell, int s) {
+  if (!ctx.sharded()) return;
+  const int cnt = ls_split_count(ell);
+  ctx.comm->allgather(xred(ctx), ctx.xgath->d(), cnt, ctx.stream());
+  launch_fin_ls(ctx.stream(), ell, s, ctx.comm->world(), ctx.xgath->d(), ctx.ds());
+  check_launch();
+}
+// dots (launch_dots layout: slots 0..na-1, the norm in slot kMaxS) -> dst[0..na(+1))
+void after_dots(Context& ctx, int na, bool with_norm, double* dst) {
+  if (!ctx.sharded()) return;
+  ctx.comm->allreduce_sum(xred(ctx), kMaxS + 1, ctx.stream());
+  if (na > 0) launch_fin_copy(ctx.stream(), xred(ctx), dst, na);
+  if (with_norm) launch_fin_copy(ctx.stream(), xred(ctx) + kMaxS, dst + na, 1);
+  check_launch();
+}
+void after_stats(Context& ctx, double* dst) {
+  if (!ctx.sharded()) return;
+  ctx.comm->allreduce_sum(xred(ctx), 3, ctx.stream());
+  launch_fin_copy(ctx.stream(), xred(ctx), dst, 3);
+  check_launch();
 }
 
 // Plain SpMV through the fused kernel (s = 1, dot with x discarded).
@@ -123,15 +180,25 @@ void spmv_dev(Context& ctx, const Operator& op, const double* x, double* y) {
   f.op = kFinStore;
   f.s = 1;
   f.dst = scal(ctx, 63);
-  launch_spmv_ph(ctx.stream(), op.csr(), x, y, x, padded_ld(op.n), 1, nullptr, f, ctx.reducer());
+  halo(ctx, op, x);
+  launch_spmv_ph(ctx.stream(), op.csr(), x, y, x, ctx.ld(op.n), 1, nullptr, f, ctx.reducer());
   check_launch();
+  after_spmv(ctx, 1, false, f);
 }
 
 // ||y||^2 -> scal[i]
 void norm2sq(Context& ctx, int64_t n, const double* y, int i) {
-  launch_dots(ctx.stream(), n, padded_ld(n), nullptr, 0, y, true, scal(ctx, i), ctx.reducer());
+  launch_dots(ctx.stream(), n, ctx.ld(n), nullptr, 0, y, true, scal(ctx, i), ctx.reducer());
   check_launch();
+  after_dots(ctx, 0, true, scal(ctx, i));
 }
+
+// Host draws of a length-n_global column restricted to this context's rows (RNG parity: every
+// rank draws the whole sequence in the reference's order and keeps its slab).
+const double* own_rows(const Context& ctx, int64_t n, const double* global) {
+  return (n == ctx.lay_n) ? global + ctx.lay_row0 : global;
+}
+int64_t draw_len(const Context& ctx, int64_t n) { return (n == ctx.lay_n) ? ctx.lay_nglobal : n; }
 
 }  // namespace
 
@@ -139,17 +206,19 @@ void norm2sq(Context& ctx, int64_t n, const double* y, int i) {
 // std::normal_distribution, column-major, so P's draws are the reference's) orthonormalised on
 // the device by classical Gram-Schmidt applied twice (orthonormalize, kernels.cpp:21-50).
 DevPtr make_cut_space(Context& ctx, int64_t n, int s, uint64_t seed) {
-  const int64_t ld = padded_ld(n);
+  const int64_t ld = ctx.ld(n);
   cudaStream_t st = ctx.stream();
   NormalStream* rng = normal_stream_create(seed);
   std::unique_ptr<NormalStream, void (*)(NormalStream*)> guard(rng, normal_stream_destroy);
-  std::vector<double> g((size_t)n * s);
+  const int64_t ng = draw_len(ctx, n);  // column-major draws over the GLOBAL rows
+  std::vector<double> g((size_t)ng * s);
   DevPtr G = ctx.alloc_vecs(n, s);
   DevPtr Q = ctx.alloc_vecs(n, s);
   for (int attempt = 0; attempt < 4; ++attempt) {
     normal_stream_fill(rng, g.data(), (int64_t)g.size());
-    CUDA_OK(cudaMemcpy2DAsync(G->ptr, sizeof(double) * ld, g.data(), sizeof(double) * n,
+    CUDA_OK(cudaMemcpy2DAsync(G->d(), sizeof(double) * ld, own_rows(ctx, n, g.data()), sizeof(double) * ng,
                               sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaStreamSynchronize(st));  // g is refilled by the next attempt
     int rank = 0;
     for (int j = 0; j < s; ++j) {
       const double* gj = G->d() + (size_t)j * ld;
@@ -158,6 +227,8 @@ DevPtr make_cut_space(Context& ctx, int64_t n, int s, uint64_t seed) {
       CUDA_OK(cudaMemcpyAsync(w, gj, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
       for (int pass = 0; pass < 2 && rank > 0; ++pass) {
         launch_dots(st, n, ld, Q->d(), rank, w, false, scal(ctx, 8), ctx.reducer());
+        check_launch();
+        after_dots(ctx, rank, false, scal(ctx, 8));
         launch_axpy_neg(st, n, ld, Q->d(), rank, scal(ctx, 8), w);
         check_launch();
       }
@@ -178,7 +249,7 @@ DevPtr make_cut_space(Context& ctx, int64_t n, int s, uint64_t seed) {
 // V = A U from the same sweep, happy breakdowns padded with seeded Gaussian directions.
 void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s, uint64_t seed,
                   double* U, double* V) {
-  const int64_t n = op.n, ld = padded_ld(n);
+  const int64_t n = op.n, ld = ctx.ld(n);
   cudaStream_t st = ctx.stream();
   norm2sq(ctx, n, r0, 0);
   if (read_scal(ctx, 1)[0] == 0.0) throw Error(MSTAB_E_ERROR, "arnoldi_init: zero start vector");
@@ -191,6 +262,8 @@ void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s, uin
     for (int pass = 0; pass < 2; ++pass)
       for (int i = 0; i <= k; ++i) {
         launch_dots(st, n, ld, U + (size_t)i * ld, 1, w->d(), false, scal(ctx, 2), ctx.reducer());
+        check_launch();
+        after_dots(ctx, 1, false, scal(ctx, 2));
         launch_axpy_neg(st, n, ld, U + (size_t)i * ld, 1, scal(ctx, 2), w->d());
         check_launch();
       }
@@ -198,7 +271,7 @@ void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s, uin
   for (int k = 0; k < s; ++k) {
     spmv_dev(ctx, op, U + (size_t)k * ld, V + (size_t)k * ld);
     if (k + 1 == s) break;
-    CUDA_OK(cudaMemcpyAsync(w->ptr, V + (size_t)k * ld, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(w->d(), V + (size_t)k * ld, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     norm2sq(ctx, n, w->d(), 1);
     mgs2(k);
     norm2sq(ctx, n, w->d(), 3);
@@ -207,9 +280,10 @@ void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s, uin
     double wnorm = std::sqrt(h[3]);
     while (wnorm <= 1e-12 * std::max(wnorm0, 1.0)) {
       if (!rng) rng.reset(normal_stream_create(seed));
-      hw.resize(n);
-      normal_stream_fill(rng.get(), hw.data(), n);
-      CUDA_OK(cudaMemcpyAsync(w->ptr, hw.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      hw.resize(draw_len(ctx, n));
+      normal_stream_fill(rng.get(), hw.data(), (int64_t)hw.size());
+      CUDA_OK(cudaMemcpyAsync(w->d(), own_rows(ctx, n, hw.data()), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      CUDA_OK(cudaStreamSynchronize(st));
       mgs2(k);
       norm2sq(ctx, n, w->d(), 3);
       wnorm = std::sqrt(read_scal(ctx, 4)[3]);
@@ -225,7 +299,8 @@ namespace {
 void enqueue_cycle(Context& ctx, const Operator& op, const double* P, int s, int ell,
                    const WSet& S, const WSet& D, const std::vector<DevPtr>& R,
                    const std::vector<DevPtr>& VL) {
-  const int64_t n = op.n, ld = padded_ld(n);
+  const int64_t n = op.n, ld = ctx.ld(n);
+  const bool shard = ctx.sharded();
   cudaStream_t st = ctx.stream();
   DevState* ds = ctx.ds();
   const Reducer red = ctx.reducer();
@@ -244,7 +319,9 @@ void enqueue_cycle(Context& ctx, const Operator& op, const double* P, int s, int
     fb.s = s;
     fb.k = k;
     fb.ell = ell;
+    if (shard) halo(ctx, op, r_out);
     launch_spmv_ph(st, A, r_out, R[k + 1]->d(), P, ld, s, nullptr, fb, red);
+    if (shard) after_spmv(ctx, s, false, fb);
     // (c) column rebuilds at the top level, each raised by one SpMV
     for (int q = 0; q < s; ++q) {
       launch_rebuild_top(st, n, ld, s, q, R[k + 1]->d(), vk_old, vk_new, VL[k + 1]->d(), ds);
@@ -254,7 +331,9 @@ void enqueue_cycle(Context& ctx, const Operator& op, const double* P, int s, int
       fc.k = k;
       fc.q = q;
       fc.ell = ell;
+      if (shard) halo(ctx, op, col(vk_new, q));
       launch_spmv_ph(st, A, col(vk_new, q), col(VL[k + 1]->d(), q), P, ld, s, nullptr, fc, red);
+      if (shard) after_spmv(ctx, s, false, fc);
     }
     // deferred (a) for r^(0..k-1), x and (c) for levels -1..k-1
     const double* lv_in[kMaxEll + 2];
@@ -284,20 +363,23 @@ void enqueue_cycle(Context& ctx, const Operator& op, const double* P, int s, int
   rr[0] = D.r->d();
   for (int i = 1; i <= ell; ++i) rr[i] = R[i]->d();
   launch_ls(st, n, ld, ell, s, rr, red);
+  if (shard) after_ls(ctx, ell, s);
   const double* lv[kMaxEll + 2];
   lv[0] = D.U->d();
   lv[1] = D.V->d();
   for (int i = 1; i <= ell; ++i) lv[i + 1] = VL[i]->d();
   launch_poly(st, n, ld, s, ell, lv, D.U->d(), D.V->d(), rr, D.r->d(), D.x->d(), D.x->d(), P, red);
   check_launch();
+  if (shard) after_poly(ctx, s);
 }
 
 }  // namespace
 
-std::shared_ptr<Operator> make_operator(Context& ctx, int64_t n, const int64_t* row_ptr,
-                                        const int64_t* col_idx, const double* values) {
+namespace {
+
+// CsrMatrix::validate (csr.cpp:11-24) on the host arrays; returns nnz.
+int64_t validate_csr(int64_t n, const int64_t* row_ptr, const int64_t* col_idx) {
   if (n < 0) throw Error(MSTAB_E_DIMENSION, "CsrOperator: negative size");
-  // CsrMatrix::validate (csr.cpp:11-24)
   if (row_ptr[0] != 0) throw Error(MSTAB_E_ERROR, "csr: row_ptr bounds");
   const int64_t nnz = row_ptr[n];
   for (int64_t i = 0; i < n; ++i) {
@@ -308,13 +390,17 @@ std::shared_ptr<Operator> make_operator(Context& ctx, int64_t n, const int64_t* 
         throw Error(MSTAB_E_ERROR, "csr: columns not strictly increasing within a row");
     }
   }
+  return nnz;
+}
+
+// Uploads n local rows (row_ptr from 0, column indices relative to the first owned row, so a
+// slab's halo columns are negative or >= n) and builds the DIA / constant-diagonal forms.
+void upload_rows(Context& ctx, Operator* op, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                 const double* values) {
+  const int64_t nnz = row_ptr[n];
   if (nnz >= (int64_t(1) << 31)) throw Error(MSTAB_E_CONFIG, "b200: nnz >= 2^31 not supported (int32 indices)");
-  static std::atomic<uint64_t> next_uid{1};
-  auto op = std::make_shared<Operator>();
-  op->uid = next_uid.fetch_add(1);
   op->n = n;
   op->nnz = nnz;
-  op->fingerprint = fnv_csr_fingerprint(n, row_ptr, col_idx, values, nnz);
   std::vector<int32_t> rp32(n + 1), ci32(nnz + 32, 0);
   for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)row_ptr[i];
   for (int64_t k = 0; k < nnz; ++k) ci32[k] = (int32_t)col_idx[k];
@@ -346,7 +432,7 @@ std::shared_ptr<Operator> make_operator(Context& ctx, int64_t n, const int64_t* 
     if (ok && (double)offs.size() * (double)n <= 1.5 * (double)nnz) {
       std::sort(offs.begin(), offs.end());
       const int nd = (int)offs.size();
-      const int64_t ld = padded_ld(n);
+      const int64_t ld = ctx.ld(n);
       std::vector<int32_t> off32(offs.begin(), offs.end());
       op->offsets = off32;
       op->ndiag = nd;
@@ -403,6 +489,83 @@ std::shared_ptr<Operator> make_operator(Context& ctx, int64_t n, const int64_t* 
     }
   }
   ctx.sync();
+}
+
+}  // namespace
+
+std::shared_ptr<Operator> make_operator(Context& ctx, int64_t n, const int64_t* row_ptr,
+                                        const int64_t* col_idx, const double* values) {
+  const int64_t nnz = validate_csr(n, row_ptr, col_idx);
+  static_cast<void>(nnz);
+  auto op = std::make_shared<Operator>();
+  op->uid = next_operator_uid();
+  op->fingerprint = fnv_csr_fingerprint(n, row_ptr, col_idx, values, row_ptr[n]);
+  op->n_global = n;
+  op->xlo = 0;
+  op->xhi = n;
+  upload_rows(ctx, op.get(), n, row_ptr, col_idx, values);
+  return op;
+}
+
+// Row slab of rank r: the rank's rows with columns relative to its first row,
+// the halo column range its rows reference, and the exchange plan. The send side is derived from
+// the peers' rows of the same global CSR, so the plans of all ranks match by construction.
+std::shared_ptr<Operator> make_operator_slab(Context& ctx, int64_t n, const int64_t* row_ptr,
+                                             const int64_t* col_idx, const double* values,
+                                             const int64_t* slabs) {
+  if (!ctx.comm) throw Error(MSTAB_E_CONFIG, "slab operator: the context has no communicator");
+  const int world = ctx.comm->world(), rank = ctx.comm->rank();
+  validate_csr(n, row_ptr, col_idx);
+  if (slabs[0] != 0 || slabs[world] != n) throw Error(MSTAB_E_DIMENSION, "slab operator: boundaries must span 0..n");
+  for (int r = 0; r < world; ++r)
+    if (slabs[r] > slabs[r + 1]) throw Error(MSTAB_E_DIMENSION, "slab operator: boundaries not ascending");
+  // column span [lo, hi) referenced by each rank's rows (at least its own rows)
+  std::vector<int64_t> lo(world), hi(world);
+  for (int r = 0; r < world; ++r) {
+    lo[r] = slabs[r];
+    hi[r] = slabs[r + 1];
+    for (int64_t k = row_ptr[slabs[r]]; k < row_ptr[slabs[r + 1]]; ++k) {
+      lo[r] = std::min(lo[r], col_idx[k]);
+      hi[r] = std::max(hi[r], col_idx[k] + 1);
+    }
+  }
+  const int64_t start = slabs[rank], end = slabs[rank + 1], nl = end - start;
+  if (nl < 1) throw Error(MSTAB_E_DIMENSION, "slab operator: empty slab");
+  auto op = std::make_shared<Operator>();
+  op->uid = next_operator_uid();
+  op->fingerprint = fnv_csr_fingerprint(n, row_ptr, col_idx, values, row_ptr[n]);
+  op->n_global = n;
+  op->row0 = start;
+  op->xlo = lo[rank] - start;
+  op->xhi = hi[rank] - start;
+  auto overlap = [](int64_t a0, int64_t a1, int64_t b0, int64_t b1, int64_t& o0, int64_t& o1) {
+    o0 = std::max(a0, b0);
+    o1 = std::min(a1, b1);
+    return o0 < o1;
+  };
+  for (int p = 0; p < world; ++p) {
+    if (p == rank) continue;
+    int64_t o0, o1;
+    // halo rows of mine owned by p (left and right of my slab)
+    if (overlap(lo[rank], start, slabs[p], slabs[p + 1], o0, o1)) op->halo.recvs.push_back({p, o0 - start, o1 - o0});
+    if (overlap(end, hi[rank], slabs[p], slabs[p + 1], o0, o1)) op->halo.recvs.push_back({p, o0 - start, o1 - o0});
+    // my rows that p references outside its slab
+    if (overlap(lo[p], slabs[p], start, end, o0, o1)) op->halo.sends.push_back({p, o0 - start, o1 - o0});
+    if (overlap(slabs[p + 1], hi[p], start, end, o0, o1)) op->halo.sends.push_back({p, o0 - start, o1 - o0});
+  }
+  // vector layout of this context: owned rows after a 64-aligned left halo
+  ctx.lay_n = nl;
+  ctx.lay_lo = (start - lo[rank] + 63) / 64 * 64;
+  ctx.lay_ld = padded_ld(ctx.lay_lo + nl + (hi[rank] - end));
+  ctx.lay_row0 = start;
+  ctx.lay_nglobal = n;
+  ctx.ws.reset();
+  ctx.pcache.reset();
+  std::vector<int64_t> rp(nl + 1), ci(row_ptr[end] - row_ptr[start]);
+  for (int64_t i = 0; i <= nl; ++i) rp[i] = row_ptr[start + i] - row_ptr[start];
+  for (size_t k = 0; k < ci.size(); ++k) ci[k] = col_idx[row_ptr[start] + (int64_t)k] - start;
+  upload_rows(ctx, op.get(), nl, rp.data(), ci.data(), values + row_ptr[start]);
+  if (!ctx.xgath) ctx.xgath = ctx.alloc(sizeof(double) * (size_t)world * kMaxXred);
   return op;
 }
 
@@ -419,9 +582,16 @@ mstab_validation_report validate(Context& ctx, const Recycle& rd, const Operator
     throw Error(MSTAB_E_STALE, "recycle data: omega history length disagrees with level");
   const int s = (int)rd.s;
   if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: recycle s must be in 1..16");
-  launch_validate(ctx.stream(), op.csr(), rd.p->d(), rd.u->d(), rd.v->d(), padded_ld(rd.n), s,
-                  ctx.reducer());
+  const int64_t vld = ctx.ld(rd.n);
+  for (int q = 0; q < s && ctx.sharded(); ++q) halo(ctx, op, rd.u->d() + (size_t)q * vld);
+  launch_validate(ctx.stream(), op.csr(), rd.p->d(), rd.u->d(), rd.v->d(), vld, s, ctx.reducer());
   check_launch();
+  if (ctx.sharded()) {
+    ctx.comm->allreduce_sum(xred(ctx), 2 + 2 * s * s, ctx.stream());
+    launch_fin_copy(ctx.stream(), xred(ctx), ctx.ds()->scal, 2);
+    launch_fin_copy(ctx.stream(), xred(ctx) + 2, ctx.ds()->gram, 2 * s * s);
+    check_launch();
+  }
   std::vector<double> gram(2 * (size_t)s * s);
   CUDA_OK(cudaMemcpyAsync(gram.data(), ctx.ds()->gram, sizeof(double) * gram.size(),
                           cudaMemcpyDeviceToHost, ctx.stream()));
@@ -492,9 +662,11 @@ void enqueue_full_cycle(Context& ctx, const Operator& op, Workspace& w, int p) {
     ft.op = kFinTrueRes;
     ft.s = w.s;
     ft.ell = w.ell;
-    launch_spmv_ph(ctx.stream(), op.csr(), D.x->d(), D.r->d(), w.P->d(), padded_ld(op.n), w.s, w.b->d(), ft,
+    halo(ctx, op, D.x->d());
+    launch_spmv_ph(ctx.stream(), op.csr(), D.x->d(), D.r->d(), w.P->d(), ctx.ld(op.n), w.s, w.b->d(), ft,
                    ctx.reducer());
     check_launch();
+    after_spmv(ctx, w.s, true, ft);
   }
 }
 
@@ -502,7 +674,7 @@ void enqueue_full_cycle(Context& ctx, const Operator& op, Workspace& w, int p) {
 // launches the kernels directly when graphs are off.
 void run_cycle(Context& ctx, const Operator& op, Workspace& w, int p) {
   cudaStream_t st = ctx.stream();
-  if (!ctx.use_graphs) {
+  if (!ctx.use_graphs || (ctx.comm && !ctx.comm->capturable())) {
     enqueue_full_cycle(ctx, op, w, p);
     return;
   }
@@ -538,7 +710,7 @@ void run_cycle(Context& ctx, const Operator& op, Workspace& w, int p) {
 
 DevPtr copy_vec(Context& ctx, const DevPtr& src, int64_t n) {
   DevPtr d = ctx.alloc_vecs(n, 1);
-  CUDA_OK(cudaMemcpyAsync(d->ptr, src->ptr, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx.stream()));
+  CUDA_OK(cudaMemcpyAsync(d->d(), src->d(), sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx.stream()));
   return d;
 }
 
@@ -557,17 +729,18 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   if (fetch && fetch->kind == MSTAB_FETCH_AT_CYCLE && fetch->cycle < 1)
     throw Error(MSTAB_E_CONFIG, "fetch policy: cycle >= 1 required");
   const int s = (int)cfg.s, ell = (int)cfg.ell;
-  const int64_t n = op.n, ld = padded_ld(n);
+  const int64_t n = op.n, ld = ctx.ld(n);
   cudaStream_t st = ctx.stream();
   const bool tres = cfg.true_residual_each_cycle != 0;
   Workspace& w = workspace(ctx, op, s, ell, tres);
   reset_status(ctx);
 
   // b: ensure_finite + bnorm (idrstab.cpp:200, :205)
-  CUDA_OK(cudaMemcpyAsync(w.b->ptr, b_in, sizeof(double) * n,
+  CUDA_OK(cudaMemcpyAsync(w.b->d(), b_in, sizeof(double) * n,
                           mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   launch_vec_stats(st, n, w.b->d(), scal(ctx, 0), ctx.reducer());
   check_launch();
+  after_stats(ctx, scal(ctx, 0));
   const double* h = read_scal(ctx, 3);
   if (h[1] > 0.0) throw Error(MSTAB_E_ERROR, "idrstab rhs: non-finite entries");
   const auto t0 = Clock::now();
@@ -582,10 +755,11 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   WSet& c0 = w.set[0];
   bool x_zero = true;
   if (x0_in) {
-    CUDA_OK(cudaMemcpyAsync(c0.x->ptr, x0_in, sizeof(double) * n,
+    CUDA_OK(cudaMemcpyAsync(c0.x->d(), x0_in, sizeof(double) * n,
                             mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     launch_vec_stats(st, n, c0.x->d(), scal(ctx, 0), ctx.reducer());
     check_launch();
+    after_stats(ctx, scal(ctx, 0));
     const double* hx = read_scal(ctx, 3);
     x_zero = hx[2] == 0.0;
     if (!x_zero && hx[1] > 0.0) throw Error(MSTAB_E_ERROR, "idrstab guess: non-finite entries");
@@ -593,7 +767,7 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
     CUDA_OK(cudaMemsetAsync(c0.x->ptr, 0, sizeof(double) * ld, st));
   }
   if (x_zero) {
-    CUDA_OK(cudaMemcpyAsync(c0.r->ptr, w.b->ptr, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(c0.r->d(), w.b->d(), sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   } else {  // r = b - A x0, one auxiliary MV (idrstab.cpp:210-216)
     spmv_dev(ctx, op, c0.x->d(), c0.r->d());
     launch_rsub(st, n, w.b->d(), c0.r->d());
@@ -641,6 +815,7 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   reset_status(ctx);
   launch_prologue(st, n, ld, s, w.P->d(), c0.V->d(), c0.r->d(), ctx.reducer());
   check_launch();
+  after_poly(ctx, s);
   double resnorm = read_status(ctx).resnorm;
   int64_t level = 0;
   res->history.push_back({0, rep.h_mv + rep.h_mv_aux, base_level, resnorm, ns_since(t0)});

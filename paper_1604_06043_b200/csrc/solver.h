@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../../include/mstab_b200.h"
+#include "comm.h"
 #include "device_state.h"
 #include "host_util.h"
 #include "kernels.h"
@@ -19,12 +20,13 @@ namespace mstab_b200 {
 struct DevMem {
   void* ptr = nullptr;
   size_t bytes = 0;
+  int64_t off = 0;  // elements before the owned rows (left halo of a row-sharded vector)
   std::shared_ptr<struct StreamHolder> stream;
   DevMem(std::shared_ptr<StreamHolder> st, size_t b);
   ~DevMem();
   DevMem(const DevMem&) = delete;
   DevMem& operator=(const DevMem&) = delete;
-  double* d() const { return static_cast<double*>(ptr); }
+  double* d() const { return static_cast<double*>(ptr) + off; }
 };
 using DevPtr = std::shared_ptr<DevMem>;
 
@@ -78,13 +80,19 @@ struct Context {
   DevPtr pcache;                       // last make_cut_space result (immutable)
   int64_t pcache_n = -1, pcache_s = -1;
   uint64_t pcache_seed = 0;
+  // Row-sharded solves (comm.h): the communicator and the vector layout of the slab operator.
+  // Vectors of length lay_n (the slab's rows) get lay_lo halo rows in front of the owned rows
+  // and column stride lay_ld; DevMem::d() points at the first owned row.
+  std::unique_ptr<Comm> comm;
+  DevPtr xgath;  // allgather landing buffer (world * kMaxXred doubles)
+  int64_t lay_n = -1, lay_lo = 0, lay_ld = 0, lay_row0 = 0, lay_nglobal = 0;
+  bool sharded() const { return comm && comm->world() > 1; }
+  int64_t ld(int64_t n) const { return n == lay_n ? lay_ld : padded_ld(n); }
   cudaStream_t stream() const { return sh->stream; }
   DevState* ds() const { return static_cast<DevState*>(ds_mem->ptr); }
-  Reducer reducer() const { return Reducer{partials->d(), ds()}; }
+  Reducer reducer() const { return Reducer{partials->d(), ds(), sharded() ? ds()->xred : nullptr}; }
   DevPtr alloc(size_t bytes) { return std::make_shared<DevMem>(sh, bytes); }
-  DevPtr alloc_vecs(int64_t n, int64_t cols) {
-    return alloc(sizeof(double) * (size_t)padded_ld(n) * (size_t)std::max<int64_t>(cols, 1));
-  }
+  DevPtr alloc_vecs(int64_t n, int64_t cols);
   void sync();
   explicit Context(int device);
   ~Context();
@@ -95,10 +103,15 @@ struct Operator {
   int64_t n = 0, nnz = 0;
   uint64_t fingerprint = 0;
   DevPtr rp, ci, val;
+  // row slab (mstab_operator_create_csr_slab): global size, first row, x index range, halo plan
+  int64_t n_global = 0, row0 = 0, xlo = 0, xhi = 0;
+  HaloPlan halo;
   DevCsr csr() const {
     DevCsr c;
     c.n = n;
     c.nnz = nnz;
+    c.xlo = xlo;
+    c.xhi = xhi;
     c.row_ptr = static_cast<const int32_t*>(rp->ptr);
     c.col_idx = static_cast<const int32_t*>(ci->ptr);
     c.values = val->d();
@@ -156,6 +169,10 @@ mstab_validation_report validate(Context& ctx, const Recycle& rd, const Operator
 
 std::shared_ptr<Operator> make_operator(Context& ctx, int64_t n, const int64_t* row_ptr,
                                         const int64_t* col_idx, const double* values);
+// Row slab of rank ctx.comm->rank() (slab_starts: world + 1 ascending boundaries).
+std::shared_ptr<Operator> make_operator_slab(Context& ctx, int64_t n, const int64_t* row_ptr,
+                                             const int64_t* col_idx, const double* values,
+                                             const int64_t* slab_starts);
 
 void spmv(Context& ctx, const Operator& op, const double* x_dev, double* y_dev);
 

@@ -169,10 +169,99 @@ class Context:
     def stream(self) -> int:
         return self.lib.dll.mstab_context_stream(self.h) or 0
 
+    # ---- row-sharded solves (include/mstab_b200.h) --------------------------
+    @staticmethod
+    def nccl_unique_id(lib: Optional[Lib] = None) -> bytes:
+        lib = lib if lib is not None else Lib()
+        buf = (C.c_uint8 * 128)()
+        _check(lib, lib.dll.mstab_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def set_comm_nccl(self, rank: int, world: int, unique_id: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        _check(self.lib, self.lib.dll.mstab_context_set_comm_nccl(self.h, int(rank), int(world), buf))
+
+    def set_comm_host(self, rank: int, world: int, comm):
+        """`comm` provides allreduce_sum(buf), allgather(inp, out) and halo_exchange(sends, recvs)
+        on numpy float64 arrays (sends / recvs: lists of (peer, array)); see TorchHostComm."""
+        self._host_comm = _HostCommAdaptor(comm)  # keeps the ctypes callbacks alive
+        _check(self.lib, self.lib.dll.mstab_context_set_comm_host(self.h, int(rank), int(world),
+                                                                  C.byref(self._host_comm.c)))
+
+    def comm_info(self):
+        r, w = C.c_int32(), C.c_int32()
+        _check(self.lib, self.lib.dll.mstab_context_comm_info(self.h, C.byref(r), C.byref(w)))
+        return r.value, w.value
+
     def __del__(self):
         if getattr(self, "h", None):
             self.lib.dll.mstab_context_destroy(self.h)
             self.h = None
+
+
+class _HostCommAdaptor:
+    """ctypes trampolines from mstab_host_comm to a Python communicator object."""
+
+    def __init__(self, comm):
+        self.comm = comm
+        arr = np.ctypeslib.as_array
+
+        def allreduce(_u, buf, count):
+            try:
+                self.comm.allreduce_sum(arr(buf, shape=(count,)))
+                return 0
+            except Exception:  # noqa: BLE001 - reported to the library as a failed callback
+                return 1
+
+        def allgather(_u, inp, out, count):
+            try:
+                w = self.comm.world
+                self.comm.allgather(arr(inp, shape=(count,)), arr(out, shape=(count * w,)))
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        def halo(_u, ns, speers, sbufs, scounts, nr, rpeers, rbufs, rcounts):
+            try:
+                sends = [(int(speers[i]), arr(sbufs[i], shape=(int(scounts[i]),))) for i in range(ns)]
+                recvs = [(int(rpeers[i]), arr(rbufs[i], shape=(int(rcounts[i]),))) for i in range(nr)]
+                self.comm.halo_exchange(sends, recvs)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        self._fns = (_capi.HostCommC.ALLREDUCE(allreduce), _capi.HostCommC.ALLGATHER(allgather),
+                     _capi.HostCommC.HALO(halo))
+        self.c = _capi.HostCommC(None, *self._fns)
+
+
+class TorchHostComm:
+    """Host communicator over an initialised torch.distributed process group (gloo on CPU):
+    the staging side of a row-sharded solve for runtimes without NCCL (and the multi-rank tests,
+    which run every rank on one GPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+
+    def allreduce_sum(self, buf):
+        import torch
+        t = torch.from_numpy(buf)
+        self.dist.all_reduce(t, group=self.group)
+
+    def allgather(self, inp, out):
+        import torch
+        n = inp.size
+        outs = [torch.from_numpy(out[r * n:(r + 1) * n]) for r in range(self.world)]
+        self.dist.all_gather(outs, torch.from_numpy(inp.copy()), group=self.group)
+
+    def halo_exchange(self, sends, recvs):
+        import torch
+        reqs = [self.dist.isend(torch.from_numpy(a.copy()), p, group=self.group) for p, a in sends]
+        reqs += [self.dist.irecv(torch.from_numpy(b), p, group=self.group) for p, b in recvs]
+        for r in reqs:
+            r.wait()
 
 
 _default_ctx: dict = {}
@@ -265,16 +354,32 @@ class CsrMatrix:
 class CsrOperator:
     """LinearOperator over a CSR matrix (operator.hpp:33-50); uploaded once, fingerprint cached."""
 
-    def __init__(self, a: CsrMatrix, ctx: Optional[Context] = None):
+    def __init__(self, a: CsrMatrix, ctx: Optional[Context] = None, slabs=None):
+        """`slabs` (world + 1 ascending row boundaries) makes this the row slab of the context's
+        rank in a row-sharded solve (the context needs a communicator first)."""
         if a.n_rows != a.n_cols:
             raise DimensionMismatch("CsrOperator: square matrix required")
         self.ctx = ctx if ctx is not None else default_context()
         self.lib = self.ctx.lib
         self.matrix = a
         h = C.c_void_p()
-        _check(self.lib, self.lib.dll.mstab_operator_create_csr(
-            self.ctx.h, a.n_rows, i64ptr(a.row_ptr), i64ptr(a.col_idx), dptr(a.values), C.byref(h)))
+        if slabs is None:
+            _check(self.lib, self.lib.dll.mstab_operator_create_csr(
+                self.ctx.h, a.n_rows, i64ptr(a.row_ptr), i64ptr(a.col_idx), dptr(a.values), C.byref(h)))
+        else:
+            self._slabs = np.ascontiguousarray(slabs, dtype=np.int64)
+            _check(self.lib, self.lib.dll.mstab_operator_create_csr_slab(
+                self.ctx.h, a.n_rows, i64ptr(a.row_ptr), i64ptr(a.col_idx), dptr(a.values),
+                i64ptr(self._slabs), C.byref(h)))
         self.h = h
+
+    @property
+    def row_begin(self) -> int:
+        return int(self.lib.dll.mstab_operator_row_begin(self.h))
+
+    @property
+    def global_size(self) -> int:
+        return int(self.lib.dll.mstab_operator_global_size(self.h))
 
     def size(self) -> int:
         return int(self.lib.dll.mstab_operator_size(self.h))
