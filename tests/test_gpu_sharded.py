@@ -126,3 +126,22 @@ def test_sharded_matches_single_gpu(gpu_ctx, name, world):
         tr_s = np.linalg.norm(bb - op1.apply(xs)) / np.linalg.norm(bb)
         tr_1 = np.linalg.norm(bb - op1.apply(xr)) / np.linalg.norm(bb)
         assert tr_s <= max(1e-7, 10.0 * tr_1), (tr_s, tr_1)
+
+
+def test_nccl_communicator_single_rank(gpu_ctx):
+    """The NCCL communicator (libnccl resolved at run time) on one rank: init, a whole-matrix slab
+    and a solve through the sharded code path with world = 1 (no exchange needed); the result is
+    the single-GPU solve's bit for bit."""
+    cfg = pb.config("c1", grid=48)
+    A = cfg.matrix()
+    ctx = m.Context(m.Lib(), 0)
+    ctx.set_comm_nccl(0, 1, m.Context.nccl_unique_id())
+    assert ctx.comm_info() == (0, 1)
+    op = m.CsrOperator(A, ctx, slabs=[0, A.n_rows])
+    x0, f = cfg.sources()
+    b = cfg.first_rhs(x0, f)
+    sc = m.SolverConfig(cfg.s, cfg.ell, 1e-8, 100000, False, 0)
+    r = m.idrstab_solve(op, b, None, sc)
+    g = m.idrstab_solve(m.CsrOperator(A, gpu_ctx), b, None, sc)
+    assert r.report.status == m.CONVERGED and r.report.cycles == g.report.cycles
+    assert np.array_equal(r.x, g.x)
