@@ -226,91 +226,117 @@ __device__ bool dev_lu_solve(int s, double* a, const double* rhs, double* x) {
   return true;
 }
 
-// The same LU + solve, by one warp: lane i holds row i of the s x s system in registers
-// (MAXS >= s). Every element sees exactly the reference's operations in the reference's order
-// (pivot = first strictly larger magnitude, elimination with the pivot inverse, forward and
-// backward substitution with ascending j), so the result is bit-identical to dev_lu_solve; the
-// dependent chain shrinks from ~s^3/3 scalar steps to ~s^2 warp steps. Call with all 32 lanes;
-// a (col-major), rhs, x live in shared memory. Returns the (warp-uniform) non-singular flag.
+// The same LU + solve, by one warp, column-oriented: lane j holds column j of the s x s system in
+// registers (MAXS >= s). Every element sees exactly the reference's operations in the reference's
+// order — pivot = first strictly larger magnitude (searched sequentially by the lane that owns
+// the pivot column: no butterfly), elimination a_ij - (a_ik * inv) a_kj skipped for a zero
+// multiplier, forward substitution with ascending j, backward substitution with ascending j and a
+// final division — so the result is bit-identical to dev_lu_solve. The row interchange is applied
+// to the right-hand side as it happens (the same permutation as rhs[perm[i]]). Per elimination
+// step the only cross-lane traffic is the pivot index and the column of multipliers, so the
+// dependent chain is ~s steps of a few shuffles (the earlier row-per-lane version needed an
+// argmax butterfly and a row broadcast per step: ~7 us at s = 8). The substitutions run on lane 0
+// from shared memory. Call with all 32 lanes; a (col-major), rhs, x live in shared memory.
 template <int MAXS>
-__device__ bool warp_lu_solve(int s, const double* a, const double* rhs, double* x) {
+__device__ bool warp_lu_solve(int s, double* a, const double* rhs, double* x) {
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const bool mine = lane < s;
-  double row[MAXS];
+  double col[MAXS];
 #pragma unroll
-  for (int j = 0; j < MAXS; ++j) row[j] = (mine && j < s) ? a[lane + j * s] : 0.0;
-  int perm = lane;
-  double mx = 0.0;  // max |M| (std::max semantics: NaN entries never win)
+  for (int i = 0; i < MAXS; ++i) col[i] = (mine && i < s) ? a[i + lane * s] : 0.0;
+  double b[MAXS];
 #pragma unroll
-  for (int j = 0; j < MAXS; ++j) mx = dmax_ref(mx, fabs(row[j]));
+  for (int i = 0; i < MAXS; ++i) b[i] = i < s ? rhs[i] : 0.0;
+  // scale = max |a_ij| with std::max semantics (NaN never wins): order-independent
+  double mx = 0.0;
+#pragma unroll
+  for (int i = 0; i < MAXS; ++i) mx = dmax_ref(mx, fabs(col[i]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = dmax_ref(mx, __shfl_xor_sync(FULL, mx, o));
   const double scale = mx;
 #pragma unroll
   for (int k = 0; k < MAXS; ++k) {
     if (k >= s) break;
-    const double akk_abs = __shfl_sync(FULL, fabs(row[k]), k);
+    // pivot search on column k (lane k), rows k.. in order: first strictly larger magnitude
     int piv = k;
-    double best = akk_abs;
-    if (!isnan(akk_abs)) {  // first index with the largest magnitude among rows k.. (NaN never wins)
-      double m = (lane >= k && mine) ? fabs(row[k]) : -1.0;
-      if (isnan(m)) m = -1.0;
-      int idx = lane;
+    double best = fabs(col[k]);
+    if (lane == k) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double mo = __shfl_xor_sync(FULL, m, o);
-        const int io = __shfl_xor_sync(FULL, idx, o);
-        if (mo > m || (mo == m && io < idx)) {
-          m = mo;
-          idx = io;
+      for (int i = k + 1; i < MAXS; ++i) {
+        if (i < s) {
+          const double m = fabs(col[i]);
+          if (m > best) {
+            best = m;
+            piv = i;
+          }
         }
       }
-      piv = idx;
-      best = m;
     }
+    piv = __shfl_sync(FULL, piv, k);
+    best = __shfl_sync(FULL, best, k);
     if (best < 1e-14 * scale || scale == 0.0) return false;
-    if (piv != k) {
-      const int src = (lane == k) ? piv : ((lane == piv) ? k : lane);
+    if (piv != k) {  // swap rows k and piv in every column and in the right-hand side
+      double ck = col[k], cp = 0.0, bp = 0.0;
 #pragma unroll
-      for (int j = 0; j < MAXS; ++j) row[j] = __shfl_sync(FULL, row[j], src);
-      perm = __shfl_sync(FULL, perm, src);
+      for (int i = k + 1; i < MAXS; ++i)
+        if (i == piv) {
+          cp = col[i];
+          bp = b[i];
+        }
+#pragma unroll
+      for (int i = k + 1; i < MAXS; ++i)
+        if (i == piv) {
+          col[i] = ck;
+          b[i] = b[k];
+        }
+      col[k] = cp;
+      b[k] = bp;
     }
-    const double inv = 1.0 / __shfl_sync(FULL, row[k], k);
-    double rk[MAXS];
+    // multipliers m_i = a_ik * (1 / a_kk), stored in place (L), by the pivot-column lane
+    if (lane == k) {
+      const double inv = 1.0 / col[k];
 #pragma unroll
-    for (int j = 0; j < MAXS; ++j) rk[j] = __shfl_sync(FULL, row[j], k);
-    if (lane > k && mine) {
-      const double mm = row[k] * inv;
-      row[k] = mm;
-      if (mm != 0.0) {
+      for (int i = k + 1; i < MAXS; ++i)
+        if (i < s) col[i] = col[i] * inv;
+    }
+    // eliminate: lanes j > k update their column with the broadcast multipliers
+    const double akj = col[k];
 #pragma unroll
-        for (int j = 0; j < MAXS; ++j)
-          if (j > k && j < s) row[j] = row[j] - mm * rk[j];
-      }
+    for (int i = k + 1; i < MAXS; ++i) {
+      if (i >= s) break;
+      const double mi = __shfl_sync(FULL, col[i], k);
+      if (lane > k && mine && mi != 0.0) col[i] = col[i] - mi * akj;
     }
   }
-  double xv = mine ? rhs[perm] : 0.0;
+  // factors back to shared memory (col-major LU), then lane 0 substitutes in the reference order
 #pragma unroll
-  for (int j = 0; j < MAXS; ++j) {  // forward: lane i subtracts L(i,j) x_j for j = 0..i-1 in order
-    if (j >= s - 1) break;
-    const double xj = __shfl_sync(FULL, xv, j);
-    if (lane > j && mine) xv = xv - row[j] * xj;
-  }
+  for (int i = 0; i < MAXS; ++i)
+    if (mine && i < s) a[i + lane * s] = col[i];
+  __syncwarp();
+  if (lane == 0) {
+    double xv[MAXS];
 #pragma unroll
-  for (int i = MAXS - 1; i >= 0; --i) {  // backward: x_i -= U(i,j) x_j for j = i+1.. ascending
-    if (i >= s) continue;
-    double t = xv;
+    for (int i = 0; i < MAXS; ++i) xv[i] = b[i];
 #pragma unroll
-    for (int j = i + 1; j < MAXS; ++j) {
-      if (j >= s) break;
-      const double xj = __shfl_sync(FULL, xv, j);
-      t = t - row[j] * xj;
+    for (int i = 1; i < MAXS; ++i) {
+      if (i >= s) break;
+#pragma unroll
+      for (int j = 0; j < i; ++j) xv[i] = xv[i] - a[i + j * s] * xv[j];
     }
-    t = t / row[i];
-    if (lane == i) xv = t;
+#pragma unroll
+    for (int i = MAXS - 1; i >= 0; --i) {
+      if (i >= s) continue;
+#pragma unroll
+      for (int j = i + 1; j < MAXS; ++j)
+        if (j < s) xv[i] = xv[i] - a[i + j * s] * xv[j];
+      xv[i] = xv[i] / a[i + i * s];
+    }
+#pragma unroll
+    for (int i = 0; i < MAXS; ++i)
+      if (i < s) x[i] = xv[i];
   }
-  if (mine) x[lane] = xv;
+  __syncwarp();
   return true;
 }
 

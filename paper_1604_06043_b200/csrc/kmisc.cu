@@ -122,13 +122,15 @@ __global__ void k_axpby_chain(int64_t n, const double* __restrict__ x, const dou
     b[i] = x[i] + alpha * g[i];
 }
 
+template <int S>
 __global__ void k_small_solve(int s, const double* m, const double* rhs, double* x, int32_t* ok) {
-  // the warp LU the finalizers run (bit-identical to the scalar dev_lu_solve)
+  // the warp LU the finalizers run (bit-identical to the scalar dev_lu_solve), at the same
+  // compile-time size bound the finalizers use (MAXS = S)
   __shared__ double lu[kMaxS * kMaxS], vin[kMaxS], vout[kMaxS];
   for (int i = threadIdx.x; i < s * s; i += blockDim.x) lu[i] = m[i];
   if ((int)threadIdx.x < s) vin[threadIdx.x] = rhs[threadIdx.x];
   __syncwarp();
-  const bool r = warp_lu_solve<kMaxS>(s, lu, vin, vout);
+  const bool r = warp_lu_solve<S>(s, lu, vin, vout);
   __syncwarp();
   if ((int)threadIdx.x < s) x[threadIdx.x] = vout[threadIdx.x];
   if (threadIdx.x == 0) *ok = r ? 1 : 0;
@@ -336,7 +338,7 @@ void launch_fin_copy(cudaStream_t st, const double* src, double* dst, int count)
 void launch_small_solve(cudaStream_t st, int s, const double* m, const double* rhs, double* x,
                         int32_t* ok) {
   LaunchScope ls(st, kKOther, 0.0);
-  k_small_solve<<<1, 32, 0, st>>>(s, m, rhs, x, ok);
+  MSTAB_DISPATCH_S(s, { k_small_solve<S><<<1, 32, 0, st>>>(s, m, rhs, x, ok); });
 }
 
 namespace {
