@@ -44,6 +44,12 @@ struct DevState {
   // totals here instead of running the dense step; the host allreduces (or allgathers) them over
   // the ranks and launches the matching finaliser kernel (kernels.h launch_fin_*).
   double xred[kMaxXred];
+  // least squares (kls.cu): CholeskyQR2 state between its two passes
+  int32_t ls_mode;                      // 1: CholeskyQR2 path, 0: Givens TSQR fallback
+  int32_t _pad_ls;
+  double ls_r1[(kMaxEll + 1) * (kMaxEll + 2) / 2];     // first Cholesky factor (packed upper)
+  double ls_r1inv[(kMaxEll + 1) * (kMaxEll + 2) / 2];  // its inverse
+  double ls_cn[kMaxEll];                // column sums of squares of Z
   uint32_t ticket;             // last-CTA-done counter (reset by the finaliser)
   uint32_t tile_next;          // dynamic tile scheduler counter (reset by the finaliser)
 };

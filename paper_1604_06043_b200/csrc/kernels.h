@@ -134,7 +134,7 @@ void launch_fin_poly(cudaStream_t st, int s, DevState* ds);
 // dots / stats / validate: copy the reduced totals where the fused kernel would have stored them
 void launch_fin_copy(cudaStream_t st, const double* src, double* dst, int count);
 // LS: merge `world` rank-local R factors (+ column sums of squares) in rank order, then solve.
-void launch_fin_ls(cudaStream_t st, int ell, int s, int world, const double* gath, DevState* ds);
+void launch_fin_ls(cudaStream_t st, int ell, int s, int world, bool chol, const double* gath, DevState* ds);
 constexpr int ls_split_count(int ell) { return (ell + 1) * (ell + 2) / 2 + ell; }
 
 // step (a), top level only: r_out = r_in - V^(k) gamma (gemv + subtract, idrstab.cpp:113-117).
@@ -153,7 +153,18 @@ void launch_rebuild_deferred(cudaStream_t st, int64_t n, int64_t ld, int s, int 
                              const double* const* r_in, double* const* r_out, const double* x_in,
                              double* x_out, DevState* ds);
 
-// least_squares_tall(Z=[r^(1)..r^(ell)], r^(0)) by one-pass Givens TSQR + tail guard.
+// least_squares_tall(Z=[r^(1)..r^(ell)], r^(0)) by CholeskyQR2 (Givens TSQR fallback) + tail guard.
+// The same as two launches (CholeskyQR2 pass 1 / pass 2 with the Givens fallback), for callers
+// that reduce across ranks between them.
+void launch_ls_pass1(cudaStream_t st, int64_t n, int ell, const double* const* r, const Reducer& red);
+void launch_ls_pass2(cudaStream_t st, int64_t n, int ell, int s, bool chol, const double* const* r,
+                     const Reducer& red);
+// CholeskyQR2 for tall systems (the one-pass Givens TSQR costs a dependent chain of rotations
+// per row: 133 us at c2 against 35 us); small systems keep the Givens TSQR, whose rounding the
+// reference's own 1e-12 trajectory tests were calibrated against.
+constexpr int64_t kCholQrMinRows = 1 << 17;
+inline bool ls_use_cholqr(int64_t n_global) { return n_global >= kCholQrMinRows; }
+void launch_fin_ls1(cudaStream_t st, int ell, DevState* ds);
 void launch_ls(cudaStream_t st, int64_t n, int64_t ld, int ell, int s, const double* const* r,
                const Reducer& red);
 

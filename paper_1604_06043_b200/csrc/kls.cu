@@ -100,11 +100,158 @@ struct LsArgs {
   const double* r[kMaxEll + 1];  // r^(0..L)
 };
 
+// ---- CholeskyQR2 (two streaming passes, no Q stored) --------------------------------------------
+// Pass 1: G1 = Z^T Z of Z = [r^(1..L) | r^(0)] (packed upper, one deterministic reduction), then
+// R1 = chol(G1) and R1^-1. Pass 2: G2 = Q^T Q with Q = Z R1^-1 formed row by row, R2 = chol(G2),
+// R = R2 R1 (the R factor of Z to working accuracy while cond(Z) <~ 1e8). Used only when every
+// Cholesky pivot of G1 keeps more than kCholKeep of its column's squared norm;
+// otherwise pass 2 runs the one-pass Givens TSQR instead (same launch, ls_mode = 0), which also
+// owns the rank-deficiency regime of the reference's test (kernels.cpp:83-84). Either way the
+// least-squares solve, rank test and tail guard are ls_finalize's.
+// A Cholesky pivot must keep more than kCholKeep of its column's squared norm (each column adds
+// a direction at least 1e-3 of its length away from the previous ones), else the Givens path.
+constexpr double kCholKeep = 1e-6;
+
 template <int L>
-__global__ void __launch_bounds__(kBlock) k_ls_tsqr(int64_t n, int s, LsArgs a, Reducer red) {
+__device__ bool chol_packed(const double* G, double* R) {
+  constexpr int D = L + 1;
+  for (int j = 0; j < D; ++j) {
+    double d = G[Tri<L>::at(j, j)];
+    for (int i = 0; i < j; ++i) d = d - R[Tri<L>::at(i, j)] * R[Tri<L>::at(i, j)];
+    if (!(d > kCholKeep * G[Tri<L>::at(j, j)]) || !isfinite(d)) return false;
+    const double rjj = sqrt(d);
+    R[Tri<L>::at(j, j)] = rjj;
+    for (int m = j + 1; m < D; ++m) {
+      double t = G[Tri<L>::at(j, m)];
+      for (int i = 0; i < j; ++i) t = t - R[Tri<L>::at(i, j)] * R[Tri<L>::at(i, m)];
+      R[Tri<L>::at(j, m)] = t / rjj;
+    }
+  }
+  return true;
+}
+
+template <int L>
+__device__ void tri_inverse(const double* R, double* Ri) {
+  constexpr int D = L + 1;
+  for (int j = D - 1; j >= 0; --j) {
+    Ri[Tri<L>::at(j, j)] = 1.0 / R[Tri<L>::at(j, j)];
+    for (int m = j + 1; m < D; ++m) {
+      double t = 0.0;
+      for (int k = j + 1; k <= m; ++k) t = t + R[Tri<L>::at(j, k)] * Ri[Tri<L>::at(k, m)];
+      Ri[Tri<L>::at(j, m)] = -t / R[Tri<L>::at(j, j)];
+    }
+  }
+}
+
+// Dense tail of pass 1 (thread 0): R1, R1^-1, column norms, path choice.
+template <int L>
+__device__ void ls_pass1_tail(const double* G, DevState* ds) {
+  for (int j = 0; j < L; ++j) ds->ls_cn[j] = G[Tri<L>::at(j, j)];
+  double R[Tri<L>::NR];
+  if (chol_packed<L>(G, R)) {
+    for (int i = 0; i < Tri<L>::NR; ++i) ds->ls_r1[i] = R[i];
+    tri_inverse<L>(R, ds->ls_r1inv);
+    ds->ls_mode = 1;
+  } else {
+    ds->ls_mode = 0;
+  }
+}
+
+// Dense tail of the CholeskyQR2 pass 2 (thread 0): R = chol(G2) R1, then the reference's solve.
+template <int L>
+__device__ void ls_finalize(const double* Rf, const double* cn, int s, DevState* ds);
+template <int L>
+__device__ void ls_pass2_tail(const double* G2, int s, DevState* ds) {
+  constexpr int D = L + 1, NR = Tri<L>::NR;
+  double R2[NR], R[NR];
+  if (chol_packed<L>(G2, R2)) {
+    for (int j = 0; j < D; ++j)
+      for (int m = j; m < D; ++m) {
+        double t = 0.0;
+        for (int k = j; k <= m; ++k) t = t + R2[Tri<L>::at(j, k)] * ds->ls_r1[Tri<L>::at(k, m)];
+        R[Tri<L>::at(j, m)] = t;
+      }
+  } else {  // cannot happen for a well-conditioned Q; keep the first factor
+    for (int i = 0; i < NR; ++i) R[i] = ds->ls_r1[i];
+  }
+  double cn[L];
+  for (int j = 0; j < L; ++j) cn[j] = ds->ls_cn[j];
+  ls_finalize<L>(R, cn, s, ds);
+}
+
+template <int L>
+__global__ void __launch_bounds__(kBlock) k_ls_gram1(int64_t n, LsArgs a, Reducer red) {
+  DevState* ds = red.ds;
+  pdl_wait();
+  constexpr int D = L + 1, NR = Tri<L>::NR;
+  double g[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) g[i] = 0.0;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    double z[D];
+#pragma unroll
+    for (int j = 0; j < L; ++j) z[j] = a.r[j + 1][row];
+    z[L] = a.r[0][row];
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+#pragma unroll
+      for (int m = j; m < D; ++m) g[Tri<L>::at(j, m)] = g[Tri<L>::at(j, m)] + z[j] * z[m];
+  }
+  pdl_trigger();
+  __shared__ double scratch[NR * 32];
+  __shared__ double blk[NR];
+  __shared__ double redv[NR];
+  block_totals<NR>(g, blk, scratch);
+  if (!cta_commit(blk, NR, red.partials, &ds->ticket, redv, red.xred)) return;
+  if (threadIdx.x == 0) ls_pass1_tail<L>(redv, ds);
+}
+
+template <int L>
+__global__ void k_fin_ls1(DevState* ds) {
+  if (threadIdx.x == 0) ls_pass1_tail<L>(ds->xred, ds);
+}
+
+template <int L>
+__global__ void __launch_bounds__(kBlock) k_ls_tsqr(int64_t n, int s, int chol, LsArgs a, Reducer red) {
   DevState* ds = red.ds;
   pdl_wait();
   constexpr int NR = Tri<L>::NR;
+  if (chol && ds->ls_mode == 1) {  // CholeskyQR2 pass 2: Gram of Q = Z R1^-1, row by row
+    constexpr int D = L + 1;
+    __shared__ double ri[NR];
+    for (int i = threadIdx.x; i < NR; i += blockDim.x) ri[i] = ds->ls_r1inv[i];
+    __syncthreads();
+    double g[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) g[i] = 0.0;
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
+         row += (int64_t)gridDim.x * blockDim.x) {
+      double z[D], q[D];
+#pragma unroll
+      for (int j = 0; j < L; ++j) z[j] = a.r[j + 1][row];
+      z[L] = a.r[0][row];
+#pragma unroll
+      for (int m = 0; m < D; ++m) {
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j <= m; ++j) t = t + z[j] * ri[Tri<L>::at(j, m)];
+        q[m] = t;
+      }
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+#pragma unroll
+        for (int m = j; m < D; ++m) g[Tri<L>::at(j, m)] = g[Tri<L>::at(j, m)] + q[j] * q[m];
+    }
+    pdl_trigger();
+    __shared__ double scratch2[NR * 32];
+    __shared__ double blk2[NR];
+    __shared__ double redv2[NR];
+    block_totals<NR>(g, blk2, scratch2);
+    if (!cta_commit(blk2, NR, red.partials, &ds->ticket, redv2, red.xred)) return;
+    if (threadIdx.x == 0) ls_pass2_tail<L>(redv2, s, ds);
+    return;
+  }
   double R[NR];
   double cn[L];
 #pragma unroll
@@ -226,9 +373,17 @@ __global__ void __launch_bounds__(kBlock) k_ls_tsqr(int64_t n, int s, LsArgs a, 
 // The factors are merged in rank order by the same Givens absorption as the in-kernel tree and
 // the column sums added in rank order, so every rank solves the identical least-squares system.
 template <int L>
-__global__ void k_fin_ls(int s, int world, const double* __restrict__ gath, DevState* ds) {
+__global__ void k_fin_ls(int s, int world, int chol, const double* __restrict__ gath, DevState* ds) {
   constexpr int NR = Tri<L>::NR;
   if (threadIdx.x != 0) return;
+  if (chol && ds->ls_mode == 1) {  // CholeskyQR2: the gathered rank-local Grams summed in rank order
+    double G2[NR];
+    for (int i = 0; i < NR; ++i) G2[i] = gath[i];
+    for (int w = 1; w < world; ++w)
+      for (int i = 0; i < NR; ++i) G2[i] = G2[i] + gath[(size_t)w * (NR + L) + i];
+    ls_pass2_tail<L>(G2, s, ds);
+    return;
+  }
   double Rc[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) Rc[i] = gath[i];
@@ -247,22 +402,42 @@ __global__ void k_fin_ls(int s, int world, const double* __restrict__ gath, DevS
 
 }  // namespace
 
-void launch_fin_ls(cudaStream_t st, int ell, int s, int world, const double* gath, DevState* ds) {
-  static_assert(ls_split_count(8) <= kMaxXred, "LS split payload exceeds xred");
-  MSTAB_DISPATCH_L(ell, { k_fin_ls<L><<<1, 32, 0, st>>>(s, world, gath, ds); });
+void launch_fin_ls1(cudaStream_t st, int ell, DevState* ds) {
+  MSTAB_DISPATCH_L(ell, { k_fin_ls1<L><<<1, 32, 0, st>>>(ds); });
 }
 
-void launch_ls(cudaStream_t st, int64_t n, int64_t ld, int ell, int s, const double* const* r,
-               const Reducer& red) {
-  (void)ld;
+void launch_fin_ls(cudaStream_t st, int ell, int s, int world, bool chol, const double* gath, DevState* ds) {
+  static_assert(ls_split_count(8) <= kMaxXred, "LS split payload exceeds xred");
+  MSTAB_DISPATCH_L(ell, { k_fin_ls<L><<<1, 32, 0, st>>>(s, world, chol ? 1 : 0, gath, ds); });
+}
+
+void launch_ls_pass1(cudaStream_t st, int64_t n, int ell, const double* const* r, const Reducer& red) {
+  LaunchScope ls(st, kKLs, vbytes(n, ell + 1.0));
+  LsArgs a{};
+  for (int i = 0; i <= ell; ++i) a.r[i] = r[i];
+  MSTAB_DISPATCH_L(ell, {
+    auto kfn = k_ls_gram1<L>;
+    launch_pdl(kfn, occupancy_grid(kfn, n, 0), kBlock, 0, st, n, a, red);
+  });
+}
+
+void launch_ls_pass2(cudaStream_t st, int64_t n, int ell, int s, bool chol, const double* const* r,
+                     const Reducer& red) {
   LaunchScope ls(st, kKLs, vbytes(n, ell + 1.0));
   LsArgs a{};
   for (int i = 0; i <= ell; ++i) a.r[i] = r[i];
   MSTAB_DISPATCH_L(ell, {
     auto kfn = k_ls_tsqr<L>;
-    const int grid = occupancy_grid(kfn, n, 0);
-    launch_pdl(kfn, grid, kBlock, 0, st, n, s, a, red);
+    launch_pdl(kfn, occupancy_grid(kfn, n, 0), kBlock, 0, st, n, s, chol ? 1 : 0, a, red);
   });
+}
+
+void launch_ls(cudaStream_t st, int64_t n, int64_t ld, int ell, int s, const double* const* r,
+               const Reducer& red) {
+  (void)ld;
+  const bool chol = ls_use_cholqr(n);
+  if (chol) launch_ls_pass1(st, n, ell, r, red);
+  launch_ls_pass2(st, n, ell, s, chol, r, red);
 }
 
 }  // namespace mstab_b200

@@ -152,11 +152,11 @@ void after_poly(Context& ctx, int s) {
   launch_fin_poly(ctx.stream(), s, ctx.ds());
   check_launch();
 }
-void after_ls(Context& ctx, int ell, int s) {
+void after_ls(Context& ctx, int ell, int s, bool chol) {
   if (!ctx.sharded()) return;
   const int cnt = ls_split_count(ell);
   ctx.comm->allgather(xred(ctx), ctx.xgath->d(), cnt, ctx.stream());
-  launch_fin_ls(ctx.stream(), ell, s, ctx.comm->world(), ctx.xgath->d(), ctx.ds());
+  launch_fin_ls(ctx.stream(), ell, s, ctx.comm->world(), chol, ctx.xgath->d(), ctx.ds());
   check_launch();
 }
 // dots (launch_dots layout: slots 0..na-1, the norm in slot kMaxS) -> dst[0..na(+1))
@@ -362,8 +362,17 @@ void enqueue_cycle(Context& ctx, const Operator& op, const double* P, int s, int
   const double* rr[kMaxEll + 1];
   rr[0] = D.r->d();
   for (int i = 1; i <= ell; ++i) rr[i] = R[i]->d();
-  launch_ls(st, n, ld, ell, s, rr, red);
-  if (shard) after_ls(ctx, ell, s);
+  const bool chol = ls_use_cholqr(op.n_global);  // same choice on every rank
+  if (chol) {
+    launch_ls_pass1(st, n, ell, rr, red);
+    if (shard) {  // pass-1 Gram summed over the ranks before the replicated Cholesky
+      ctx.comm->allreduce_sum(xred(ctx), (ell + 1) * (ell + 2) / 2, st);
+      launch_fin_ls1(st, ell, ctx.ds());
+      check_launch();
+    }
+  }
+  launch_ls_pass2(st, n, ell, s, chol, rr, red);
+  if (shard) after_ls(ctx, ell, s, chol);
   const double* lv[kMaxEll + 2];
   lv[0] = D.U->d();
   lv[1] = D.V->d();

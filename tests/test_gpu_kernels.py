@@ -103,3 +103,37 @@ def test_cut_space_and_arnoldi(gpu_ctx, golden_kernels):
     u, v, _ = m.arnoldi_init(ope, np.eye(6)[0], 3, 4)
     assert np.max(np.abs(u - g["arn_eye_u"])) <= 1e-13
     assert np.max(np.abs(u.T @ u - np.eye(3))) <= 1e-12
+
+
+@pytest.mark.parametrize("ell", [1, 2, 4, 8])
+def test_least_squares_cholqr2_tall(gpu_ctx, ell):
+    """Tall systems (n >= 2^17) take the CholeskyQR2 path; checked against LAPACK's QR
+    least-squares solution (numpy.linalg.lstsq) at the conditioning bound of the method."""
+    rng = np.random.default_rng(100 + ell)
+    n = 1 << 18
+    z = rng.standard_normal((n, ell)) * np.logspace(0, -2, ell)
+    r = z @ rng.standard_normal(ell) + 0.3 * rng.standard_normal(n)
+    t = m.least_squares_tall(z, r, gpu_ctx)
+    ref = np.linalg.lstsq(z, r, rcond=None)[0]
+    cond = np.linalg.cond(z)
+    assert np.linalg.norm(t - ref) <= 1e-14 * cond * np.linalg.norm(ref) * 10
+
+
+def test_least_squares_tall_fallback_ill_conditioned(gpu_ctx):
+    """A tall power basis too ill-conditioned for CholeskyQR2 falls back to the Givens TSQR in the
+    same launch and still matches LAPACK to cond * eps."""
+    from paper_1604_06043_b200 import problems as pb
+    A = pb.config("c1", grid=512).matrix()   # N = 262144
+    op = m.CsrOperator(A, gpu_ctx)
+    rng = np.random.default_rng(5)
+    v = rng.standard_normal(A.n_rows)
+    cols = [v]
+    for _ in range(6):
+        cols.append(op.apply(cols[-1]))
+    z = np.stack(cols[1:], axis=1)
+    r = cols[0]
+    cond = np.linalg.cond(z)
+    assert cond > 1e4  # beyond the CholeskyQR2 acceptance bound
+    t = m.least_squares_tall(z, r, gpu_ctx)
+    ref = np.linalg.lstsq(z, r, rcond=None)[0]
+    assert np.linalg.norm(t - ref) <= 1e-15 * cond * np.linalg.norm(ref) * 10
