@@ -6,6 +6,8 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "solver.h"
 
@@ -443,6 +445,36 @@ int mstab_kernel_arnoldi(mstab_context* ctx, const mstab_operator* op, const dou
 // ---- sequence-driver helpers ------------------------------------------------------------------
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+// Element-wise host loops of the sequence driver, split over host threads (each element is
+// computed by exactly one thread with the same operations, so the result does not depend on the
+// split). The .cpp is compiled with -ffp-contract=off: x/dt, +f, *h2 round separately.
+template <typename F>
+void host_parallel(int64_t n, F&& body) {
+  const int64_t grain = 1 << 16;
+  unsigned hw = std::thread::hardware_concurrency();
+  int nt = (int)std::min<int64_t>(hw ? hw : 1, std::max<int64_t>(1, n / grain));
+  nt = std::min(nt, 16);
+  if (nt <= 1) {
+    body(0, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  pool.reserve(nt - 1);
+  const int64_t chunk = (n + nt - 1) / nt;
+  for (int t = 1; t < nt; ++t) {
+    const int64_t a = std::min<int64_t>(n, t * chunk), b = std::min<int64_t>(n, a + chunk);
+    pool.emplace_back([&body, a, b] { body(a, b); });
+  }
+  body(0, std::min<int64_t>(n, chunk));
+  for (auto& th : pool) th.join();
+}
+}  // namespace
+
+extern "C" {
+
 int mstab_harness_euler_rhs(mstab_context* ctx, int64_t n, const double* x, const double* f,
                             double dt, double h2, double* b, int32_t mem) {
   return guarded([&] {
@@ -451,11 +483,9 @@ int mstab_harness_euler_rhs(mstab_context* ctx, int64_t n, const double* x, cons
       launch_euler_rhs(ctx->impl->stream(), n, x, f, dt, h2, b);
       ctx->impl->sync();
     } else {
-      for (int64_t i = 0; i < n; ++i) {
-        const volatile double q = x[i] / dt;
-        const volatile double t = q + f[i];
-        b[i] = h2 * t;
-      }
+      host_parallel(n, [=](int64_t a, int64_t e) {
+        for (int64_t i = a; i < e; ++i) b[i] = h2 * (x[i] / dt + f[i]);
+      });
     }
   });
 }
@@ -468,10 +498,9 @@ int mstab_harness_axpby(mstab_context* ctx, int64_t n, const double* x, const do
       launch_axpby_chain(ctx->impl->stream(), n, x, g, alpha, b);
       ctx->impl->sync();
     } else {
-      for (int64_t i = 0; i < n; ++i) {
-        const volatile double t = alpha * g[i];
-        b[i] = x[i] + t;
-      }
+      host_parallel(n, [=](int64_t a, int64_t e) {
+        for (int64_t i = a; i < e; ++i) b[i] = x[i] + alpha * g[i];
+      });
     }
   });
 }

@@ -116,19 +116,19 @@ __device__ bool cta_commit(const double* blk, int nslots, double* partials, uint
   if (!s_last) return false;
   __threadfence();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // This reduction is on the critical path of every fused dense step (the whole grid waits for
+  // it): each lane issues all of its partial loads (up to 16 per batch, independent) before
+  // summing them in index order, so a slot costs ~one L2 round trip instead of G/128.
   for (int i = w; i < nslots; i += nw) {
     const double* p = partials + (size_t)i * G;
     double acc = 0.0;
-    int c = lane;
-    for (; c + 96 < G; c += 128) {
-      const double a0 = __ldcg(p + c), a1 = __ldcg(p + c + 32), a2 = __ldcg(p + c + 64),
-                   a3 = __ldcg(p + c + 96);
-      acc += a0;
-      acc += a1;
-      acc += a2;
-      acc += a3;
+    for (int c0 = lane; c0 < G; c0 += 32 * 16) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = (c0 + 32 * u < G) ? __ldcg(p + c0 + 32 * u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc += v[u];
     }
-    for (; c < G; c += 32) acc += __ldcg(p + c);
     acc = warp_sum(acc);
     if (lane == 0) red[i] = acc;
   }
