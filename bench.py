@@ -52,11 +52,18 @@ def dist_env():
 
 
 def workload_desc(cfg, A):
+    ws_gb = (2 * (2 + 2 * cfg.s) + cfg.ell * (cfg.s + 1) + 1 + cfg.s) * cfg.N * 8 / 1e9
+    if cfg.kind == "convdiff":
+        what = (f"{cfg.dim}-D conv-diff {cfg.grid}^{cfg.dim} {cfg.stencil}-pt upwind, beta={tuple(cfg.beta)}, "
+                f"implicit-Euler RHS sequence b_(i+1) = h^2(x_i/dt + f)")
+    else:
+        what = (f"random banded N={cfg.N}, 27 nnz/row, half-width {cfg.half_width}, diagonally dominant, "
+                f"RHS sequence b_(i+1) = x_i + 0.1 g_i")
     return {
-        "workload": f"{cfg.name}: 3-D conv-diff {cfg.grid}^3 7-pt upwind Pe=200, implicit-Euler RHS sequence, "
-                    f"M({cfg.s},{cfg.ell})stab tol 1e-8 (true residual), fetch at half tolerance",
+        "workload": f"{cfg.name}: {what}, M({cfg.s},{cfg.ell})stab tol 1e-8 (true residual), fetch at half tolerance",
         "N": int(A.n_rows), "nnz": int(A.nnz()), "s": cfg.s, "ell": cfg.ell, "sequence_len": cfg.n_rhs,
-        "l2": "working set ~80 N-vectors = 1.34 GB >> 126 MB L2 (no flush needed)",
+        "l2": f"working set ~{ws_gb:.2f} GB of N-vectors vs 126 MB L2"
+              + (" (no flush needed)" if ws_gb > 1.0 else " (L2-resident: latency-bound config)"),
     }
 
 
@@ -107,32 +114,45 @@ class Sequence:
     """One chained sequence. With a row-slab operator (N > 1 GPUs) every vector here is the
     rank's own rows [lo, hi) and the solve calls are collective."""
 
-    def __init__(self, m, cfg, op, ctx, seed, device_mode, torch=None, rows=None):
+    def __init__(self, m, cfg, op, ctx, seed, device_mode, torch=None, rows=None, n_steps=64):
         self.m, self.cfg, self.op, self.ctx, self.torch = m, cfg, op, ctx, torch
         cfg.seed = seed
-        x0, f = cfg.sources()
         lo, hi = rows if rows is not None else (0, cfg.N)
-        self.f = np.ascontiguousarray(f[lo:hi])
+        self.lo, self.hi = lo, hi
         self.sc = m.SolverConfig(cfg.s, cfg.ell, cfg.tol, 100000, True, 0)
         self.fp = m.FetchPolicy.at_half_tolerance()
         self.device_mode = device_mode
         self.rec = None
         self.restarts = 0
         self.log = []
+        self.i = 1  # 1-based index of the next solve in the sequence
         N = hi - lo
-        b0 = np.ascontiguousarray(cfg.first_rhs(x0, f)[lo:hi])
+        if cfg.kind == "convdiff":
+            x0, f = cfg.sources()
+            self.f = np.ascontiguousarray(f[lo:hi])
+            b0 = np.ascontiguousarray(cfg.first_rhs(x0, f)[lo:hi])
+        else:  # banded: g_i drawn up front (host RNG outside the timed region)
+            from paper_1604_06043_b200 import problems as pb
+            b0 = np.ascontiguousarray(cfg.first_rhs()[lo:hi])
+            self.g = [np.ascontiguousarray(pb.normal(1000 + cfg.seed + i, cfg.N)[lo:hi])
+                      for i in range(1, n_steps + 1)]
         if device_mode:
             dev = torch.device("cuda", torch.cuda.current_device())
-            self.f_d = torch.from_numpy(self.f).to(dev)
+            if cfg.kind == "convdiff":
+                self.f_d = torch.from_numpy(self.f).to(dev)
+            else:
+                self.g_d = [torch.from_numpy(g).to(dev) for g in self.g]
             self.x_d = torch.empty(N, dtype=torch.float64, device=dev)
             self.b_d = torch.from_numpy(b0).to(dev)
             torch.cuda.synchronize()
         else:
+            if cfg.kind != "convdiff":
+                self.g = [torch.from_numpy(g).pin_memory().numpy() for g in self.g]
             self.b_h = torch.from_numpy(b0).pin_memory().numpy()
             self.x_h = torch.empty(N, dtype=torch.float64).pin_memory().numpy()
 
     def step(self):
-        m, t = self.m, self.torch
+        m = self.m
         b = self.b_d if self.device_mode else self.b_h
         restarted = False
         t0 = time.perf_counter()
@@ -149,16 +169,26 @@ class Sequence:
         self.rec = r.handoff()
         c = self.cfg
         dll, h = self.ctx.lib.dll, self.ctx.h
-        # b_{i+1} = h^2 (x_i/dt + f) through the C-ABI harness helper (same rounding on both paths)
-        nloc = self.f.size
+        nloc = self.hi - self.lo
+        # next right-hand side through the C-ABI harness helpers (same rounding on both paths):
+        # conv-diff b_{i+1} = h^2 (x_i/dt + f); banded b_{i+1} = x_i + 0.1 g_i
         if self.device_mode:
             r.x_into(self.x_d)  # D2D on the solver stream (synchronised)
-            dll.mstab_harness_euler_rhs(h, nloc, self.x_d.data_ptr(), self.f_d.data_ptr(), c.dt, c.h2,
+            if c.kind == "convdiff":
+                dll.mstab_harness_euler_rhs(h, nloc, self.x_d.data_ptr(), self.f_d.data_ptr(), c.dt, c.h2,
+                                            self.b_d.data_ptr(), 1)
+            else:
+                dll.mstab_harness_axpby(h, nloc, self.x_d.data_ptr(), self.g_d[self.i - 1].data_ptr(), 0.1,
                                         self.b_d.data_ptr(), 1)
         else:
             r.x_into(self.x_h)  # D2H into pinned host memory
-            dll.mstab_harness_euler_rhs(h, nloc, self.x_h.ctypes.data, self.f.ctypes.data, c.dt, c.h2,
+            if c.kind == "convdiff":
+                dll.mstab_harness_euler_rhs(h, nloc, self.x_h.ctypes.data, self.f.ctypes.data, c.dt, c.h2,
+                                            self.b_h.ctypes.data, 0)
+            else:
+                dll.mstab_harness_axpby(h, nloc, self.x_h.ctypes.data, self.g[self.i - 1].ctypes.data, 0.1,
                                         self.b_h.ctypes.data, 0)
+        self.i += 1
         return r
 
 
@@ -208,7 +238,8 @@ def run_b200(args):
         return float(t.item())
 
     # ---- value: device-resident inputs -------------------------------------------------------
-    seq = Sequence(m, cfg, op, ctx, seed=0, device_mode=True, torch=torch, rows=rows)
+    seq = Sequence(m, cfg, op, ctx, seed=0, device_mode=True, torch=torch, rows=rows,
+                   n_steps=args.warmup + 2 * args.steps + 1)
     for _ in range(args.warmup):
         seq.step()
     barrier()
@@ -240,7 +271,8 @@ def run_b200(args):
     value = args.steps / (ms_max / 1e3)  # one sequence over all ranks: whole-job RHS/s
 
     # ---- e2e: host buffers through the C-ABI --------------------------------------------------
-    seq_h = Sequence(m, cfg, op, ctx, seed=0, device_mode=False, torch=torch, rows=rows)
+    seq_h = Sequence(m, cfg, op, ctx, seed=0, device_mode=False, torch=torch, rows=rows,
+                     n_steps=args.warmup + args.steps + 1)
     for _ in range(args.warmup):
         seq_h.step()
     barrier()
