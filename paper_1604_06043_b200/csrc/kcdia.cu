@@ -38,7 +38,6 @@ __global__ void __launch_bounds__(kBlock, S <= 8 ? 4 : 2)
   const int64_t n = a.n;
   const int nd = ND > 0 ? ND : a.ndiag;
   const int mb = a.mask_bytes;
-  pdl_wait();
   double part[NS];
 #pragma unroll
   for (int i = 0; i < NS; ++i) part[i] = 0.0;
@@ -52,6 +51,7 @@ __global__ void __launch_bounds__(kBlock, S <= 8 ? 4 : 2)
                               : __ldg(static_cast<const uint32_t*>(a.dia_mask) + r));
   };
   const int32_t rstride = gridDim.x * blockDim.x;
+  pdl_wait();
   uint32_t mnext = load_mask(blockIdx.x * blockDim.x + threadIdx.x);
   for (int32_t row = blockIdx.x * blockDim.x + threadIdx.x; row < (int32_t)n; row += rstride) {
     const uint32_t m = mnext;
@@ -90,9 +90,11 @@ __global__ void __launch_bounds__(kBlock, S <= 8 ? 4 : 2)
   __shared__ double scratch[NS * 32];
   __shared__ double blk[NS];
   __shared__ double redv[NS];
+  __shared__ FinStage fs;
+  if (!red.xred) fin_prestage(fin, ds, fs);
   block_totals<NS>(part, blk, scratch);
   if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv, red.xred)) return;
-  finalize_spmv<S>(fin, redv, ds);
+  finalize_spmv<S>(fin, redv, ds, fs);
 }
 
 template <int S, bool TRUE_RES, int ND>

@@ -346,16 +346,40 @@ __device__ void set_breakdown(DevState* ds, int code, int mv) {
   ds->st.mv_at_breakdown = mv;
 }
 
-// The dense step after an SpMV reduction, run by ALL threads of the last CTA: the s x s system
-// is staged from global memory into shared memory in parallel (one element per thread; a single
-// thread walking ds->Ma would pay ~s^2 dependent L2 round trips), thread 0 factors and solves in
-// shared memory (warp 0, warp_lu_solve), and the solution is written back in parallel.
-template <int MAXS>
-__device__ void finalize_spmv(const FinParams& f, const double* red, DevState* ds) {
-  __shared__ double lu[kMaxS * kMaxS];
-  __shared__ double vin[kMaxS], vout[kMaxS];
-  __shared__ int ok;
+// The dense step after an SpMV reduction. Its inputs that do not depend on this launch's
+// reduction (the known columns of the s x s system and, for a column step, the right-hand side)
+// are staged into shared memory by EVERY CTA before its ticket (fin_prestage), so the last CTA
+// starts the factorisation as soon as the partials are summed instead of paying another L2
+// round trip; thread 0..31 (warp_lu_solve) factor and solve, and the solution is written back
+// in parallel.
+struct FinStage {
+  double lu[kMaxS * kMaxS];
+  double vin[kMaxS], vout[kMaxS];
+  int ok;
+};
+
+__device__ void fin_prestage(const FinParams& f, const DevState* ds, FinStage& fs) {
   const int s = f.s, t = threadIdx.x, nt = blockDim.x;
+  if (f.op == kFinRhsEta0 || f.op == kFinTrueRes) {
+    for (int i = t; i < s * s; i += nt) fs.lu[i] = ds->Ma[i];
+  } else if (f.op == kFinColEta) {
+    const int q = f.q;
+    // msys_{q+1} = [P^H V^(k+1)_{0..q}, P^H V^(k)_{q+1..s-1}] (idrstab.cpp:133-137); column q
+    // arrives with the reduction. After the last column the level's P^H V^(k+1) is all of Mn.
+    for (int i = t; i < s * s; i += nt) {
+      const int c = i / s;
+      if (c < q)
+        fs.lu[i] = ds->Mn[i];
+      else if (c > q)
+        fs.lu[i] = ds->Ma[i];
+    }
+    if (t < s) fs.vin[t] = ds->rhs[t];
+  }
+}
+
+template <int MAXS>
+__device__ void finalize_spmv(const FinParams& f, const double* red, DevState* ds, FinStage& fs) {
+  const int s = f.s, t = threadIdx.x;
   if (f.op == kFinStore) {
     if (t < s) f.dst[t] = red[t];
     return;
@@ -366,34 +390,24 @@ __device__ void finalize_spmv(const FinParams& f, const double* red, DevState* d
   if (f.op == kFinRhsEta0) {  // after step (b) of level k: rhs and eta_0 (msys_0 = P^H V^(k))
     if (t < s) {
       ds->rhs[t] = red[t];
-      vin[t] = red[t];
+      fs.vin[t] = red[t];
     }
-    for (int i = t; i < s * s; i += nt) lu[i] = ds->Ma[i];
     dst = ds->eta;
     mv = f.k * (s + 1) + 1;
   } else if (f.op == kFinColEta) {  // after V^(k+1)_q = A v_q^(k)
     const int q = f.q, k = f.k;
     if (t < s) {
       ds->Mn[t + q * s] = red[t];
-      vin[t] = ds->rhs[t];
+      fs.lu[t + q * s] = red[t];
     }
     if (q + 1 < s) {
-      // msys_{q+1} = [P^H V^(k+1)_{0..q}, P^H V^(k)_{q+1..s-1}]  (idrstab.cpp:133-137)
-      for (int i = t; i < s * s; i += nt) {
-        const int c = i / s;
-        lu[i] = (c < q) ? ds->Mn[i] : (c == q ? red[i - c * s] : ds->Ma[i]);
-      }
       dst = ds->eta + (q + 1) * s;
       mv = k * (s + 1) + 1 + (q + 1);
     } else {
       // level done: Ma := P^H V^(k+1), g := P^H r^(k+1); gamma of level k+1 unless it is the last
-      for (int i = t; i < s * s; i += nt) {
-        const int c = i / s;
-        const double v = (c == q) ? red[i - c * s] : ds->Mn[i];
-        lu[i] = v;
-        ds->Ma[i] = v;
-      }
-      if (t < s) ds->g[t] = ds->rhs[t];
+      __syncthreads();
+      for (int i = t; i < s * s; i += blockDim.x) ds->Ma[i] = fs.lu[i];
+      if (t < s) ds->g[t] = fs.vin[t];
       if (k + 1 < f.ell) {
         dst = ds->gamma + (k + 1) * kMaxS;
         mv = (k + 1) * (s + 1);
@@ -405,9 +419,8 @@ __device__ void finalize_spmv(const FinParams& f, const double* red, DevState* d
     if (t == 0) ds->st.resnorm = sqrt(red[s]);
     if (t < s) {
       ds->g[t] = red[t];
-      vin[t] = red[t];
+      fs.vin[t] = red[t];
     }
-    for (int i = t; i < s * s; i += nt) lu[i] = ds->Ma[i];
     dst = ds->gamma;
     pending = true;
   } else {
@@ -416,15 +429,15 @@ __device__ void finalize_spmv(const FinParams& f, const double* red, DevState* d
   __syncthreads();
   if (!solve) return;
   if (t < 32) {
-    const bool r = warp_lu_solve<MAXS>(s, lu, vin, vout);
-    if (t == 0) ok = r ? 1 : 0;
+    const bool r = warp_lu_solve<MAXS>(s, fs.lu, fs.vin, fs.vout);
+    if (t == 0) fs.ok = r ? 1 : 0;
   }
   __syncthreads();
-  if (t < s) dst[t] = vout[t];
+  if (t < s) dst[t] = fs.vout[t];
   if (t == 0) {
     if (pending)
-      ds->st.pending_singular = ok ? 0 : 1;
-    else if (!ok)
+      ds->st.pending_singular = fs.ok ? 0 : 1;
+    else if (!fs.ok)
       set_breakdown(ds, kBreakSingular, mv);
   }
 }

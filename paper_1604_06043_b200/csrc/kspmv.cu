@@ -82,9 +82,11 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ph(DevCsr a, const double* __re
   __shared__ double scratch[NS * 32];
   __shared__ double blk[NS];
   __shared__ double redv[NS];
+  __shared__ FinStage fs;
+  if (!red.xred) fin_prestage(fin, ds, fs);
   block_totals<NS>(part, blk, scratch);
   if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv, red.xred)) return;
-  finalize_spmv<S>(fin, redv, ds);
+  finalize_spmv<S>(fin, redv, ds, fs);
 }
 
 // SpMV on the DIA form (kernels.h DevCsr): two rows per thread; every load of the row pair
@@ -170,9 +172,11 @@ __global__ void __launch_bounds__(kBlock, 2) k_spmv_dia(DevCsr a, const double* 
   __shared__ double scratch[NS * 32];
   __shared__ double blk[NS];
   __shared__ double redv[NS];
+  __shared__ FinStage fs;
+  if (!red.xred) fin_prestage(fin, ds, fs);
   block_totals<NS>(part, blk, scratch);
   if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv, red.xred)) return;
-  finalize_spmv<S>(fin, redv, ds);
+  finalize_spmv<S>(fin, redv, ds, fs);
 }
 
 // ---- TMA-pipelined DIA SpMV -----------------------------------------------------------------------
@@ -295,9 +299,11 @@ __global__ void __launch_bounds__(kBlock) k_spmv_dia_tma(DevCsr a, const double*
   __shared__ double scratch[NS * 32];
   __shared__ double blk[NS];
   __shared__ double redv[NS];
+  __shared__ FinStage fs;
+  if (!red.xred) fin_prestage(fin, ds, fs);
   block_totals<NS>(part, blk, scratch);
   if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv, red.xred)) return;
-  finalize_spmv<S>(fin, redv, ds);
+  finalize_spmv<S>(fin, redv, ds, fs);
 }
 
 template <int S, bool TRUE_RES>
@@ -323,9 +329,11 @@ void launch_dia_tma(cudaStream_t st, const DevCsr& a, const double* x, double* y
 template <int S>
 __global__ void __launch_bounds__(kBlock) k_fin_spmv(FinParams fin, DevState* ds) {
   __shared__ double redv[S + 1];
+  __shared__ FinStage fs;
   if (threadIdx.x <= S) redv[threadIdx.x] = ds->xred[threadIdx.x];
+  fin_prestage(fin, ds, fs);
   __syncthreads();
-  finalize_spmv<S>(fin, redv, ds);
+  finalize_spmv<S>(fin, redv, ds, fs);
 }
 
 }  // namespace
