@@ -51,14 +51,22 @@ __global__ void __launch_bounds__(kBlock, S <= 8 ? 4 : 2)
                               : __ldg(static_cast<const uint32_t*>(a.dia_mask) + r));
   };
   const int32_t rstride = gridDim.x * blockDim.x;
+  // The first row's mask and P values are loaded BEFORE pdl_wait: both are fixed for the whole
+  // sequence (nothing in the cycle writes them), so they overlap the predecessor's drain; x,
+  // which the predecessor writes, is read only after the wait.
+  const int32_t row0 = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t mnext = load_mask(row0);
+  double pv[S];
+#pragma unroll
+  for (int c = 0; c < S; ++c) pv[c] = row0 < (int32_t)n ? __ldg(p + c * ld + row0) : 0.0;
   pdl_wait();
-  uint32_t mnext = load_mask(blockIdx.x * blockDim.x + threadIdx.x);
-  for (int32_t row = blockIdx.x * blockDim.x + threadIdx.x; row < (int32_t)n; row += rstride) {
+  for (int32_t row = row0; row < (int32_t)n; row += rstride) {
     const uint32_t m = mnext;
     mnext = load_mask(row + rstride);
-    double pv[S];
+    if (row != row0) {
 #pragma unroll
-    for (int c = 0; c < S; ++c) pv[c] = __ldg(p + c * ld + row);
+      for (int c = 0; c < S; ++c) pv[c] = __ldg(p + c * ld + row);
+    }
     const double bv = TRUE_RES ? __ldg(b + row) : 0.0;
     double acc = 0.0;
     if (ND > 0) {

@@ -42,6 +42,9 @@ struct DevCsr {
   // Valid index range [xlo, xhi) of the x vector the SpMV reads: [0, n) on one GPU; in a
   // row-sharded solve the owned rows plus the halo on either side (negative xlo).
   int64_t xlo = 0, xhi = 0;
+  // Column band of the stored entries: blo <= col - row <= bhi for every entry (0, 0 when empty).
+  // A narrow band lets the CSR SpMV keep a sliding x window in shared memory (kspmv.cu k_spmv_ring).
+  int64_t blo = 0, bhi = 0;
 };
 constexpr int kMaxDiag = 64;
 constexpr int kMaxConstDiag = 32;

@@ -324,6 +324,147 @@ void launch_dia_tma(cudaStream_t st, const DevCsr& a, const double* x, double* y
   kfn<<<grid, kBlock, smem, st>>>(a, x, y, p, ld, b, T, fin, red);
 }
 
+// ---- banded CSR: sliding x window in shared memory ---------------------------------------------
+// On a banded irregular matrix (c3: 27 random columns per row within +-4096) the gathers of
+// k_spmv_ph are L1-wavefront bound (ncu, c3: L1/TEX 90% busy at 15% hit rate, DRAM 39%): every
+// gather instruction touches 32 unrelated lines. Here one 1024-thread CTA per SM walks ONE
+// contiguous row range in tiles of 1024 rows and keeps x[t0 + blo, t0 + 1024 + bhi) in a
+// shared-memory ring of kRing doubles (slot = col mod kRing), so every gather is a shared-memory
+// load. Advancing a tile needs only its 1024 new x values, which each thread prefetches into a
+// register at the start of the previous tile and stores after it (the slots they overwrite belong
+// to columns below t0 + blo: no tile reads them again), so the only per-tile synchronisation is
+// one barrier.
+// A warp streams the CSR slice of its 32 rows in coalesced chunks of kRingStage entries: every
+// lane loads kRingStage/32 (value, column) pairs, forms their products value * x[column] from the
+// ring (all lanes busy, independent loads) and parks them in shared memory; then each lane adds
+// its own row's products in CSR order. The product and the sum are the reference's two roundings
+// (csr.cpp:107-110: acc = acc + v * x), so the result is bit-identical.
+constexpr int kRing = 16384;          // doubles (128 KB)
+constexpr int kRingBlock = 1024;      // threads = rows per tile
+constexpr int kRingStage = 256;       // CSR entries per warp chunk (8 per lane)
+constexpr size_t kRingSmem = (size_t)kRing * 8 + (size_t)(kRingBlock / 32) * kRingStage * 8;
+
+template <int S, bool TRUE_RES>
+__global__ void __launch_bounds__(kRingBlock, 1) k_spmv_ring(DevCsr a, const double* __restrict__ x,
+                                                             double* __restrict__ y,
+                                                             const double* __restrict__ p, int64_t ld,
+                                                             const double* __restrict__ b,
+                                                             int64_t rows_per_cta, FinParams fin,
+                                                             Reducer red) {
+  extern __shared__ __align__(16) double ring_smem[];
+  double* ring = ring_smem;
+  DevState* ds = red.ds;
+  constexpr int NS = S + (TRUE_RES ? 1 : 0);
+  constexpr int PER = kRingStage / 32;
+  double part[NS];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) part[i] = 0.0;
+  const int64_t n = a.n;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* sp = ring_smem + kRing + wid * kRingStage;  // this warp's products
+  const int32_t* __restrict__ rp = a.row_ptr;
+  const int32_t* __restrict__ ci = a.col_idx;
+  const double* __restrict__ va = a.values;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(n, r0 + rows_per_cta);
+  pdl_wait();
+  // window of the first tile
+  if (r0 < r1) {
+    const int64_t w0 = max(a.xlo, r0 + a.blo), w1 = min(a.xhi, min(r1, r0 + kRingBlock) + a.bhi);
+    for (int64_t c = w0 + threadIdx.x; c < w1; c += kRingBlock) ring[c & (kRing - 1)] = __ldg(x + c);
+  }
+  __syncthreads();
+  for (int64_t t0 = r0; t0 < r1; t0 += kRingBlock) {
+    const int64_t t1 = min(r1, t0 + kRingBlock);
+    // this thread's x value of the NEXT tile's window extension [t1 + bhi, t2 + bhi)
+    const int64_t t2 = min(r1, t1 + kRingBlock);
+    const int64_t nc = t1 + a.bhi + threadIdx.x;
+    const bool has_next = t1 < r1 && nc < min(a.xhi, t2 + a.bhi) && nc >= a.xlo;
+    const double xnext = has_next ? __ldg(x + nc) : 0.0;
+    const int64_t base = t0 + wid * 32;
+    if (base < t1) {
+      const int64_t row = base + lane;
+      const bool valid = row < t1;
+      const int64_t last = (base + 32 < t1) ? base + 32 : t1;
+      const int beg = valid ? __ldg(rp + row) : 0;
+      const int end = valid ? __ldg(rp + row + 1) : 0;
+      const int wbeg = __shfl_sync(0xffffffffu, beg, 0);
+      const int wend = __ldg(rp + last);
+      double pv[S];
+#pragma unroll
+      for (int c = 0; c < S; ++c) pv[c] = valid ? __ldg(p + c * ld + row) : 0.0;
+      const double bv = (TRUE_RES && valid) ? b[row] : 0.0;
+      double acc = 0.0;
+      // chunk loads are issued one chunk ahead: the next chunk's (value, column) pairs are in
+      // flight while the lanes add up the current chunk's products
+      double v[PER];
+      int32_t cc[PER];
+      auto load_chunk = [&](int chunk) {
+        const int cnt = min(kRingStage, wend - chunk);
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int i = lane + 32 * u;
+          v[u] = i < cnt ? __ldg(va + chunk + i) : 0.0;
+          cc[u] = i < cnt ? __ldg(ci + chunk + i) : 0;
+        }
+      };
+      if (wbeg < wend) load_chunk(wbeg);
+      for (int chunk = wbeg; chunk < wend; chunk += kRingStage) {
+        const int cnt = min(kRingStage, wend - chunk);
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int i = lane + 32 * u;
+          if (i < cnt) sp[i] = v[u] * ring[cc[u] & (kRing - 1)];
+        }
+        __syncwarp();
+        if (chunk + kRingStage < wend) load_chunk(chunk + kRingStage);
+        const int lo = max(beg, chunk) - chunk, hi = min(end, chunk + cnt) - chunk;
+        for (int k = lo; k < hi; ++k) acc = acc + sp[k];
+        __syncwarp();
+      }
+      if (valid) {
+        if (TRUE_RES) acc = bv - acc;
+        y[row] = acc;
+#pragma unroll
+        for (int c = 0; c < S; ++c) part[c] = part[c] + pv[c] * acc;
+        if (TRUE_RES) part[S] = part[S] + acc * acc;
+      }
+    }
+    if (has_next) ring[nc & (kRing - 1)] = xnext;
+    __syncthreads();
+  }
+  pdl_trigger();
+  __shared__ double scratch[NS * 32];
+  __shared__ double blk[NS];
+  __shared__ double redv[NS];
+  __shared__ FinStage fs;
+  if (!red.xred) fin_prestage(fin, ds, fs);
+  block_totals<NS>(part, blk, scratch);
+  if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv, red.xred)) return;
+  finalize_spmv<S>(fin, redv, ds, fs);
+}
+
+// The ring holds two tiles plus the band (the next tile's values land while this one is read);
+// wider bands use k_spmv_ph.
+inline bool ring_fits(const DevCsr& a) { return a.bhi - a.blo + 2 * kRingBlock <= kRing; }
+
+template <int S, bool TRUE_RES>
+void launch_ring(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p, int64_t ld,
+                 const double* b, const FinParams& fin, const Reducer& red) {
+  auto kfn = k_spmv_ring<S, TRUE_RES>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingSmem);
+    configured = true;
+  }
+  const int64_t ntiles = (a.n + kRingBlock - 1) / kRingBlock;
+  int64_t grid = std::min<int64_t>(g_num_sms, std::max<int64_t>(1, ntiles));
+  const int64_t tiles_per_cta = (ntiles + grid - 1) / grid;
+  grid = std::max<int64_t>(1, (ntiles + tiles_per_cta - 1) / tiles_per_cta);
+  launch_pdl(kfn, (int)grid, kRingBlock, kRingSmem, st, a, x, y, p, ld, b, tiles_per_cta * kRingBlock, fin,
+             red);
+}
+
 // Row-sharded finaliser of an SpMV reduction: the allreduced totals (ds->xred) run through the
 // same finalize_spmv tail the fused kernels run in their last CTA.
 template <int S>
@@ -371,6 +512,16 @@ void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y
         const int grid = occupancy_grid(kfn, (a.n + 1) / 2, 0);
         launch_pdl(kfn, grid, kBlock, 0, st, a, x, y, p, ld, b, fin, red);
       }
+    });
+    return;
+  }
+  static const bool no_ring = std::getenv("MSTAB_NO_RING") != nullptr;
+  if (!no_ring && ring_fits(a)) {
+    MSTAB_DISPATCH_S(s, {
+      if (b)
+        launch_ring<S, true>(st, a, x, y, p, ld, b, fin, red);
+      else
+        launch_ring<S, false>(st, a, x, y, p, ld, b, fin, red);
     });
     return;
   }

@@ -410,6 +410,14 @@ void upload_rows(Context& ctx, Operator* op, int64_t n, const int64_t* row_ptr, 
   if (nnz >= (int64_t(1) << 31)) throw Error(MSTAB_E_CONFIG, "b200: nnz >= 2^31 not supported (int32 indices)");
   op->n = n;
   op->nnz = nnz;
+  int64_t blo = 0, bhi = 0;
+  for (int64_t i = 0; i < n; ++i)
+    if (row_ptr[i + 1] > row_ptr[i]) {
+      blo = std::min(blo, col_idx[row_ptr[i]] - i);  // columns ascend within a row
+      bhi = std::max(bhi, col_idx[row_ptr[i + 1] - 1] - i);
+    }
+  op->blo = blo;
+  op->bhi = bhi;
   std::vector<int32_t> rp32(n + 1), ci32(nnz + 32, 0);
   for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)row_ptr[i];
   for (int64_t k = 0; k < nnz; ++k) ci32[k] = (int32_t)col_idx[k];

@@ -112,6 +112,8 @@ struct Operator {
     c.nnz = nnz;
     c.xlo = xlo;
     c.xhi = xhi;
+    c.blo = blo;
+    c.bhi = bhi;
     c.row_ptr = static_cast<const int32_t*>(rp->ptr);
     c.col_idx = static_cast<const int32_t*>(ci->ptr);
     c.values = val->d();
@@ -131,6 +133,7 @@ struct Operator {
   }
   std::vector<int32_t> offsets;  // DIA offsets (host copy)
   // DIA form of the same matrix (kernels.h DevCsr), built at upload when it pays off
+  int64_t blo = 0, bhi = 0;  // column band (kernels.h DevCsr)
   int32_t ndiag = 0;
   int64_t dia_ld = 0;
   DevPtr dia_val, dia_off;

@@ -1,0 +1,136 @@
+"""BASELINE config c5: the (s, ell) parameter sweep on the 256^3 7-point conv-diff sequence, M(s,ell)stab
+with recycling vs plain IDR(s)stab(ell) (every right-hand side solved fresh; s = ell = 1 is BiCGStab,
+test_solvers.cpp:514-541), on one B200.
+
+For every (s, ell) in {1,2,4,8,16} x {1,2,4,8}, both variants run the same 10-RHS implicit-Euler
+sequence (b_{i+1} = h^2 (x_i/dt + f), each variant chained on its own solutions) with device-resident
+b/x; the whole sequence is timed with CUDA events on the solver stream (first solve included: it
+is the fresh IDRstab that starts the recycling chain). Per (s, ell) it records RHS/s, cycles and
+matrix-vector products per RHS, the worst true relative residual, and the per-kernel average
+duration / HBM GB/s of a second, profiled pass over the first 3 right-hand sides of the Mstab
+variant (CUDA events around every launch; they slow the step, so the timed pass runs without them).
+
+usage: python tools/sweep_c5.py [--grid 256] [--rhs 10] [--s 1,2,4,8,16] [--ell 1,2,4,8] [--out FILE]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import bench  # noqa: E402  (Sequence, peaks, Clocks)
+
+
+def run_sequence(m, cfg, op, ctx, torch, stream, n_rhs, recycle):
+    seq = bench.Sequence(m, cfg, op, ctx, seed=0, device_mode=True, torch=torch, n_steps=n_rhs + 1)
+    h_mv = []
+    ctx.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n_rhs):
+        if not recycle:
+            seq.rec = None  # plain IDR(s)stab(ell): every right-hand side starts fresh
+        r = seq.step()
+        h_mv.append(int(r._rep.h_mv))
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    log = seq.log
+    return {
+        "rhs_per_s": round(n_rhs / (ms / 1e3), 4), "ms_total": round(ms, 3),
+        "cycles": [r["cycles"] for r in log], "h_mv": h_mv,
+        "mean_cycles": float(np.mean([r["cycles"] for r in log])),
+        "max_true_relres": max(r["relres"] for r in log),
+        "all_converged": all(r["status"] == 0 for r in log), "restarts": seq.restarts,
+    }
+
+
+def kernel_profile(m, lib, cfg, op, ctx, torch, n_rhs, hbm):
+    from paper_1604_06043_b200 import _capi
+    seq = bench.Sequence(m, cfg, op, ctx, seed=0, device_mode=True, torch=torch, n_steps=n_rhs + 1)
+    ctx.synchronize()
+    lib.dll.mstab_profiling_reset()
+    lib.dll.mstab_profiling_enable(1)
+    for _ in range(n_rhs):
+        seq.step()
+    ctx.synchronize()
+    lib.dll.mstab_profiling_enable(0)
+    stats = (_capi.KernelClassStatsC * 16)()
+    ncls = lib.dll.mstab_profiling_read(stats, 16)
+    out = {}
+    for i in range(ncls):
+        s = stats[i]
+        if s.launches == 0:
+            continue
+        avg_ms = s.total_ms / s.launches
+        gbs = (s.total_bytes / s.launches) / (avg_ms / 1e3) / 1e9 if avg_ms > 0 else 0.0
+        out[lib.dll.mstab_kernel_class_name(i).decode()] = {
+            "launches": int(s.launches), "avg_us": round(avg_ms * 1e3, 2), "gbs": round(gbs, 1),
+            "frac": round(gbs / hbm, 3)}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--grid", type=int, default=256)
+    ap.add_argument("--rhs", type=int, default=10)
+    ap.add_argument("--s", default="1,2,4,8,16")
+    ap.add_argument("--ell", default="1,2,4,8")
+    ap.add_argument("--profile-rhs", type=int, default=3)
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+    import torch
+    import paper_1604_06043_b200 as m
+    from paper_1604_06043_b200 import problems as pb
+
+    lib = m.Lib()
+    ctx = m.Context(lib, 0)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    base = pb.config("c5", grid=args.grid)
+    t0 = time.perf_counter()
+    A = base.matrix()
+    op = m.CsrOperator(A, ctx)
+    setup_s = time.perf_counter() - t0
+    hbm, hbm_src = bench.peaks()
+    rows = []
+    with bench.Clocks(0) as clk:
+        for s in [int(v) for v in args.s.split(",")]:
+            for ell in [int(v) for v in args.ell.split(",")]:
+                cfg = pb.config("c5", grid=args.grid)
+                cfg.s, cfg.ell = s, ell
+                row = {"s": s, "ell": ell}
+                try:
+                    row["mstab"] = run_sequence(m, cfg, op, ctx, torch, stream, args.rhs, recycle=True)
+                    row["idrstab"] = run_sequence(m, cfg, op, ctx, torch, stream, args.rhs, recycle=False)
+                    if args.profile_rhs > 0:
+                        row["kernels"] = kernel_profile(m, lib, cfg, op, ctx, torch, args.profile_rhs, hbm)
+                except m.Error as e:  # reported, not hidden: a breakdown of one (s, ell) is a result
+                    row["error"] = f"{type(e).__name__}: {e}"
+                rows.append(row)
+                ms, ids = row.get("mstab", {}), row.get("idrstab", {})
+                print(f"s={s:2d} ell={ell}  mstab {ms.get('rhs_per_s', 0):8.3f} RHS/s cycles "
+                      f"{ms.get('mean_cycles', 0):7.1f} relres {ms.get('max_true_relres', 0):.1e}  |  idrstab "
+                      f"{ids.get('rhs_per_s', 0):8.3f} RHS/s cycles {ids.get('mean_cycles', 0):7.1f}"
+                      + (f"  {row['error']}" if "error" in row else ""), flush=True)
+    out = {
+        "workload": f"c5: 3-D conv-diff {args.grid}^3 7-pt upwind, beta=(1,.5,.25)*200, implicit-Euler "
+                    f"sequence of {args.rhs} RHS, tol 1e-8 (true residual), fetch at half tolerance; "
+                    "synthetic seeded inputs (DESIGN.md §5)",
+        "N": int(A.n_rows), "nnz": int(A.nnz()), "n_gpus": 1, "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src,
+        "operator_setup_s": round(setup_s, 2), "clocks": clk.summary(), "rows": rows,
+    }
+    text = json.dumps(out)
+    if args.out:
+        Path(args.out).write_text(json.dumps(out, indent=1))
+    print(text)
+
+
+if __name__ == "__main__":
+    main()
