@@ -44,6 +44,7 @@ extern "C" {
 #define MSTAB_E_IO (-7)            /* mstab::IoError */
 #define MSTAB_E_SINGULAR (-8)      /* mstab::SingularProjection (only from the kernel helpers) */
 #define MSTAB_E_RANK (-9)          /* mstab::RankDeficient (only from the kernel helpers) */
+#define MSTAB_E_ZEROPIVOT (-10)    /* mstab::ZeroPivot (build_jacobi / build_ilu0, precond.cpp:33,56-82) */
 #define MSTAB_E_CUDA (-20)         /* device/runtime failure (no reference counterpart) */
 #define MSTAB_E_NOTREAL (-21)      /* complex data rejected: this build is the real fp64 path */
 
@@ -146,6 +147,36 @@ void* mstab_context_stream(mstab_context* ctx);
 int mstab_operator_create_csr(mstab_context* ctx, int64_t n, const int64_t* row_ptr,
                               const int64_t* col_idx, const double* values, mstab_operator** out);
 void mstab_operator_destroy(mstab_operator* op);
+
+/* ---- split preconditioning (precond.hpp, precond.cpp) -----------------------
+ * PrecondKind (precond.hpp:12). mstab_precond_build restates build_jacobi / build_ilu0
+ * (precond.cpp:23-99) on the host: the factors L (lower, diagonal stored) and R (upper) of A in CSR
+ * with ascending columns, like CsrMatrix::from_triplets. Each output array must hold nnz(A) + n
+ * entries (row_ptr: n + 1); *l_nnz / *r_nnz receive the counts. Errors: MSTAB_E_ZEROPIVOT
+ * (ZeroPivot), MSTAB_E_NOTREAL (Jacobi on a negative diagonal: the reference's square root is
+ * imaginary).
+ * mstab_operator_create_precond is PreconditionedOperator(pc, a) (precond.hpp:57-74): the operator
+ * L^-1 A R^-1 on the device, with the reference's combined fingerprint (precond.cpp:203-210).
+ * Every apply runs the upper solve, the SpMV and the lower solve on the device; the triangular
+ * solves are bit-identical to upper_solve / lower_solve (precond.cpp:101-133). kind NONE gives
+ * the plain CsrOperator (factors ignored). Single-GPU contexts only.
+ * mstab_precond_solve: y = L^-1 x (which = 0: lower_solve, preconditioned_rhs) or y = R^-1 x
+ * (which = 1: upper_solve, unpreconditioned_solution), mem as in mstab_operator_apply. */
+#define MSTAB_PRECOND_NONE 0
+#define MSTAB_PRECOND_JACOBI 1
+#define MSTAB_PRECOND_ILU0 2
+int mstab_precond_build(int32_t kind, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                        const double* values, int64_t* l_row_ptr, int64_t* l_col_idx, double* l_values,
+                        int64_t* l_nnz, int64_t* r_row_ptr, int64_t* r_col_idx, double* r_values,
+                        int64_t* r_nnz);
+int mstab_operator_create_precond(mstab_context* ctx, int64_t n, const int64_t* row_ptr,
+                                  const int64_t* col_idx, const double* values, int32_t kind,
+                                  const int64_t* l_row_ptr, const int64_t* l_col_idx, const double* l_values,
+                                  const int64_t* r_row_ptr, const int64_t* r_col_idx, const double* r_values,
+                                  mstab_operator** out);
+int32_t mstab_operator_precond_kind(const mstab_operator* op);
+int mstab_precond_solve(mstab_context* ctx, const mstab_operator* op, int32_t which, const double* x, double* y,
+                        int32_t mem);
 int64_t mstab_operator_size(const mstab_operator* op);        /* LinearOperator::size (operator.hpp:21) */
 int64_t mstab_operator_nnz(const mstab_operator* op);
 uint64_t mstab_operator_fingerprint(const mstab_operator* op); /* operator.cpp:35 */

@@ -13,6 +13,7 @@
 #include "mstab/errors.hpp"
 #include "mstab/kernels.hpp"
 #include "mstab/operator.hpp"
+#include "mstab/precond.hpp"
 #include "mstab/recycle.hpp"
 #include "mstab/solvers/baselines.hpp"
 #include "mstab/solvers/idrstab.hpp"
@@ -26,7 +27,8 @@ struct mstab_context {
 };
 struct mstab_operator {
   mstab::CsrMatrix m;
-  std::unique_ptr<mstab::CsrOperator> op;
+  mstab::SplitPreconditioner pc;  // build_none() unless created by mstab_operator_create_precond
+  std::unique_ptr<mstab::LinearOperator> op;  // CsrOperator or PreconditionedOperator(pc, m)
   uint64_t fp = 0;
 };
 struct mstab_recycle {
@@ -41,6 +43,9 @@ namespace {
 thread_local std::string g_err;
 
 struct ConfigErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NotRealErr : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
@@ -73,12 +78,18 @@ int guarded(F&& f) {
   } catch (const mstab::RankDeficient& e) {
     g_err = e.what();
     return MSTAB_E_RANK;
+  } catch (const mstab::ZeroPivot& e) {
+    g_err = e.what();
+    return MSTAB_E_ZEROPIVOT;
   } catch (const mstab::Error& e) {
     g_err = e.what();
     return MSTAB_E_ERROR;
   } catch (const ConfigErr& e) {
     g_err = e.what();
     return MSTAB_E_CONFIG;
+  } catch (const NotRealErr& e) {
+    g_err = e.what();
+    return MSTAB_E_NOTREAL;
   } catch (const std::exception& e) {
     g_err = e.what();
     return MSTAB_E_ERROR;
@@ -87,6 +98,28 @@ int guarded(F&& f) {
 
 void host_only(int32_t mem) {
   if (mem != MSTAB_MEM_HOST) throw ConfigErr("reference implementation: host memory only");
+}
+
+mstab::CsrMatrix to_csr(int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const double* values) {
+  mstab::CsrMatrix m;
+  m.n_rows = m.n_cols = (size_t)n;
+  const int64_t nnz = row_ptr[n];
+  m.row_ptr.assign(row_ptr, row_ptr + n + 1);
+  m.col_idx.assign(col_idx, col_idx + nnz);
+  m.values.resize((size_t)nnz);
+  for (int64_t k = 0; k < nnz; ++k) m.values[(size_t)k] = Complex(values[k], 0.0);
+  m.validate();
+  return m;
+}
+
+void from_csr(const mstab::CsrMatrix& m, int64_t* rp, int64_t* ci, double* val, int64_t* nnz) {
+  for (size_t i = 0; i <= m.n_rows; ++i) rp[i] = (int64_t)m.row_ptr[i];
+  for (size_t k = 0; k < m.col_idx.size(); ++k) {
+    if (m.values[k].imag() != 0.0) throw NotRealErr("precond: complex factor");
+    ci[k] = (int64_t)m.col_idx[k];
+    val[k] = m.values[k].real();
+  }
+  *nnz = (int64_t)m.col_idx.size();
 }
 
 mstab::Vector to_vec(const double* x, int64_t n) {
@@ -139,6 +172,65 @@ int mstab_operator_create_csr(mstab_context*, int64_t n, const int64_t* row_ptr,
     o->op = std::make_unique<mstab::CsrOperator>(o->m);
     o->fp = o->op->fingerprint();
     *out = o.release();
+  });
+}
+
+int mstab_precond_build(int32_t kind, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                        const double* values, int64_t* l_row_ptr, int64_t* l_col_idx, double* l_values,
+                        int64_t* l_nnz, int64_t* r_row_ptr, int64_t* r_col_idx, double* r_values,
+                        int64_t* r_nnz) {
+  return guarded([&] {
+    const mstab::CsrMatrix a = to_csr(n, row_ptr, col_idx, values);
+    mstab::SplitPreconditioner pc;
+    if (kind == MSTAB_PRECOND_JACOBI)
+      pc = mstab::build_jacobi(a);
+    else if (kind == MSTAB_PRECOND_ILU0)
+      pc = mstab::build_ilu0(a);
+    else
+      throw ConfigErr("precond: unknown kind");
+    from_csr(pc.l_factor, l_row_ptr, l_col_idx, l_values, l_nnz);
+    from_csr(pc.r_factor, r_row_ptr, r_col_idx, r_values, r_nnz);
+  });
+}
+
+int mstab_operator_create_precond(mstab_context*, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                  const double* values, int32_t kind, const int64_t* l_row_ptr,
+                                  const int64_t* l_col_idx, const double* l_values, const int64_t* r_row_ptr,
+                                  const int64_t* r_col_idx, const double* r_values, mstab_operator** out) {
+  return guarded([&] {
+    auto o = std::make_unique<mstab_operator>();
+    o->m = to_csr(n, row_ptr, col_idx, values);
+    if (kind == MSTAB_PRECOND_NONE) {
+      o->op = std::make_unique<mstab::CsrOperator>(o->m);
+    } else {
+      if (kind != MSTAB_PRECOND_JACOBI && kind != MSTAB_PRECOND_ILU0) throw ConfigErr("precond: unknown kind");
+      o->pc.kind = kind == MSTAB_PRECOND_JACOBI ? mstab::PrecondKind::Jacobi : mstab::PrecondKind::Ilu0;
+      o->pc.l_factor = to_csr(n, l_row_ptr, l_col_idx, l_values);
+      o->pc.r_factor = to_csr(n, r_row_ptr, r_col_idx, r_values);
+      o->op = std::make_unique<mstab::PreconditionedOperator>(o->pc, o->m);
+    }
+    o->fp = o->op->fingerprint();
+    *out = o.release();
+  });
+}
+
+int32_t mstab_operator_precond_kind(const mstab_operator* op) {
+  if (!op) return MSTAB_PRECOND_NONE;
+  return op->pc.kind == mstab::PrecondKind::Jacobi ? MSTAB_PRECOND_JACOBI
+         : op->pc.kind == mstab::PrecondKind::Ilu0 ? MSTAB_PRECOND_ILU0
+                                                    : MSTAB_PRECOND_NONE;
+}
+
+int mstab_precond_solve(mstab_context*, const mstab_operator* op, int32_t which, const double* x, double* y,
+                        int32_t mem) {
+  return guarded([&] {
+    host_only(mem);
+    const int64_t n = (int64_t)op->m.n_rows;
+    if (which != 0 && which != 1) throw ConfigErr("precond_solve: which must be 0 (L) or 1 (R)");
+    const mstab::Vector xv = to_vec(x, n);
+    const mstab::Vector out = which == 0 ? mstab::preconditioned_rhs(op->pc, xv)
+                                         : mstab::unpreconditioned_solution(op->pc, xv);
+    for (int64_t i = 0; i < n; ++i) y[i] = out[(size_t)i].real();
   });
 }
 // Row-sharded solves are a B200 extension (the reference is single-process): the

@@ -84,6 +84,12 @@ ABI = [
     ("mstab_operator_nnz", C.c_int64, [_P]),
     ("mstab_operator_fingerprint", C.c_uint64, [_P]),
     ("mstab_operator_apply", C.c_int, [_P, _P, _P, _P, C.c_int32]),
+    ("mstab_precond_build", C.c_int, [C.c_int32, C.c_int64, _I64, _I64, _D, _I64, _I64, _D, _I64, _I64, _I64, _D,
+                                      _I64]),
+    ("mstab_operator_create_precond", C.c_int, [_P, C.c_int64, _I64, _I64, _D, C.c_int32, _I64, _I64, _D, _I64,
+                                                _I64, _D, C.POINTER(_P)]),
+    ("mstab_operator_precond_kind", C.c_int32, [_P]),
+    ("mstab_precond_solve", C.c_int, [_P, _P, C.c_int32, _P, _P, C.c_int32]),
     ("mstab_recycle_create", C.c_int, [_P, C.c_int64, C.c_int64, _P, _P, _P, C.c_int32, _D, C.c_int64,
                                        C.c_int64, C.c_uint64, C.POINTER(_P)]),
     ("mstab_recycle_destroy", None, [_P]),

@@ -166,6 +166,55 @@ int mstab_operator_apply(mstab_context* ctx, const mstab_operator* op, const dou
   });
 }
 
+int mstab_precond_build(int32_t kind, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                        const double* values, int64_t* l_row_ptr, int64_t* l_col_idx, double* l_values,
+                        int64_t* l_nnz, int64_t* r_row_ptr, int64_t* r_col_idx, double* r_values,
+                        int64_t* r_nnz) {
+  return guarded([&] {
+    precond_build(kind, n, row_ptr, col_idx, values, l_row_ptr, l_col_idx, l_values, r_row_ptr, r_col_idx,
+                  r_values);
+    *l_nnz = l_row_ptr[n];
+    *r_nnz = r_row_ptr[n];
+  });
+}
+
+int mstab_operator_create_precond(mstab_context* ctx, int64_t n, const int64_t* row_ptr,
+                                  const int64_t* col_idx, const double* values, int32_t kind,
+                                  const int64_t* l_row_ptr, const int64_t* l_col_idx, const double* l_values,
+                                  const int64_t* r_row_ptr, const int64_t* r_col_idx, const double* r_values,
+                                  mstab_operator** out) {
+  return guarded([&] {
+    bind(ctx);
+    auto o = std::make_unique<mstab_operator>();
+    o->impl = make_operator_precond(*ctx->impl, n, row_ptr, col_idx, values, kind, l_row_ptr, l_col_idx, l_values,
+                                    r_row_ptr, r_col_idx, r_values);
+    *out = o.release();
+  });
+}
+
+int32_t mstab_operator_precond_kind(const mstab_operator* op) {
+  return op && op->impl && op->impl->pc ? op->impl->pc->kind : MSTAB_PRECOND_NONE;
+}
+
+int mstab_precond_solve(mstab_context* ctx, const mstab_operator* op, int32_t which, const double* x, double* y,
+                        int32_t mem) {
+  return guarded([&] {
+    bind(ctx);
+    Context& c = *ctx->impl;
+    const int64_t n = op->impl->n;
+    if (which != 0 && which != 1) throw Error(MSTAB_E_CONFIG, "precond_solve: which must be 0 (L) or 1 (R)");
+    const cudaMemcpyKind in = mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const cudaMemcpyKind out = mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    DevPtr dx = c.alloc_vecs(n, 1), dy = c.alloc_vecs(n, 1);
+    if (cudaMemcpyAsync(dx->d(), x, sizeof(double) * n, in, c.stream()) != cudaSuccess)
+      throw Error(MSTAB_E_CUDA, "upload x");
+    precond_solve(c, *op->impl, which, dx->d(), dy->d());
+    if (cudaMemcpyAsync(y, dy->d(), sizeof(double) * n, out, c.stream()) != cudaSuccess)
+      throw Error(MSTAB_E_CUDA, "download y");
+    c.sync();
+  });
+}
+
 int mstab_recycle_create(mstab_context* ctx, int64_t n, int64_t s, const double* p, const double* u,
                          const double* v, int32_t mem, const double* omega_re_im,
                          int64_t omega_count, int64_t level_j, uint64_t fingerprint,

@@ -182,8 +182,29 @@ void launch_prologue(cudaStream_t st, int64_t n, int64_t ld, int s, const double
 
 // ---- validate (recycle.cpp:40-83): ||V - A U||^2, ||V||^2 per column, P^H P, V^H V ----------
 // Results land in ds->scal[0..1] (dev_num, dev_den) and ds->gram (P^H P then V^H V).
+// ---- split preconditioning (ktri.cu, precond.cpp:23-219) ------------------------------------
+// One triangular factor of a SplitPreconditioner on the device: CSR (int32) in ascending column
+// order as CsrMatrix::from_triplets leaves it, or, for a diagonal-only factor (split Jacobi),
+// just the diagonal (`diag` non-null).
+struct DevTri {
+  int64_t n = 0, nnz = 0;
+  const int32_t* rp = nullptr;
+  const int32_t* ci = nullptr;
+  const double* val = nullptr;
+  const double* diag = nullptr;
+  bool lower = true;
+};
+// x = F^-1 b (lower_solve / upper_solve, precond.cpp:101-133), bit-identical; `sync` is n + 1
+// ints of scratch (done flags + ticket), zeroed by the launcher.
+void launch_tri_solve(cudaStream_t st, const DevTri& f, const double* b, double* x, int* sync);
+// y = w (b == nullptr) or y = b - w, with the P^H y (+ ||y||^2) reduction and finalize_spmv(fin).
+void launch_ph_fin(cudaStream_t st, int64_t n, int64_t ld, int s, const double* w, double* y, const double* p,
+                   const double* b, const FinParams& fin, const Reducer& red);
+
+// au: the products A U precomputed by the caller (preconditioned operators), else nullptr and
+// the kernel forms them from the CSR.
 void launch_validate(cudaStream_t st, const DevCsr& a, const double* p, const double* u,
-                     const double* v, int64_t ld, int s, const Reducer& red);
+                     const double* v, int64_t ld, int s, const Reducer& red, const double* au = nullptr);
 
 // ---- generic helpers (initialisation paths; not per-cycle) --------------------------------
 // dst[j] = dot(A_j, y) for j < na (A_j = a + j*ld); dst[na] = ||y||^2 when with_norm.

@@ -206,7 +206,7 @@ template <int S>
 __global__ void __launch_bounds__(kBlock) k_validate(DevCsr a, const double* __restrict__ p,
                                                      const double* __restrict__ u,
                                                      const double* __restrict__ v, int64_t ld,
-                                                     Reducer red) {
+                                                     Reducer red, const double* __restrict__ au) {
   DevState* ds = red.ds;
   using GM = GramMap<S>;
   extern __shared__ double dsm[];
@@ -221,12 +221,17 @@ __global__ void __launch_bounds__(kBlock) k_validate(DevCsr a, const double* __r
       double acc[S];
 #pragma unroll
       for (int q = 0; q < S; ++q) acc[q] = 0.0;
-      const int beg = a.row_ptr[row], end = a.row_ptr[row + 1];
-      for (int k = beg; k < end; ++k) {
-        const double av = a.values[k];
-        const int col = a.col_idx[k];
+      if (au) {
 #pragma unroll
-        for (int q = 0; q < S; ++q) acc[q] = acc[q] + av * __ldg(u + q * ld + col);
+        for (int q = 0; q < S; ++q) acc[q] = au[q * ld + row];
+      } else {
+        const int beg = a.row_ptr[row], end = a.row_ptr[row + 1];
+        for (int k = beg; k < end; ++k) {
+          const double av = a.values[k];
+          const int col = a.col_idx[k];
+#pragma unroll
+          for (int q = 0; q < S; ++q) acc[q] = acc[q] + av * __ldg(u + q * ld + col);
+        }
       }
 #pragma unroll
       for (int q = 0; q < S; ++q) {
@@ -324,13 +329,13 @@ void launch_prologue(cudaStream_t st, int64_t n, int64_t ld, int s, const double
 }
 
 void launch_validate(cudaStream_t st, const DevCsr& a, const double* p, const double* u,
-                     const double* v, int64_t ld, int s, const Reducer& red) {
+                     const double* v, int64_t ld, int s, const Reducer& red, const double* au) {
   LaunchScope ls(st, kKValidate, csr_bytes(a) + vbytes(a.n, 3.0 * s));
   MSTAB_DISPATCH_S(s, {
     auto kfn = k_validate<S>;
     const size_t sm = gram_smem<S>();
     const int grid = occupancy_grid(kfn, a.n, sm);
-    kfn<<<grid, kBlock, sm, st>>>(a, p, u, v, ld, red);
+    kfn<<<grid, kBlock, sm, st>>>(a, p, u, v, ld, red, au);
   });
 }
 

@@ -174,8 +174,39 @@ void after_stats(Context& ctx, double* dst) {
   check_launch();
 }
 
+// w = L^-1 A R^-1 x for a preconditioned operator (apply_preconditioned, precond.cpp:169-174):
+// upper solve, SpMV (its fused dot is discarded), lower solve.
+void precond_chain(Context& ctx, const Operator& op, const double* x, double* w) {
+  Precond& pc = *op.pc;
+  cudaStream_t st = ctx.stream();
+  launch_tri_solve(st, pc.R, x, pc.t1->d(), reinterpret_cast<int*>(pc.sync->ptr));
+  FinParams f;
+  f.op = kFinStore;
+  f.s = 1;
+  f.dst = scal(ctx, 63);
+  launch_spmv_ph(st, op.csr(), pc.t1->d(), pc.t2->d(), pc.t1->d(), ctx.ld(op.n), 1, nullptr, f, ctx.reducer());
+  launch_tri_solve(st, pc.L, pc.t2->d(), w, reinterpret_cast<int*>(pc.sync->ptr));
+  check_launch();
+}
+
+// y = op x (or the true residual y = b - op x) with the fused P^H epilogue and finaliser `f`:
+// one kernel for a plain CSR operator, the preconditioned chain + k_ph_fin otherwise.
+void apply_ph(Context& ctx, const Operator& op, const double* x, double* y, const double* P, int s,
+              const double* b, const FinParams& f) {
+  if (!op.pc) {
+    launch_spmv_ph(ctx.stream(), op.csr(), x, y, P, ctx.ld(op.n), s, b, f, ctx.reducer());
+    return;
+  }
+  precond_chain(ctx, op, x, op.pc->t3->d());
+  launch_ph_fin(ctx.stream(), op.n, ctx.ld(op.n), s, op.pc->t3->d(), y, P, b, f, ctx.reducer());
+}
+
 // Plain SpMV through the fused kernel (s = 1, dot with x discarded).
 void spmv_dev(Context& ctx, const Operator& op, const double* x, double* y) {
+  if (op.pc) {
+    precond_chain(ctx, op, x, y);
+    return;
+  }
   FinParams f;
   f.op = kFinStore;
   f.s = 1;
@@ -304,7 +335,6 @@ void enqueue_cycle(Context& ctx, const Operator& op, const double* P, int s, int
   cudaStream_t st = ctx.stream();
   DevState* ds = ctx.ds();
   const Reducer red = ctx.reducer();
-  const DevCsr A = op.csr();
   auto col = [ld](double* base, int q) { return base + (size_t)q * ld; };
   for (int k = 0; k < ell; ++k) {
     // (a) top level: r^(k) -= V^(k) gamma_k
@@ -320,7 +350,7 @@ void enqueue_cycle(Context& ctx, const Operator& op, const double* P, int s, int
     fb.k = k;
     fb.ell = ell;
     if (shard) halo(ctx, op, r_out);
-    launch_spmv_ph(st, A, r_out, R[k + 1]->d(), P, ld, s, nullptr, fb, red);
+    apply_ph(ctx, op, r_out, R[k + 1]->d(), P, s, nullptr, fb);
     if (shard) after_spmv(ctx, s, false, fb);
     // (c) column rebuilds at the top level, each raised by one SpMV
     for (int q = 0; q < s; ++q) {
@@ -332,7 +362,7 @@ void enqueue_cycle(Context& ctx, const Operator& op, const double* P, int s, int
       fc.q = q;
       fc.ell = ell;
       if (shard) halo(ctx, op, col(vk_new, q));
-      launch_spmv_ph(st, A, col(vk_new, q), col(VL[k + 1]->d(), q), P, ld, s, nullptr, fc, red);
+      apply_ph(ctx, op, col(vk_new, q), col(VL[k + 1]->d(), q), P, s, nullptr, fc);
       if (shard) after_spmv(ctx, s, false, fc);
     }
     // deferred (a) for r^(0..k-1), x and (c) for levels -1..k-1
@@ -586,6 +616,177 @@ std::shared_ptr<Operator> make_operator_slab(Context& ctx, int64_t n, const int6
   return op;
 }
 
+// ---- split preconditioning (precond.cpp) --------------------------------------------------------
+namespace {
+
+// max |a_ij| (precond.cpp:13-17)
+double diag_scale(int64_t nnz, const double* values) {
+  double s = 0.0;
+  for (int64_t k = 0; k < nnz; ++k) s = std::max(s, std::abs(values[k]));
+  return s;
+}
+
+std::string zero_pivot(int64_t row) { return "zero pivot in row " + std::to_string(row); }
+
+// Builds the CSR of a factor from per-row (col, value) lists already in ascending column order.
+void emit_rows(int64_t n, const std::vector<std::vector<std::pair<int64_t, double>>>& rows, int64_t* rp,
+               int64_t* ci, double* val) {
+  rp[0] = 0;
+  int64_t k = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    for (const auto& e : rows[i]) {
+      ci[k] = e.first;
+      val[k] = e.second;
+      ++k;
+    }
+    rp[i + 1] = k;
+  }
+}
+
+DevTri upload_factor(Context& ctx, int64_t n, const int64_t* rp, const int64_t* ci, const double* val, bool lower,
+                     DevPtr& d_rp, DevPtr& d_ci, DevPtr& d_val, DevPtr& d_diag) {
+  DevTri f;
+  f.n = n;
+  f.nnz = rp[n];
+  f.lower = lower;
+  cudaStream_t st = ctx.stream();
+  bool diagonal = f.nnz == n;
+  for (int64_t i = 0; i < n && diagonal; ++i) diagonal = rp[i + 1] - rp[i] == 1 && ci[rp[i]] == i;
+  if (diagonal) {  // split Jacobi: the factor is its diagonal
+    d_diag = ctx.alloc(sizeof(double) * std::max<int64_t>(n, 1));
+    CUDA_OK(cudaMemcpyAsync(d_diag->ptr, val, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    f.diag = d_diag->d();
+    ctx.sync();
+    return f;
+  }
+  std::vector<int32_t> rp32(n + 1), ci32(std::max<int64_t>(f.nnz, 1));
+  for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)rp[i];
+  for (int64_t k = 0; k < f.nnz; ++k) ci32[k] = (int32_t)ci[k];
+  d_rp = ctx.alloc(sizeof(int32_t) * (n + 1));
+  d_ci = ctx.alloc(sizeof(int32_t) * ci32.size());
+  d_val = ctx.alloc(sizeof(double) * ci32.size());
+  CUDA_OK(cudaMemcpyAsync(d_rp->ptr, rp32.data(), sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, st));
+  CUDA_OK(cudaMemcpyAsync(d_ci->ptr, ci32.data(), sizeof(int32_t) * ci32.size(), cudaMemcpyHostToDevice, st));
+  CUDA_OK(cudaMemcpyAsync(d_val->ptr, val, sizeof(double) * std::max<int64_t>(f.nnz, 0), cudaMemcpyHostToDevice, st));
+  f.rp = static_cast<const int32_t*>(d_rp->ptr);
+  f.ci = static_cast<const int32_t*>(d_ci->ptr);
+  f.val = d_val->d();
+  ctx.sync();
+  return f;
+}
+
+}  // namespace
+
+void precond_build(int kind, int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                   int64_t* l_rp, int64_t* l_ci, double* l_val, int64_t* r_rp, int64_t* r_ci, double* r_val) {
+  validate_csr(n, row_ptr, col_idx);
+  const int64_t nnz = row_ptr[n];
+  const double scale = diag_scale(nnz, values);
+  std::vector<std::vector<std::pair<int64_t, double>>> lrows(n), rrows(n);
+  if (kind == MSTAB_PRECOND_JACOBI) {  // build_jacobi (precond.cpp:23-37)
+    for (int64_t i = 0; i < n; ++i) {
+      double d = 0.0;
+      for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k)
+        if (col_idx[k] == i) d = values[k];
+      if (std::abs(d) < 1e-14 * scale || scale == 0.0) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(i));
+      // std::sqrt of a complex with a negative real part is imaginary: not a real operator
+      if (d < 0.0) throw Error(MSTAB_E_NOTREAL, "jacobi: negative diagonal gives a complex square root");
+      lrows[i].push_back({i, std::sqrt(d)});
+      rrows[i].push_back({i, std::sqrt(d)});
+    }
+  } else if (kind == MSTAB_PRECOND_ILU0) {  // build_ilu0 (precond.cpp:39-99), IKJ on A's pattern
+    std::vector<double> val(values, values + nnz);
+    std::vector<int64_t> diag_pos(n, -1);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k)
+        if (col_idx[k] == i) diag_pos[i] = k;
+    for (int64_t i = 0; i < n; ++i)
+      if (diag_pos[i] < 0) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(i));
+    for (int64_t i = 0; i < n; ++i) {
+      for (int64_t ki = row_ptr[i]; ki < row_ptr[i + 1]; ++ki) {
+        const int64_t k = col_idx[ki];
+        if (k >= i) break;
+        const double piv = val[diag_pos[k]];
+        if (std::abs(piv) < 1e-14 * scale || scale == 0.0) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(k));
+        const double lik = val[ki] / piv;
+        val[ki] = lik;
+        int64_t pk = diag_pos[k] + 1, pi = ki + 1;
+        while (pk < row_ptr[k + 1] && pi < row_ptr[i + 1]) {
+          if (col_idx[pk] < col_idx[pi]) {
+            ++pk;
+          } else if (col_idx[pk] > col_idx[pi]) {
+            ++pi;
+          } else {
+            val[pi] = val[pi] - lik * val[pk];
+            ++pk;
+            ++pi;
+          }
+        }
+      }
+      if (std::abs(val[diag_pos[i]]) < 1e-14 * scale || scale == 0.0) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(i));
+    }
+    // unit lower L (explicit 1.0 diagonal, last in its row) and upper R carrying the pivots
+    for (int64_t i = 0; i < n; ++i) {
+      for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+        if (col_idx[k] < i)
+          lrows[i].push_back({col_idx[k], val[k]});
+        else
+          rrows[i].push_back({col_idx[k], val[k]});
+      }
+      lrows[i].push_back({i, 1.0});
+    }
+  } else {
+    throw Error(MSTAB_E_CONFIG, "precond: unknown kind");
+  }
+  emit_rows(n, lrows, l_rp, l_ci, l_val);
+  emit_rows(n, rrows, r_rp, r_ci, r_val);
+}
+
+std::shared_ptr<Operator> make_operator_precond(Context& ctx, int64_t n, const int64_t* row_ptr,
+                                                const int64_t* col_idx, const double* values, int kind,
+                                                const int64_t* l_rp, const int64_t* l_ci, const double* l_val,
+                                                const int64_t* r_rp, const int64_t* r_ci, const double* r_val) {
+  if (ctx.comm) throw Error(MSTAB_E_CONFIG, "b200: preconditioned operators are single-GPU");
+  auto op = make_operator(ctx, n, row_ptr, col_idx, values);
+  if (kind == MSTAB_PRECOND_NONE) return op;
+  if (kind != MSTAB_PRECOND_JACOBI && kind != MSTAB_PRECOND_ILU0) throw Error(MSTAB_E_CONFIG, "precond: unknown kind");
+  validate_csr(n, l_rp, l_ci);
+  validate_csr(n, r_rp, r_ci);
+  for (int64_t i = 0; i < n; ++i) {  // the solves need one stored diagonal entry per row
+    bool dl = false, dr = false;
+    for (int64_t k = l_rp[i]; k < l_rp[i + 1]; ++k) dl = dl || (l_ci[k] == i && l_val[k] != 0.0);
+    for (int64_t k = r_rp[i]; k < r_rp[i + 1]; ++k) dr = dr || (r_ci[k] == i && r_val[k] != 0.0);
+    if (!dl || !dr) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(i));
+  }
+  // PreconditionedOperator::fingerprint (precond.cpp:203-210)
+  uint64_t h = op->fingerprint;
+  const uint64_t hl = fnv_csr_fingerprint(n, l_rp, l_ci, l_val, l_rp[n]);
+  h ^= hl + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  const uint64_t hr = fnv_csr_fingerprint(n, r_rp, r_ci, r_val, r_rp[n]);
+  h ^= hr + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  op->fingerprint = h;
+  auto pc = std::make_shared<Precond>();
+  pc->kind = kind;
+  pc->L = upload_factor(ctx, n, l_rp, l_ci, l_val, true, pc->l_rp, pc->l_ci, pc->l_val, pc->l_diag);
+  pc->R = upload_factor(ctx, n, r_rp, r_ci, r_val, false, pc->r_rp, pc->r_ci, pc->r_val, pc->r_diag);
+  pc->t1 = ctx.alloc_vecs(n, 1);
+  pc->t2 = ctx.alloc_vecs(n, 1);
+  pc->t3 = ctx.alloc_vecs(n, 1);
+  pc->sync = ctx.alloc(sizeof(int) * (size_t)(n + 1));
+  op->pc = pc;
+  return op;
+}
+
+void precond_solve(Context& ctx, const Operator& op, int which, const double* x_dev, double* y_dev) {
+  if (!op.pc) {  // build_none: both factors are the identity
+    CUDA_OK(cudaMemcpyAsync(y_dev, x_dev, sizeof(double) * op.n, cudaMemcpyDeviceToDevice, ctx.stream()));
+    return;
+  }
+  launch_tri_solve(ctx.stream(), which == 0 ? op.pc->L : op.pc->R, x_dev, y_dev,
+                   reinterpret_cast<int*>(op.pc->sync->ptr));
+  check_launch();
+}
+
 void spmv(Context& ctx, const Operator& op, const double* x_dev, double* y_dev) {
   reset_status(ctx);
   spmv_dev(ctx, op, x_dev, y_dev);
@@ -601,7 +802,18 @@ mstab_validation_report validate(Context& ctx, const Recycle& rd, const Operator
   if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: recycle s must be in 1..16");
   const int64_t vld = ctx.ld(rd.n);
   for (int q = 0; q < s && ctx.sharded(); ++q) halo(ctx, op, rd.u->d() + (size_t)q * vld);
-  launch_validate(ctx.stream(), op.csr(), rd.p->d(), rd.u->d(), rd.v->d(), vld, s, ctx.reducer());
+  const double* au = nullptr;
+  if (op.pc) {  // A U through the preconditioned chain, column by column
+    Precond& pc = *op.pc;
+    if (!pc.au || pc.au_s < s) {
+      ctx.sync();
+      pc.au = ctx.alloc_vecs(op.n, s);
+      pc.au_s = s;
+    }
+    for (int q = 0; q < s; ++q) precond_chain(ctx, op, rd.u->d() + (size_t)q * vld, pc.au->d() + (size_t)q * vld);
+    au = pc.au->d();
+  }
+  launch_validate(ctx.stream(), op.csr(), rd.p->d(), rd.u->d(), rd.v->d(), vld, s, ctx.reducer(), au);
   check_launch();
   if (ctx.sharded()) {
     ctx.comm->allreduce_sum(xred(ctx), 2 + 2 * s * s, ctx.stream());
@@ -680,8 +892,7 @@ void enqueue_full_cycle(Context& ctx, const Operator& op, Workspace& w, int p) {
     ft.s = w.s;
     ft.ell = w.ell;
     halo(ctx, op, D.x->d());
-    launch_spmv_ph(ctx.stream(), op.csr(), D.x->d(), D.r->d(), w.P->d(), ctx.ld(op.n), w.s, w.b->d(), ft,
-                   ctx.reducer());
+    apply_ph(ctx, op, D.x->d(), D.r->d(), w.P->d(), w.s, w.b->d(), ft);
     check_launch();
     after_spmv(ctx, w.s, true, ft);
   }

@@ -98,6 +98,16 @@ struct Context {
   ~Context();
 };
 
+// Split preconditioner L, R of a preconditioned operator L^-1 A R^-1 (precond.hpp:16-24,
+// PreconditionedOperator), the factors on the device plus the scratch its applies use.
+struct Precond {
+  int kind = 0;  // MSTAB_PRECOND_*
+  DevPtr l_rp, l_ci, l_val, l_diag, r_rp, r_ci, r_val, r_diag;
+  DevTri L, R;
+  DevPtr t1, t2, t3, sync, au;  // chain temporaries, tri-solve flags, A U block of validate
+  int au_s = 0;
+};
+
 struct Operator {
   uint64_t uid = 0;  // unique per created operator (workspace/graph cache key)
   int64_t n = 0, nnz = 0;
@@ -142,6 +152,7 @@ struct Operator {
   int32_t mask_bytes = 0;
   std::vector<double> cvals;
   DevPtr dia_mask;
+  std::shared_ptr<Precond> pc;  // preconditioned operator L^-1 A R^-1 (nullptr: plain CSR)
 };
 
 struct Recycle {
@@ -178,6 +189,18 @@ std::shared_ptr<Operator> make_operator_slab(Context& ctx, int64_t n, const int6
                                              const int64_t* slab_starts);
 
 void spmv(Context& ctx, const Operator& op, const double* x_dev, double* y_dev);
+
+// build_jacobi / build_ilu0 (precond.cpp:23-99) on the host, real data: the factors in CSR with
+// ascending columns (CsrMatrix::from_triplets order). Capacities: nnz(A) + n entries each.
+void precond_build(int kind, int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                   int64_t* l_rp, int64_t* l_ci, double* l_val, int64_t* r_rp, int64_t* r_ci, double* r_val);
+// PreconditionedOperator(pc, a) (precond.cpp:188-219) with the factors given as CSR.
+std::shared_ptr<Operator> make_operator_precond(Context& ctx, int64_t n, const int64_t* row_ptr,
+                                                const int64_t* col_idx, const double* values, int kind,
+                                                const int64_t* l_rp, const int64_t* l_ci, const double* l_val,
+                                                const int64_t* r_rp, const int64_t* r_ci, const double* r_val);
+// y = L^-1 x (which = 0, lower_solve) or y = R^-1 x (which = 1, upper_solve) with the operator's factors.
+void precond_solve(Context& ctx, const Operator& op, int which, const double* x_dev, double* y_dev);
 
 // make_cut_space (baselines.cpp:36-47): returns the orthonormal n x s block P on the device.
 DevPtr make_cut_space(Context& ctx, int64_t n, int s, uint64_t seed);

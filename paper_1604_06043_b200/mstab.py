@@ -69,9 +69,13 @@ class NotReal(ConfigError):
     pass
 
 
+class ZeroPivot(Error):
+    """errors.hpp:39-45 (build_jacobi / build_ilu0)."""
+
+
 _ERR = {-1: Error, -2: DimensionMismatch, -3: ConfigError, -4: FingerprintMismatch, -5: StaleData,
         -6: ParseError, -7: IoError, -8: SingularProjection, -9: RankDeficient, -20: CudaError,
-        -21: NotReal}
+        -21: NotReal, -10: ZeroPivot}
 
 
 def _check(lib: Lib, rc: int):
@@ -408,6 +412,105 @@ class CsrOperator:
         if getattr(self, "h", None):
             self.lib.dll.mstab_operator_destroy(self.h)
             self.h = None
+
+
+# ---- split preconditioning (precond.hpp) ------------------------------------------------------
+class PrecondKind:
+    """precond.hpp:12."""
+    NONE = 0
+    JACOBI = 1
+    ILU0 = 2
+
+
+@dataclass
+class SplitPreconditioner:
+    """Split preconditioner L, R for L^-1 A R^-1 xt = L^-1 b (precond.hpp:16-24): L lower with its
+    diagonal stored, R upper with the pivots; immutable after build."""
+    l_factor: Optional[CsrMatrix]
+    r_factor: Optional[CsrMatrix]
+    kind: int = PrecondKind.NONE
+
+
+def _build(kind: int, a: CsrMatrix, lib: Optional[Lib] = None) -> SplitPreconditioner:
+    if a.n_rows != a.n_cols:
+        raise DimensionMismatch(("jacobi" if kind == PrecondKind.JACOBI else "ilu0") + ": square matrix required")
+    lib = lib or default_context().lib
+    n, cap = a.n_rows, a.nnz() + a.n_rows
+    lrp, rrp = np.empty(n + 1, np.int64), np.empty(n + 1, np.int64)
+    lci, rci = np.empty(max(cap, 1), np.int64), np.empty(max(cap, 1), np.int64)
+    lva, rva = np.empty(max(cap, 1)), np.empty(max(cap, 1))
+    ln, rn = C.c_int64(), C.c_int64()
+    _check(lib, lib.dll.mstab_precond_build(kind, n, i64ptr(a.row_ptr), i64ptr(a.col_idx), dptr(a.values),
+                                            i64ptr(lrp), i64ptr(lci), dptr(lva), C.byref(ln), i64ptr(rrp),
+                                            i64ptr(rci), dptr(rva), C.byref(rn)))
+    L = CsrMatrix(n, n, lrp, lci[:ln.value].copy(), lva[:ln.value].copy())
+    R = CsrMatrix(n, n, rrp, rci[:rn.value].copy(), rva[:rn.value].copy())
+    return SplitPreconditioner(L, R, kind)
+
+
+def build_jacobi(a: CsrMatrix, lib: Optional[Lib] = None) -> SplitPreconditioner:
+    """Split Jacobi, sqrt(diag) in both factors (precond.cpp:23-37). Raises ZeroPivot."""
+    return _build(PrecondKind.JACOBI, a, lib)
+
+
+def build_ilu0(a: CsrMatrix, lib: Optional[Lib] = None) -> SplitPreconditioner:
+    """ILU(0) on A's pattern, IKJ order (precond.cpp:39-99). Raises ZeroPivot."""
+    return _build(PrecondKind.ILU0, a, lib)
+
+
+def build_none() -> SplitPreconditioner:
+    return SplitPreconditioner(None, None, PrecondKind.NONE)
+
+
+class PreconditionedOperator(CsrOperator):
+    """Operator view of L^-1 A R^-1 (precond.hpp:57-74) on the device: every apply is the upper
+    solve, the SpMV and the lower solve; fingerprint combined as precond.cpp:203-210."""
+
+    def __init__(self, pc: SplitPreconditioner, a: CsrMatrix, ctx: Optional[Context] = None):
+        if a.n_rows != a.n_cols:
+            raise DimensionMismatch("precond operator: square required")
+        self.ctx = ctx if ctx is not None else default_context()
+        self.lib = self.ctx.lib
+        self.matrix = a
+        self.pc = pc
+        h = C.c_void_p()
+        if pc.kind == PrecondKind.NONE:
+            _check(self.lib, self.lib.dll.mstab_operator_create_csr(
+                self.ctx.h, a.n_rows, i64ptr(a.row_ptr), i64ptr(a.col_idx), dptr(a.values), C.byref(h)))
+        else:
+            L, R = pc.l_factor, pc.r_factor
+            _check(self.lib, self.lib.dll.mstab_operator_create_precond(
+                self.ctx.h, a.n_rows, i64ptr(a.row_ptr), i64ptr(a.col_idx), dptr(a.values), pc.kind,
+                i64ptr(L.row_ptr), i64ptr(L.col_idx), dptr(L.values), i64ptr(R.row_ptr), i64ptr(R.col_idx),
+                dptr(R.values), C.byref(h)))
+        self.h = h
+
+    def _solve(self, which: int, x) -> np.ndarray:
+        x = _f64(x)
+        if x.size != self.size():
+            raise DimensionMismatch("precond: dimension mismatch")
+        out = np.empty_like(x)
+        _check(self.lib, self.lib.dll.mstab_precond_solve(self.ctx.h, self.h, which, x.ctypes.data,
+                                                          out.ctypes.data, _capi.MEM_HOST))
+        return out
+
+    def lower_solve(self, b) -> np.ndarray:
+        """x = L^-1 b (precond.cpp:101-116)."""
+        return self._solve(0, b)
+
+    def upper_solve(self, b) -> np.ndarray:
+        """x = R^-1 b (precond.cpp:118-133)."""
+        return self._solve(1, b)
+
+
+def preconditioned_rhs(op: PreconditionedOperator, b) -> np.ndarray:
+    """L^-1 b (precond.cpp:181-184), on the device of the operator that holds the factors."""
+    return op.lower_solve(b)
+
+
+def unpreconditioned_solution(op: PreconditionedOperator, x_tilde) -> np.ndarray:
+    """R^-1 xt (precond.cpp:176-179)."""
+    return op.upper_solve(x_tilde)
 
 
 # ---- recycle data (recycle.hpp) ---------------------------------------------------------------

@@ -17,7 +17,8 @@
 //     from the C-ABI codes; breakdowns are a status with the reason string (:290-293);
 //   * SolveResult owns deep copies of x, the report (histories, per-cycle tau), final_data and
 //     the fetched snapshot (recycle.cpp:26-38).
-// B200 restrictions (no CPU fallback): the operator must be a CsrOperator and all data real
+// B200 restrictions (no CPU fallback): the operator must be a CsrOperator or a
+// PreconditionedOperator over one (split Jacobi / ILU(0), precond.hpp) and all data real
 // (imaginary parts exactly 0); anything else is rejected with ConfigError.
 #include <complex>
 #include <cstdint>
@@ -29,6 +30,7 @@
 #include "mstab/csr.hpp"
 #include "mstab/errors.hpp"
 #include "mstab/operator.hpp"
+#include "mstab/precond.hpp"
 #include "mstab/recycle.hpp"
 #include "mstab/solvers/idrstab.hpp"
 #include "mstab/solvers/report.hpp"
@@ -51,6 +53,7 @@ namespace {
     case MSTAB_E_SINGULAR: throw SingularProjection(msg);
     case MSTAB_E_RANK: throw RankDeficient(msg);
     case MSTAB_E_NOTREAL: throw ConfigError(msg);
+    case MSTAB_E_ZEROPIVOT: throw Error(msg);
     default: throw Error(msg);
   }
 }
@@ -92,12 +95,48 @@ std::vector<double> real_parts(std::span<const Complex> v, const char* what) {
   return out;
 }
 
-// Uploads the CSR matrix once per content (keyed by address, re-checked by the reference's own
-// fingerprint, csr.cpp:28-43, which the reference recomputes on every solve anyway).
+// PreconditionedOperator keeps its preconditioner and matrix private (precond.hpp:71-72) and has
+// no accessors. The shim reads them without touching the reference: an explicit instantiation
+// may name a private member ([temp.spec.general]/6), and the friend defined inside it hands the
+// member pointer out.
+template <typename Tag, typename Tag::type M>
+struct MemberOf {
+  friend typename Tag::type member(Tag) { return M; }
+};
+struct PcOf {
+  using type = const SplitPreconditioner* PreconditionedOperator::*;
+  friend type member(PcOf);
+};
+struct MatOf {
+  using type = const CsrMatrix* PreconditionedOperator::*;
+  friend type member(MatOf);
+};
+template struct MemberOf<PcOf, &PreconditionedOperator::pc_>;
+template struct MemberOf<MatOf, &PreconditionedOperator::a_>;
+
+struct Csr64 {
+  std::vector<int64_t> rp, ci;
+  std::vector<double> va;
+  Csr64(const CsrMatrix& m, const char* what)
+      : rp(m.row_ptr.begin(), m.row_ptr.end()), ci(m.col_idx.begin(), m.col_idx.end()), va(real_parts(m.values, what)) {}
+};
+
+// Uploads the operator once per content (keyed by address, re-checked by the reference's own
+// fingerprint, csr.cpp:28-43 / precond.cpp:203-210, which the reference recomputes on every
+// solve anyway). A PreconditionedOperator goes up with its factors: L^-1 A R^-1 on the device.
 mstab_operator* device_operator(Session& ss, const LinearOperator& a) {
-  const auto* csr = dynamic_cast<const CsrOperator*>(&a);
-  if (!csr) throw ConfigError("b200: only CsrOperator is supported on the device path");
-  const CsrMatrix& m = csr->matrix();
+  const CsrMatrix* mp = nullptr;
+  const SplitPreconditioner* pc = nullptr;
+  if (const auto* csr = dynamic_cast<const CsrOperator*>(&a)) {
+    mp = &csr->matrix();
+  } else if (const auto* pre = dynamic_cast<const PreconditionedOperator*>(&a)) {
+    mp = pre->*member(MatOf{});
+    pc = pre->*member(PcOf{});
+    if (pc->kind == PrecondKind::None) pc = nullptr;
+  } else {
+    throw ConfigError("b200: only CsrOperator and PreconditionedOperator are supported on the device path");
+  }
+  const CsrMatrix& m = *mp;
   const uint64_t fp = a.fingerprint();
   for (auto it = ss.ops.begin(); it != ss.ops.end(); ++it)
     if (it->m == &m && it->fp == fp && it->nnz == m.nnz()) {
@@ -106,11 +145,16 @@ mstab_operator* device_operator(Session& ss, const LinearOperator& a) {
     }
   if (!m.is_real()) throw ConfigError("b200: complex operator not supported (real fp64 path)");
   const int64_t n = (int64_t)m.n_rows;
-  std::vector<int64_t> rp(m.row_ptr.begin(), m.row_ptr.end());
-  std::vector<int64_t> ci(m.col_idx.begin(), m.col_idx.end());
-  std::vector<double> va = real_parts(m.values, "operator");
+  const Csr64 am(m, "operator");
   mstab_operator* op = nullptr;
-  check(mstab_operator_create_csr(ss.ctx, n, rp.data(), ci.data(), va.data(), &op));
+  if (pc) {
+    const Csr64 l(pc->l_factor, "preconditioner"), r(pc->r_factor, "preconditioner");
+    const int32_t kind = pc->kind == PrecondKind::Jacobi ? MSTAB_PRECOND_JACOBI : MSTAB_PRECOND_ILU0;
+    check(mstab_operator_create_precond(ss.ctx, n, am.rp.data(), am.ci.data(), am.va.data(), kind, l.rp.data(),
+                                        l.ci.data(), l.va.data(), r.rp.data(), r.ci.data(), r.va.data(), &op));
+  } else {
+    check(mstab_operator_create_csr(ss.ctx, n, am.rp.data(), am.ci.data(), am.va.data(), &op));
+  }
   ss.ops.push_front({&m, fp, m.nnz(), op});
   while (ss.ops.size() > 8) {
     mstab_operator_destroy(ss.ops.back().op);

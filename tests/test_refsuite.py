@@ -1,5 +1,5 @@
 """The reference's OWN GTest suites (proj/tests/test_solvers.cpp, test_recycle.cpp,
-test_harness.cpp), compiled unmodified by oracle/Makefile against a minimal GTest-compatible
+test_harness.cpp, test_precond.cpp), compiled unmodified by oracle/Makefile against a minimal GTest-compatible
 header (oracle/gtest_mini):
 
 * ref_<suite>  — linked with the reference library: pins gtest_mini (every assertion passes on the
@@ -17,7 +17,7 @@ import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
 SUITE_DIR = ROOT / "oracle" / "_ref" / "suite"
-SUITES = ["test_solvers", "test_recycle", "test_harness"]
+SUITES = ["test_solvers", "test_recycle", "test_harness", "test_precond"]
 
 
 def run_suite(path):
