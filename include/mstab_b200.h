@@ -45,6 +45,7 @@ extern "C" {
 #define MSTAB_E_SINGULAR (-8)      /* mstab::SingularProjection (only from the kernel helpers) */
 #define MSTAB_E_RANK (-9)          /* mstab::RankDeficient (only from the kernel helpers) */
 #define MSTAB_E_ZEROPIVOT (-10)    /* mstab::ZeroPivot (build_jacobi / build_ilu0, precond.cpp:33,56-82) */
+#define MSTAB_E_MISSING_OMEGAS (-11) /* mstab::MissingOmegas (sridr_solve, sridr.cpp:33-34) */
 #define MSTAB_E_CUDA (-20)         /* device/runtime failure (no reference counterpart) */
 #define MSTAB_E_NOTREAL (-21)      /* complex data rejected: this build is the real fp64 path */
 
@@ -212,6 +213,13 @@ int mstab_recycle_load(mstab_context* ctx, const char* path, mstab_recycle** out
 int mstab_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
                 int32_t mem, const mstab_solver_config* cfg, const mstab_recycle* recycle,
                 const mstab_fetch_policy* fetch, mstab_result** out);
+/* sridr_solve (include/mstab/solvers/sridr.hpp, src/sridr.cpp:23-118): SRIDR with ell = 1 on the
+ * recycle data's fixed block for its J recorded relaxations (one product per cycle), then IDR(s)
+ * cycles. The result holds x and the report (no final_data / fetched). Errors as sridr_solve:
+ * ConfigError (ell != 1, s mismatch), MissingOmegas, and validate's FingerprintMismatch/StaleData. */
+int mstab_sridr_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
+                      int32_t mem, const mstab_solver_config* cfg, const mstab_recycle* recycle,
+                      mstab_result** out);
 void mstab_result_destroy(mstab_result* res);
 int mstab_result_report(const mstab_result* res, mstab_report* out);
 /* SolveResult::x, copied into x (N values in `mem`). */

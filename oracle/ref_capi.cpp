@@ -17,6 +17,7 @@
 #include "mstab/recycle.hpp"
 #include "mstab/solvers/baselines.hpp"
 #include "mstab/solvers/idrstab.hpp"
+#include "mstab/solvers/sridr.hpp"
 #include "mstab_b200.h"
 #include "mstab_b200_kernels.h"
 
@@ -36,6 +37,7 @@ struct mstab_recycle {
 };
 struct mstab_result {
   mstab::SolveResult r;
+  bool sridr = false;  // sridr_solve returns x and the report only
 };
 
 namespace {
@@ -78,6 +80,9 @@ int guarded(F&& f) {
   } catch (const mstab::RankDeficient& e) {
     g_err = e.what();
     return MSTAB_E_RANK;
+  } catch (const mstab::MissingOmegas& e) {
+    g_err = e.what();
+    return MSTAB_E_MISSING_OMEGAS;
   } catch (const mstab::ZeroPivot& e) {
     g_err = e.what();
     return MSTAB_E_ZEROPIVOT;
@@ -356,6 +361,25 @@ int mstab_solve(mstab_context*, const mstab_operator* op, const double* b, const
   });
 }
 
+int mstab_sridr_solve(mstab_context*, const mstab_operator* op, const double* b, const double* x0, int32_t mem,
+                      const mstab_solver_config* cfg, const mstab_recycle* recycle, mstab_result** out) {
+  return guarded([&] {
+    host_only(mem);
+    if (!recycle) throw ConfigErr("sridr: recycle data required");
+    const int64_t n = (int64_t)op->m.n_rows;
+    mstab::SolverConfig sc{(size_t)cfg->s, (size_t)cfg->ell, cfg->tol, cfg->max_mv,
+                           cfg->true_residual_each_cycle != 0, cfg->seed};
+    mstab::Vector bv = to_vec(b, n);
+    mstab::Vector xv = x0 ? to_vec(x0, n) : mstab::Vector{};
+    auto [x, rep] = mstab::sridr_solve(*op->op, bv, xv, sc, *recycle->d);
+    auto r = std::make_unique<mstab_result>();
+    r->r.x = std::move(x);
+    r->r.report = std::move(rep);
+    r->sridr = true;
+    *out = r.release();
+  });
+}
+
 void mstab_result_destroy(mstab_result* res) { delete res; }
 
 int mstab_result_report(const mstab_result* res, mstab_report* out) {
@@ -410,7 +434,10 @@ int64_t mstab_result_taus(const mstab_result* res, double* re_im, int64_t cap) {
 }
 
 int mstab_result_final_data(const mstab_result* res, mstab_recycle** out) {
-  return guarded([&] { *out = new mstab_recycle{std::make_shared<mstab::RecycleData>(res->r.final_data)}; });
+  return guarded([&] {
+    if (res->sridr) throw mstab::Error("no final recycle data (sridr result)");
+    *out = new mstab_recycle{std::make_shared<mstab::RecycleData>(res->r.final_data)};
+  });
 }
 
 int mstab_result_fetched(const mstab_result* res, mstab_recycle** out) {
@@ -421,7 +448,10 @@ int mstab_result_fetched(const mstab_result* res, mstab_recycle** out) {
 }
 
 int mstab_result_handoff(const mstab_result* res, mstab_recycle** out) {
-  return guarded([&] { *out = new mstab_recycle{std::make_shared<mstab::RecycleData>(res->r.handoff())}; });
+  return guarded([&] {
+    if (res->sridr) throw mstab::Error("no recycle data (sridr result)");
+    *out = new mstab_recycle{std::make_shared<mstab::RecycleData>(res->r.handoff())};
+  });
 }
 
 // ---- kernel-level helpers -----------------------------------------------------------------

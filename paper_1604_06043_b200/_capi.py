@@ -100,6 +100,7 @@ ABI = [
     ("mstab_recycle_load", C.c_int, [_P, C.c_char_p, C.POINTER(_P)]),
     ("mstab_solve", C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(SolverConfigC), _P,
                               C.POINTER(FetchPolicyC), C.POINTER(_P)]),
+    ("mstab_sridr_solve", C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(SolverConfigC), _P, C.POINTER(_P)]),
     ("mstab_result_destroy", None, [_P]),
     ("mstab_result_report", C.c_int, [_P, C.POINTER(ReportC)]),
     ("mstab_result_x", C.c_int, [_P, _P, _P, C.c_int32]),

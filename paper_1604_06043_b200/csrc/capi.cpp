@@ -345,6 +345,18 @@ int mstab_solve(mstab_context* ctx, const mstab_operator* op, const double* b, c
   });
 }
 
+int mstab_sridr_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
+                      int32_t mem, const mstab_solver_config* cfg, const mstab_recycle* recycle,
+                      mstab_result** out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!recycle) throw Error(MSTAB_E_CONFIG, "sridr: recycle data required");
+    auto r = std::make_unique<mstab_result>();
+    r->impl = sridr(*ctx->impl, *op->impl, b, x0, mem, *cfg, *recycle->impl);
+    *out = r.release();
+  });
+}
+
 void mstab_result_destroy(mstab_result* res) { delete res; }
 
 int mstab_result_report(const mstab_result* res, mstab_report* out) {
@@ -382,6 +394,7 @@ int64_t mstab_result_taus(const mstab_result* res, double* re_im, int64_t cap) {
 
 int mstab_result_final_data(const mstab_result* res, mstab_recycle** out) {
   return guarded([&] {
+    if (!res->impl->final_data) throw Error(MSTAB_E_ERROR, "no final recycle data (sridr result)");
     auto h = std::make_unique<mstab_recycle>();
     h->impl = res->impl->final_data;
     *out = h.release();
@@ -399,6 +412,7 @@ int mstab_result_fetched(const mstab_result* res, mstab_recycle** out) {
 
 int mstab_result_handoff(const mstab_result* res, mstab_recycle** out) {
   return guarded([&] {
+    if (!res->impl->fetched && !res->impl->final_data) throw Error(MSTAB_E_ERROR, "no recycle data (sridr result)");
     auto h = std::make_unique<mstab_recycle>();
     h->impl = res->impl->fetched ? res->impl->fetched : res->impl->final_data;
     *out = h.release();

@@ -7,6 +7,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 
 #include "device_state.h"
 
@@ -166,7 +167,10 @@ void launch_ls_pass2(cudaStream_t st, int64_t n, int ell, int s, bool chol, cons
 // per row: 133 us at c2 against 35 us); small systems keep the Givens TSQR, whose rounding the
 // reference's own 1e-12 trajectory tests were calibrated against.
 constexpr int64_t kCholQrMinRows = 1 << 17;
-inline bool ls_use_cholqr(int64_t n_global) { return n_global >= kCholQrMinRows; }
+inline bool ls_use_cholqr(int64_t n_global) {
+  static const bool givens_only = std::getenv("MSTAB_LS_GIVENS") != nullptr;  // diagnostics
+  return !givens_only && n_global >= kCholQrMinRows;
+}
 void launch_fin_ls1(cudaStream_t st, int ell, DevState* ds);
 void launch_ls(cudaStream_t st, int64_t n, int64_t ld, int ell, int s, const double* const* r,
                const Reducer& red);
@@ -200,6 +204,15 @@ void launch_tri_solve(cudaStream_t st, const DevTri& f, const double* b, double*
 // y = w (b == nullptr) or y = b - w, with the P^H y (+ ||y||^2) reduction and finalize_spmv(fin).
 void launch_ph_fin(cudaStream_t st, int64_t n, int64_t ld, int s, const double* w, double* y, const double* p,
                    const double* b, const FinParams& fin, const Reducer& red);
+
+// ---- SRIDR recycled phase (ksridr.cu, sridr.cpp:57-81) ------------------------------------
+// rt = r - V gamma, xt = x + U gamma (gamma = ds->gamma[0..s))
+void launch_sridr_corr(cudaStream_t st, int64_t n, int64_t ld, int s, const double* r, const double* x,
+                       const double* u, const double* v, double* rt, double* xt, const DevState* ds);
+// r = rt - omega art, x = xt + omega rt, then P^H r, ||r||^2 and finalize_spmv(fin)
+void launch_sridr_update(cudaStream_t st, int64_t n, int64_t ld, int s, double omega, const double* rt,
+                         const double* art, const double* xt, double* r, double* x, const double* p,
+                         const FinParams& fin, const Reducer& red);
 
 // au: the products A U precomputed by the caller (preconditioned operators), else nullptr and
 // the kernel forms them from the CSR.

@@ -1115,4 +1115,142 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   return res;
 }
 
+// sridr_solve (sridr.cpp:23-118): the recycled phase replays the donor's J relaxations with V
+// fixed (one product per cycle, ksridr.cu), then standard IDR(s) cycles (ell = 1) seeded with the
+// recycled block, on the same captured cycle graphs as idrstab_solve.
+std::unique_ptr<SolveResultImpl> sridr(Context& ctx, const Operator& op, const double* b_in, const double* x0_in,
+                                       int mem, const mstab_solver_config& cfg, const Recycle& rc) {
+  if (cfg.s < 1) throw Error(MSTAB_E_CONFIG, "config: s >= 1 required");
+  if (cfg.ell < 1) throw Error(MSTAB_E_CONFIG, "config: ell >= 1 required");
+  if (!(cfg.tol > 0.0)) throw Error(MSTAB_E_CONFIG, "config: tol > 0 required");
+  if (cfg.max_mv < cfg.s + 1) throw Error(MSTAB_E_CONFIG, "config: max_mv >= s + 1 required");
+  if (cfg.ell != 1) throw Error(MSTAB_E_CONFIG, "sridr: ell == 1 required");
+  if (cfg.s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: s <= 16 is supported");
+  const int s = (int)cfg.s;
+  const int64_t n = op.n, ld = ctx.ld(n);
+  cudaStream_t st = ctx.stream();
+  const bool tres = cfg.true_residual_each_cycle != 0;
+  validate(ctx, rc, op);
+  if (rc.s != cfg.s) throw Error(MSTAB_E_CONFIG, "sridr: recycle s != config s");
+  const int64_t J = rc.level_j;
+  if ((int64_t)rc.omega.size() != J)
+    throw Error(MSTAB_E_MISSING_OMEGAS, "sridr: recycle data lacks the relaxation history");
+  for (const auto& w : rc.omega)
+    if (w.imag() != 0.0) throw Error(MSTAB_E_NOTREAL, "sridr: complex relaxation history (real fp64 path)");
+  Workspace& w = workspace(ctx, op, s, 1, tres);
+  reset_status(ctx);
+  const auto t0 = Clock::now();
+  auto res = std::make_unique<SolveResultImpl>();
+  res->n = n;
+  mstab_report& rep = res->report;
+  std::memset(&rep, 0, sizeof(rep));
+  rep.ell = 1;
+  rep.h_mv_aux += s;  // validation applies A to U
+
+  CUDA_OK(cudaMemcpyAsync(w.b->d(), b_in, sizeof(double) * n,
+                          mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  launch_vec_stats(st, n, w.b->d(), scal(ctx, 0), ctx.reducer());
+  check_launch();
+  rep.bnorm = std::sqrt(read_scal(ctx, 3)[0]);
+  WSet& c0 = w.set[0];
+  bool x_zero = true;
+  if (x0_in) {
+    CUDA_OK(cudaMemcpyAsync(c0.x->d(), x0_in, sizeof(double) * n,
+                            mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    launch_vec_stats(st, n, c0.x->d(), scal(ctx, 0), ctx.reducer());
+    check_launch();
+    x_zero = read_scal(ctx, 3)[2] == 0.0;
+  } else {
+    CUDA_OK(cudaMemsetAsync(c0.x->ptr, 0, sizeof(double) * ld, st));
+  }
+  CUDA_OK(cudaMemcpyAsync(c0.r->d(), w.b->d(), sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  if (!x_zero) {  // r = b - A x (sridr.cpp:44-48)
+    spmv_dev(ctx, op, c0.x->d(), c0.r->d());
+    launch_rsub(st, n, w.b->d(), c0.r->d());
+    check_launch();
+    rep.h_mv_aux++;
+  }
+  if (w.p_src != rc.p->ptr) {
+    CUDA_OK(cudaMemcpyAsync(w.P->ptr, rc.p->ptr, sizeof(double) * ld * s, cudaMemcpyDeviceToDevice, st));
+    w.p_src = rc.p->ptr;
+  }
+  const double* P = w.P->d();
+  // P^H V (kept in ds->Ma for the whole recycled phase), P^H r, ||r||, gamma = (P^H V)^-1 P^H r
+  reset_status(ctx);
+  launch_prologue(st, n, ld, s, P, rc.v->d(), c0.r->d(), ctx.reducer());
+  check_launch();
+  CycleStatus cs = read_status(ctx);
+  double resnorm = cs.resnorm;
+  res->history.push_back({0, rep.h_mv + rep.h_mv_aux, 0, resnorm, ns_since(t0)});
+  const double threshold = cfg.tol * rep.bnorm;
+  int64_t j = 0;
+  bool broke = false;
+  auto breakdown = [&](const char* why) {
+    rep.status = MSTAB_STATUS_BREAKDOWN;
+    std::snprintf(rep.breakdown_reason, sizeof(rep.breakdown_reason), "%s", why);
+    broke = true;
+  };
+  if (J > 0 && cs.pending_singular) breakdown("sridr: projection block P^H V is singular");
+  // recycled phase: rt, xt in the idle ping-pong set, A rt in R[1]
+  double* rt = w.set[1].r->d();
+  double* xt = w.set[1].x->d();
+  double* art = w.R[1]->d();
+  while (!broke && j < J && resnorm > threshold && rep.h_mv < cfg.max_mv) {
+    launch_sridr_corr(st, n, ld, s, c0.r->d(), c0.x->d(), rc.u->d(), rc.v->d(), rt, xt, ctx.ds());
+    check_launch();
+    spmv_dev(ctx, op, rt, art);
+    FinParams f;
+    f.op = kFinTrueRes;  // ||r||, P^H r and the next gamma from the fixed P^H V
+    f.s = s;
+    launch_sridr_update(st, n, ld, s, rc.omega[(size_t)j].real(), rt, art, xt, c0.r->d(), c0.x->d(), P, f,
+                        ctx.reducer());
+    check_launch();
+    rep.h_mv++;
+    ++j;
+    rep.cycles = j;
+    rep.h_rd = j * s;
+    cs = read_status(ctx);
+    resnorm = cs.resnorm;
+    res->history.push_back({j, rep.h_mv + rep.h_mv_aux, j, resnorm, ns_since(t0)});
+  }
+  // standard IDR(s) cycles seeded with the recycled block (sridr.cpp:86-108)
+  int p = 0;
+  if (!broke && resnorm > threshold && rep.h_mv < cfg.max_mv) {
+    CUDA_OK(cudaMemcpyAsync(c0.U->ptr, rc.u->ptr, sizeof(double) * ld * s, cudaMemcpyDeviceToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(c0.V->ptr, rc.v->ptr, sizeof(double) * ld * s, cudaMemcpyDeviceToDevice, st));
+    reset_status(ctx);
+    launch_prologue(st, n, ld, s, P, c0.V->d(), c0.r->d(), ctx.reducer());
+    check_launch();
+    read_status(ctx);
+    while (resnorm > threshold && rep.h_mv < cfg.max_mv) {
+      run_cycle(ctx, op, w, p);
+      const CycleStatus& ccs = read_status(ctx);
+      if (w.graph[p].profiled) prof_accumulate(w.graph[p].prof);
+      if (ccs.breakdown) {
+        rep.h_mv += ccs.mv_at_breakdown;
+        breakdown(ccs.breakdown == kBreakRank ? "least_squares_tall: stabilization block lost rank"
+                                              : "solve_small: pivot collapse");
+        break;
+      }
+      p = 1 - p;
+      ++j;
+      rep.cycles = j;
+      rep.h_mv += s + 1;
+      rep.h_rd = j * s;
+      res->taus.push_back(ccs.tau[0]);
+      if (tres) rep.h_mv_aux++;
+      resnorm = ccs.resnorm;
+      res->history.push_back({j, rep.h_mv + rep.h_mv_aux, j, resnorm, ns_since(t0)});
+    }
+  }
+  if (!broke) rep.status = resnorm <= threshold ? MSTAB_STATUS_CONVERGED : MSTAB_STATUS_MAXMV;
+  rep.final_resnorm = resnorm;
+  res->x = copy_vec(ctx, w.set[p].x, n);
+  rep.history_len = (int64_t)res->history.size();
+  rep.tau_len = (int64_t)res->taus.size();
+  ctx.sync();
+  rep.wall_ns_total = ns_since(t0);
+  return res;
+}
+
 }  // namespace mstab_b200

@@ -178,6 +178,10 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
                                        const double* x0, int mem, const mstab_solver_config& cfg,
                                        const Recycle* recycle, const mstab_fetch_policy* fetch);
 
+// sridr_solve (sridr.cpp:23-118) on the device; the result carries x and the report only.
+std::unique_ptr<SolveResultImpl> sridr(Context& ctx, const Operator& op, const double* b, const double* x0, int mem,
+                                       const mstab_solver_config& cfg, const Recycle& recycle);
+
 // validate (recycle.cpp:40-83). Throws Error with the reference's class code.
 mstab_validation_report validate(Context& ctx, const Recycle& rd, const Operator& op);
 

@@ -73,9 +73,13 @@ class ZeroPivot(Error):
     """errors.hpp:39-45 (build_jacobi / build_ilu0)."""
 
 
+class MissingOmegas(Error):
+    """errors.hpp:56-58 (sridr_solve without the donor's relaxation history)."""
+
+
 _ERR = {-1: Error, -2: DimensionMismatch, -3: ConfigError, -4: FingerprintMismatch, -5: StaleData,
         -6: ParseError, -7: IoError, -8: SingularProjection, -9: RankDeficient, -20: CudaError,
-        -21: NotReal, -10: ZeroPivot}
+        -21: NotReal, -10: ZeroPivot, -11: MissingOmegas}
 
 
 def _check(lib: Lib, rc: int):
@@ -701,6 +705,26 @@ def mstab_solve(a: CsrOperator, b, x0, cfg: SolverConfig, recycle: RecycleData,
                 fetch_policy: Optional[FetchPolicy] = None) -> SolveResult:
     """M(s,ell)stab: idrstab_solve with mandatory recycle data (idrstab.hpp:94-96)."""
     return idrstab_solve(a, b, x0, cfg, recycle, fetch_policy)
+
+
+def sridr_solve(a: CsrOperator, b, x0, cfg: SolverConfig, recycle: RecycleData):
+    """SRIDR (sridr.hpp, sridr.cpp:23-118): returns (x, report) like the reference's pair."""
+    ctx, lib = a.ctx, a.lib
+    n = a.size()
+    b = _f64(b)
+    if b.size != n:
+        raise DimensionMismatch("sridr: rhs size")
+    xptr = None
+    if x0 is not None and len(x0) > 0:
+        x0 = _f64(x0)
+        xptr = x0.ctypes.data
+    c = cfg._c()
+    h = C.c_void_p()
+    _check(lib, lib.dll.mstab_sridr_solve(ctx.h, a.h, b.ctypes.data, xptr, _capi.MEM_HOST, C.byref(c), recycle.h,
+                                          C.byref(h)))
+    res = SolveResult(ctx, h)
+    res.n = n
+    return res.x, res.report
 
 
 # ---- kernel-level helpers (include/mstab_b200_kernels.h) --------------------------------------

@@ -34,6 +34,7 @@
 #include "mstab/recycle.hpp"
 #include "mstab/solvers/idrstab.hpp"
 #include "mstab/solvers/report.hpp"
+#include "mstab/solvers/sridr.hpp"
 #include "mstab/types.hpp"
 #include "mstab_b200.h"
 
@@ -54,6 +55,7 @@ namespace {
     case MSTAB_E_RANK: throw RankDeficient(msg);
     case MSTAB_E_NOTREAL: throw ConfigError(msg);
     case MSTAB_E_ZEROPIVOT: throw Error(msg);
+    case MSTAB_E_MISSING_OMEGAS: throw MissingOmegas(msg);
     default: throw Error(msg);
   }
 }
@@ -210,53 +212,14 @@ RecycleData download_recycle(Session& ss, mstab_recycle* h) {
   return rd;
 }
 
-}  // namespace
-
-SolveResult idrstab_solve(const LinearOperator& a, const Vector& b, const Vector& x0,
-                          const SolverConfig& cfg, const RecycleData* recycle,
-                          const FetchPolicy* fetch_policy) {
-  cfg.validate();
-  const std::size_t n = a.size();
-  if (b.size() != n) throw DimensionMismatch("idrstab: rhs size");
-  if (!x0.empty() && x0.size() != n) throw DimensionMismatch("idrstab: guess size");
-  ensure_finite(b, "idrstab rhs");
-  if (!x0.empty()) ensure_finite(x0, "idrstab guess");
-
-  Session& ss = session();
-  mstab_operator* op = device_operator(ss, a);
-  const std::vector<double> bh = real_parts(b, "rhs");
-  const std::vector<double> xh = real_parts(x0, "guess");
-  RecycleHandle rh;
-  if (recycle) upload_recycle(ss, *recycle, rh);
-
-  mstab_solver_config c{};
-  c.s = (int64_t)cfg.s;
-  c.ell = (int64_t)cfg.ell;
-  c.tol = cfg.tol;
-  c.max_mv = cfg.max_mv;
-  c.true_residual_each_cycle = cfg.true_residual_each_cycle ? 1 : 0;
-  c.seed = cfg.seed;
-  mstab_fetch_policy fp{};
-  if (fetch_policy) {
-    fp.kind = fetch_policy->kind == FetchPolicy::Kind::AtCycle          ? MSTAB_FETCH_AT_CYCLE
-              : fetch_policy->kind == FetchPolicy::Kind::AtHalfTolerance ? MSTAB_FETCH_AT_HALF_TOLERANCE
-                                                                         : MSTAB_FETCH_MANUAL;
-    fp.cycle = (int64_t)fetch_policy->cycle;
-  }
-  mstab_result* res = nullptr;
-  check(::mstab_solve(ss.ctx, op, bh.data(), x0.empty() ? nullptr : xh.data(), MSTAB_MEM_HOST, &c, rh.h,
-                    fetch_policy ? &fp : nullptr, &res));
-  std::unique_ptr<mstab_result, void (*)(mstab_result*)> guard(res, mstab_result_destroy);
-
-  SolveResult out;
+// SolveResult::x and SolveReport (histories, per-cycle tau) from a C-ABI result.
+void read_result(Session& ss, mstab_result* res, size_t n, size_t cfg_ell, Vector& x_out, SolveReport& rep) {
   mstab_report r{};
   check(mstab_result_report(res, &r));
   std::vector<double> x(n);
   check(mstab_result_x(ss.ctx, res, x.data(), MSTAB_MEM_HOST));
-  out.x.resize(n);
-  for (size_t i = 0; i < n; ++i) out.x[i] = Complex(x[i]);
-
-  SolveReport& rep = out.report;
+  x_out.resize(n);
+  for (size_t i = 0; i < n; ++i) x_out[i] = Complex(x[i]);
   rep.h_mv = r.h_mv;
   rep.h_mv_aux = r.h_mv_aux;
   rep.h_rd = r.h_rd;
@@ -276,12 +239,61 @@ SolveResult idrstab_solve(const LinearOperator& a, const Vector& b, const Vector
   std::vector<double> taus(2 * (size_t)r.tau_len);
   if (r.tau_len > 0 && mstab_result_taus(res, taus.data(), r.tau_len) != r.tau_len)
     throw Error("b200: tau read failed");
-  const int64_t ell = r.ell > 0 ? r.ell : (int64_t)cfg.ell;
+  const int64_t ell = r.ell > 0 ? r.ell : (int64_t)cfg_ell;
   for (int64_t c0 = 0; c0 + ell <= r.tau_len; c0 += ell) {
     std::vector<Complex> t;
     for (int64_t j = 0; j < ell; ++j) t.emplace_back(taus[2 * (c0 + j)], taus[2 * (c0 + j) + 1]);
     rep.omega_history.push_back(std::move(t));
   }
+}
+
+mstab_solver_config to_c(const SolverConfig& cfg) {
+  mstab_solver_config c{};
+  c.s = (int64_t)cfg.s;
+  c.ell = (int64_t)cfg.ell;
+  c.tol = cfg.tol;
+  c.max_mv = cfg.max_mv;
+  c.true_residual_each_cycle = cfg.true_residual_each_cycle ? 1 : 0;
+  c.seed = cfg.seed;
+  return c;
+}
+
+}  // namespace
+
+SolveResult idrstab_solve(const LinearOperator& a, const Vector& b, const Vector& x0,
+                          const SolverConfig& cfg, const RecycleData* recycle,
+                          const FetchPolicy* fetch_policy) {
+  cfg.validate();
+  const std::size_t n = a.size();
+  if (b.size() != n) throw DimensionMismatch("idrstab: rhs size");
+  if (!x0.empty() && x0.size() != n) throw DimensionMismatch("idrstab: guess size");
+  ensure_finite(b, "idrstab rhs");
+  if (!x0.empty()) ensure_finite(x0, "idrstab guess");
+
+  Session& ss = session();
+  mstab_operator* op = device_operator(ss, a);
+  const std::vector<double> bh = real_parts(b, "rhs");
+  const std::vector<double> xh = real_parts(x0, "guess");
+  RecycleHandle rh;
+  if (recycle) upload_recycle(ss, *recycle, rh);
+
+  mstab_solver_config c = to_c(cfg);
+  mstab_fetch_policy fp{};
+  if (fetch_policy) {
+    fp.kind = fetch_policy->kind == FetchPolicy::Kind::AtCycle          ? MSTAB_FETCH_AT_CYCLE
+              : fetch_policy->kind == FetchPolicy::Kind::AtHalfTolerance ? MSTAB_FETCH_AT_HALF_TOLERANCE
+                                                                         : MSTAB_FETCH_MANUAL;
+    fp.cycle = (int64_t)fetch_policy->cycle;
+  }
+  mstab_result* res = nullptr;
+  check(::mstab_solve(ss.ctx, op, bh.data(), x0.empty() ? nullptr : xh.data(), MSTAB_MEM_HOST, &c, rh.h,
+                    fetch_policy ? &fp : nullptr, &res));
+  std::unique_ptr<mstab_result, void (*)(mstab_result*)> guard(res, mstab_result_destroy);
+
+  SolveResult out;
+  read_result(ss, res, n, cfg.ell, out.x, out.report);
+  mstab_report r{};
+  check(mstab_result_report(res, &r));
 
   RecycleHandle fin;
   check(mstab_result_final_data(res, &fin.h));
@@ -298,6 +310,30 @@ SolveResult mstab_solve(const LinearOperator& a, const Vector& b, const Vector& 
                         const SolverConfig& cfg, const RecycleData& recycle,
                         const FetchPolicy* fetch_policy) {
   return idrstab_solve(a, b, x0, cfg, &recycle, fetch_policy);
+}
+
+// sridr_solve (sridr.hpp, sridr.cpp:23-118) on the device: the recycled phase and the IDR(s)
+// cycles both run on the B200 (ksridr.cu + the cycle graphs).
+std::pair<Vector, SolveReport> sridr_solve(const LinearOperator& a, const Vector& b, const Vector& x0,
+                                           const SolverConfig& cfg, const RecycleData& recycle) {
+  cfg.validate();
+  if (cfg.ell != 1) throw ConfigError("sridr: ell == 1 required");
+  const std::size_t n = a.size();
+  if (b.size() != n) throw DimensionMismatch("sridr: rhs size");
+  Session& ss = session();
+  mstab_operator* op = device_operator(ss, a);
+  const std::vector<double> bh = real_parts(b, "rhs");
+  const std::vector<double> xh = real_parts(x0, "guess");
+  RecycleHandle rh;
+  upload_recycle(ss, recycle, rh);
+  const mstab_solver_config c = to_c(cfg);
+  mstab_result* res = nullptr;
+  check(::mstab_sridr_solve(ss.ctx, op, bh.data(), x0.empty() ? nullptr : xh.data(), MSTAB_MEM_HOST, &c, rh.h,
+                            &res));
+  std::unique_ptr<mstab_result, void (*)(mstab_result*)> guard(res, mstab_result_destroy);
+  std::pair<Vector, SolveReport> out;
+  read_result(ss, res, n, 1, out.first, out.second);
+  return out;
 }
 
 }  // namespace mstab

@@ -291,3 +291,61 @@ def test_golden_sequences_teacher_forced(gpu_ctx, golden_seq, key):
         tr_ref = np.linalg.norm(true_res(op, b, xr)) / np.linalg.norm(b)
         tr = np.linalg.norm(true_res(op, b, r.x)) / np.linalg.norm(b)
         assert tr <= max(1e-8, 1.5 * tr_ref)
+
+
+# ---- Sridr.* (test_solvers.cpp:411-459) and parity with the reference's sridr_solve ---------------
+def _sridr_donor(ctx, n, s, fetch_cycle, seed):
+    op = m.CsrOperator(tri(n), ctx)
+    donor = m.idrstab_solve(op, np.ones(n), None, m.SolverConfig(s, 1, 1e-8, 100000, False, seed), None,
+                            m.FetchPolicy.at_cycle(fetch_cycle))
+    return op, donor
+
+
+def test_sridr_recycled_phase_costs_one_product_per_cycle(gpu_ctx):
+    op, donor = _sridr_donor(gpu_ctx, 24, 2, 8, 9)
+    f = donor.fetched
+    assert len(f.omega_history) == 8
+    x, rep = m.sridr_solve(op, pb.sinewave(24), None, m.SolverConfig(2, 1, 1e-30, 8, False, 9), f)
+    assert rep.cycles == 8 and rep.h_mv == 8 and rep.h_rd == 16
+
+
+def test_sridr_missing_omegas_rejected(gpu_ctx):
+    op = m.CsrOperator(tri(16), gpu_ctx)
+    p = m.make_cut_space(16, 2, 15, gpu_ctx)
+    u, v, _ = m.arnoldi_init(op, np.ones(16), 2, 15)
+    data = m.fetch(p, u, v, [], 3, op.fingerprint(), gpu_ctx)
+    with pytest.raises(m.MissingOmegas):
+        m.sridr_solve(op, np.ones(16), None, m.SolverConfig(2, 1, 1e-8, 1000, False, 15), data)
+    with pytest.raises(m.ConfigError):
+        m.sridr_solve(op, np.ones(16), None, m.SolverConfig(2, 2, 1e-8, 1000, False, 15), data)
+
+
+@pytest.mark.parametrize("s,fetch_cycle", [(2, 8), (4, 5), (4, 3), (8, 2)])
+def test_sridr_matches_reference(s, fetch_cycle, gpu_ctx, ref_ctx):
+    """Teacher-forced: both implementations run SRIDR on the reference donor's hand-off."""
+    a = pb.convdiff(2, 48, 5, (100.0, 100.0, 0.0), 1e-2)
+    cfg = pb.config("c1", grid=48)
+    x0, f = cfg.sources()
+    b1 = cfg.first_rhs(x0, f)
+    rop = m.CsrOperator(a, ref_ctx)
+    donor = m.idrstab_solve(rop, b1, None, m.SolverConfig(s, 1, 1e-8, 100000, False, 0), None,
+                            m.FetchPolicy.at_cycle(fetch_cycle))
+    h = donor.fetched
+    b2 = cfg.next_rhs(1, donor.x, f)
+    sc = m.SolverConfig(s, 1, 1e-8, 100000, True, 0)
+    xr, rr = m.sridr_solve(rop, b2, None, sc, h)
+    gop = m.CsrOperator(a, gpu_ctx)
+    hg = m.fetch(h.p, h.u, h.v, h.omega_history, h.level_J, h.matrix_fingerprint, gpu_ctx)
+    xg, rg = m.sridr_solve(gop, b2, None, sc, hg)
+    assert rg.status == rr.status  # both converge, or both break down (then with the same reason)
+    assert abs(rg.cycles - rr.cycles) <= 2
+    assert rg.h_mv_aux == rr.h_mv_aux
+    # the recycled phase is deterministic element-wise: its residual history agrees closely
+    J = min(h.level_J, rr.cycles, rg.cycles)
+    for i in range(J + 1):
+        a_, b_ = rg.residual_history[i].resnorm, rr.residual_history[i].resnorm
+        assert abs(a_ - b_) <= 1e-9 * max(1.0, b_), (i, a_, b_)
+    if rr.status == m.CONVERGED:
+        assert np.linalg.norm(xg - xr) <= 1e-6 * np.linalg.norm(xr)
+    else:
+        assert rg.breakdown_reason.split(":")[0] == rr.breakdown_reason.split(":")[0]
