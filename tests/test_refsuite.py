@@ -5,7 +5,7 @@ header (oracle/gtest_mini):
 * ref_<suite>  — linked with the reference library: pins gtest_mini (every assertion passes on the
   code the suites were written for);
 * b200_<suite> — linked with the C++ drop-in shim (paper_1604_06043_b200/shim/idrstab_b200.cpp):
-  every mstab::idrstab_solve / mstab::mstab_solve the suites make, directly or through
+  every mstab::idrstab_solve / mstab_solve / sridr_solve the suites make, directly or through
   run_sequence (harness.cpp), runs on the B200 through libmstab_b200.so.
 
 The binaries are built in the container that has /root/reference (build() / `make ref`) and travel
