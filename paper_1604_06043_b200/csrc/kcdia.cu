@@ -28,8 +28,13 @@ struct MaskOf {
                                       typename std::conditional<(ND <= 16), uint16_t, uint32_t>::type>::type;
 };
 
+// 512-thread CTAs, two per SM: the same 32 warps per SM as 4 x 256, but half the per-CTA partials,
+// so the last CTA sums each reduced value with one batch of loads per lane (the tail of every
+// SpMV sits on the critical path of the column loop).
+constexpr int kCdiaBlock = 512;
+
 template <int S, bool TRUE_RES, int ND>
-__global__ void __launch_bounds__(kBlock, S <= 8 ? 4 : 2)
+__global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
     k_spmv_cdia(DevCsr a, const double* __restrict__ x, double* __restrict__ y,
                 const double* __restrict__ p, int64_t ld, const double* __restrict__ b,
                 FinParams fin, Reducer red) {
@@ -51,22 +56,14 @@ __global__ void __launch_bounds__(kBlock, S <= 8 ? 4 : 2)
                               : __ldg(static_cast<const uint32_t*>(a.dia_mask) + r));
   };
   const int32_t rstride = gridDim.x * blockDim.x;
-  // The first row's mask and P values are loaded BEFORE pdl_wait: both are fixed for the whole
-  // sequence (nothing in the cycle writes them), so they overlap the predecessor's drain; x,
-  // which the predecessor writes, is read only after the wait.
-  const int32_t row0 = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t mnext = load_mask(row0);
-  double pv[S];
-#pragma unroll
-  for (int c = 0; c < S; ++c) pv[c] = row0 < (int32_t)n ? __ldg(p + c * ld + row0) : 0.0;
   pdl_wait();
-  for (int32_t row = row0; row < (int32_t)n; row += rstride) {
+  uint32_t mnext = load_mask(blockIdx.x * blockDim.x + threadIdx.x);
+  for (int32_t row = blockIdx.x * blockDim.x + threadIdx.x; row < (int32_t)n; row += rstride) {
     const uint32_t m = mnext;
     mnext = load_mask(row + rstride);
-    if (row != row0) {
+    double pv[S];
 #pragma unroll
-      for (int c = 0; c < S; ++c) pv[c] = __ldg(p + c * ld + row);
-    }
+    for (int c = 0; c < S; ++c) pv[c] = __ldg(p + c * ld + row);
     const double bv = TRUE_RES ? __ldg(b + row) : 0.0;
     double acc = 0.0;
     if (ND > 0) {
@@ -95,7 +92,7 @@ __global__ void __launch_bounds__(kBlock, S <= 8 ? 4 : 2)
     if (TRUE_RES) part[S] = part[S] + acc * acc;
   }
   pdl_trigger();
-  __shared__ double scratch[NS * 32];
+  __shared__ double scratch[NS * 32];  // block_totals: up to 32 warps
   __shared__ double blk[NS];
   __shared__ double redv[NS];
   __shared__ FinStage fs;
@@ -109,7 +106,7 @@ template <int S, bool TRUE_RES, int ND>
 void launch_cdia_nd(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
                     int64_t ld, const double* b, const FinParams& fin, const Reducer& red) {
   auto kfn = k_spmv_cdia<S, TRUE_RES, ND>;
-  launch_pdl(kfn, occupancy_grid(kfn, a.n, 0), kBlock, 0, st, a, x, y, p, ld, b, fin, red);
+  launch_pdl(kfn, occupancy_grid(kfn, a.n, 0, kCdiaBlock), kCdiaBlock, 0, st, a, x, y, p, ld, b, fin, red);
 }
 
 // Specialised stencil widths: 5 (2-D 5-point: c1), 7 (3-D 7-point: c2, c5), 27 (27-point: c4).

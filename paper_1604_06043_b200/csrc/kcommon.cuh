@@ -446,7 +446,7 @@ __device__ void finalize_spmv(const FinParams& f, const double* red, DevState* d
 // call, which would starve the GPU between launches).
 
 template <typename K>
-int occupancy_grid(K kernel, int64_t n, size_t dyn_smem) {
+int occupancy_grid(K kernel, int64_t n, size_t dyn_smem, int block = kBlock) {
   int per_sm = 0;
   {
     std::lock_guard<std::mutex> lk(g_occ_mu);
@@ -454,12 +454,12 @@ int occupancy_grid(K kernel, int64_t n, size_t dyn_smem) {
     if (it != g_occ.end()) {
       per_sm = it->second;
     } else {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, dyn_smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, dyn_smem);
       if (per_sm < 1) per_sm = 1;
       g_occ[reinterpret_cast<const void*>(kernel)] = per_sm;
     }
   }
-  int64_t want = (n + kBlock - 1) / kBlock;
+  int64_t want = (n + block - 1) / block;
   int64_t cap = (int64_t)g_num_sms * per_sm;
   if (cap > kMaxGrid) cap = kMaxGrid;
   if (want > cap) want = cap;

@@ -57,20 +57,57 @@ __global__ void __launch_bounds__(kBlock) k_level_update(int64_t n, int64_t ld, 
 }
 
 // step (c), top level, column q (idrstab.cpp:140-148 at i = k)
+// With `early`, each thread's first row pair of operands is copied into shared memory with
+// cp.async BEFORE pdl_wait, while the predecessor (the SpMV of column q-1, or step (b) for q = 0)
+// is still in its reduction + LU tail. Everything but the predecessor's own output (r^(k+1) for
+// q = 0, V^(k+1)_{q-1} for q > 0) was written by earlier kernels and is final; those and eta are
+// read after the wait. The copies bypass registers, so the streaming loop keeps its occupancy.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int S>
 __global__ void __launch_bounds__(kBlock) k_rebuild_top(int64_t n, int64_t ld, int q,
                                                         const double* __restrict__ rnext,
                                                         const double* __restrict__ vk_in,
                                                         double* __restrict__ vk_out,
                                                         const double* __restrict__ vk1,
-                                                        DevState* ds) {
+                                                        DevState* ds, int early) {
+  extern __shared__ __align__(16) double2 pre[];  // [S + 1][blockDim]: columns 0..S-1, then r^(k+1)
+  const int64_t npair = (n + 1) >> 1;
+  const int64_t pr0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool first = early && pr0 < npair && 2 * pr0 + 1 < n;
+  const int t = threadIdx.x, bd = blockDim.x;
+  if (first) {
+    const int64_t row = 2 * pr0;
+    if (q > 0) cp_async16(&pre[S * bd + t], rnext + row);
+#pragma unroll
+    for (int c = 0; c < S; ++c)
+      if (c != q - 1) cp_async16(&pre[c * bd + t], ((c < q) ? vk1 : vk_in) + c * ld + row);
+  }
   pdl_wait();
   double et[S];
 #pragma unroll
   for (int c = 0; c < S; ++c) et[c] = ds->eta[q * S + c];
-  const int64_t npair = (n + 1) >> 1;
-  for (int64_t pr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pr < npair;
-       pr += (int64_t)gridDim.x * blockDim.x) {
+  if (first) {
+    const int64_t row = 2 * pr0;
+    const double2 late = *reinterpret_cast<const double2*>(q == 0 ? rnext + row : vk1 + (q - 1) * ld + row);
+    cp_async_wait_all();
+    const double2 rn = q == 0 ? late : pre[S * bd + t];
+    double n0 = rn.x, n1 = rn.y;
+#pragma unroll
+    for (int c = 0; c < S; ++c) {
+      const double2 m = (c == q - 1) ? late : pre[c * bd + t];
+      n0 = n0 + (-et[c]) * m.x;
+      n1 = n1 + (-et[c]) * m.y;
+    }
+    *reinterpret_cast<double2*>(vk_out + q * ld + row) = make_double2(n0, n1);
+  }
+  for (int64_t pr = first ? pr0 + stride : pr0; pr < npair; pr += stride) {
     const int64_t row = 2 * pr;
     if (row + 1 < n) {
       const double2 rn = *reinterpret_cast<const double2*>(rnext + row);
@@ -174,10 +211,17 @@ void launch_level_update(cudaStream_t st, int64_t n, int64_t ld, int s, int k, c
 void launch_rebuild_top(cudaStream_t st, int64_t n, int64_t ld, int s, int q, const double* rnext,
                         const double* vk_in, double* vk_out, const double* vk1, DevState* ds) {
   LaunchScope ls(st, kKRebuildTop, vbytes(n, s + 2.0));
+  static const bool early = std::getenv("MSTAB_NO_EARLY") == nullptr;
   MSTAB_DISPATCH_S(s, {
     auto kfn = k_rebuild_top<S>;
-    const int grid = occupancy_grid(kfn, n, 0);
-    launch_pdl(kfn, grid, kBlock, 0, st, n, ld, q, rnext, vk_in, vk_out, vk1, ds);
+    const size_t smem = early ? (size_t)(S + 1) * kBlock * sizeof(double2) : 0;
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((S + 1) * kBlock * sizeof(double2)));
+      configured = true;
+    }
+    const int grid = occupancy_grid(kfn, n, smem);
+    launch_pdl(kfn, grid, kBlock, smem, st, n, ld, q, rnext, vk_in, vk_out, vk1, ds, early ? 1 : 0);
   });
 }
 
