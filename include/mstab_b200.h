@@ -220,6 +220,13 @@ int mstab_solve(mstab_context* ctx, const mstab_operator* op, const double* b, c
 int mstab_sridr_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
                       int32_t mem, const mstab_solver_config* cfg, const mstab_recycle* recycle,
                       mstab_result** out);
+/* The comparison baselines (include/mstab/solvers/baselines.hpp, src/baselines.cpp:49-262) on
+ * the device: bicgstab_solve (shadow: N values in `mem`, or NULL for r0) and gmres_solve
+ * (full-memory, modified Gram-Schmidt, no restarts). The result holds x and the report. */
+int mstab_bicgstab_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
+                         int32_t mem, double tol, int64_t max_mv, const double* shadow, mstab_result** out);
+int mstab_gmres_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
+                      int32_t mem, double tol, int64_t max_it, mstab_result** out);
 void mstab_result_destroy(mstab_result* res);
 int mstab_result_report(const mstab_result* res, mstab_report* out);
 /* SolveResult::x, copied into x (N values in `mem`). */

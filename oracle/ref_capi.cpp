@@ -37,7 +37,7 @@ struct mstab_recycle {
 };
 struct mstab_result {
   mstab::SolveResult r;
-  bool sridr = false;  // sridr_solve returns x and the report only
+  bool sridr = false;  // sridr_solve and the baselines return x and the report only
 };
 
 namespace {
@@ -372,6 +372,39 @@ int mstab_sridr_solve(mstab_context*, const mstab_operator* op, const double* b,
     mstab::Vector bv = to_vec(b, n);
     mstab::Vector xv = x0 ? to_vec(x0, n) : mstab::Vector{};
     auto [x, rep] = mstab::sridr_solve(*op->op, bv, xv, sc, *recycle->d);
+    auto r = std::make_unique<mstab_result>();
+    r->r.x = std::move(x);
+    r->r.report = std::move(rep);
+    r->sridr = true;
+    *out = r.release();
+  });
+}
+
+int mstab_bicgstab_solve(mstab_context*, const mstab_operator* op, const double* b, const double* x0, int32_t mem,
+                         double tol, int64_t max_mv, const double* shadow, mstab_result** out) {
+  return guarded([&] {
+    host_only(mem);
+    const int64_t n = (int64_t)op->m.n_rows;
+    const mstab::Vector bv = to_vec(b, n);
+    const mstab::Vector xv = x0 ? to_vec(x0, n) : mstab::Vector{};
+    const mstab::Vector sv = shadow ? to_vec(shadow, n) : mstab::Vector{};
+    auto [x, rep] = mstab::bicgstab_solve(*op->op, bv, xv, tol, max_mv, shadow ? &sv : nullptr);
+    auto r = std::make_unique<mstab_result>();
+    r->r.x = std::move(x);
+    r->r.report = std::move(rep);
+    r->sridr = true;
+    *out = r.release();
+  });
+}
+
+int mstab_gmres_solve(mstab_context*, const mstab_operator* op, const double* b, const double* x0, int32_t mem,
+                      double tol, int64_t max_it, mstab_result** out) {
+  return guarded([&] {
+    host_only(mem);
+    const int64_t n = (int64_t)op->m.n_rows;
+    const mstab::Vector bv = to_vec(b, n);
+    const mstab::Vector xv = x0 ? to_vec(x0, n) : mstab::Vector{};
+    auto [x, rep] = mstab::gmres_solve(*op->op, bv, xv, tol, max_it);
     auto r = std::make_unique<mstab_result>();
     r->r.x = std::move(x);
     r->r.report = std::move(rep);

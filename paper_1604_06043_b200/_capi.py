@@ -101,6 +101,8 @@ ABI = [
     ("mstab_solve", C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(SolverConfigC), _P,
                               C.POINTER(FetchPolicyC), C.POINTER(_P)]),
     ("mstab_sridr_solve", C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(SolverConfigC), _P, C.POINTER(_P)]),
+    ("mstab_bicgstab_solve", C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_double, C.c_int64, _P, C.POINTER(_P)]),
+    ("mstab_gmres_solve", C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_double, C.c_int64, C.POINTER(_P)]),
     ("mstab_result_destroy", None, [_P]),
     ("mstab_result_report", C.c_int, [_P, C.POINTER(ReportC)]),
     ("mstab_result_x", C.c_int, [_P, _P, _P, C.c_int32]),

@@ -357,6 +357,26 @@ int mstab_sridr_solve(mstab_context* ctx, const mstab_operator* op, const double
   });
 }
 
+int mstab_bicgstab_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
+                         int32_t mem, double tol, int64_t max_mv, const double* shadow, mstab_result** out) {
+  return guarded([&] {
+    bind(ctx);
+    auto r = std::make_unique<mstab_result>();
+    r->impl = bicgstab(*ctx->impl, *op->impl, b, x0, mem, tol, max_mv, shadow);
+    *out = r.release();
+  });
+}
+
+int mstab_gmres_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
+                      int32_t mem, double tol, int64_t max_it, mstab_result** out) {
+  return guarded([&] {
+    bind(ctx);
+    auto r = std::make_unique<mstab_result>();
+    r->impl = gmres(*ctx->impl, *op->impl, b, x0, mem, tol, max_it);
+    *out = r.release();
+  });
+}
+
 void mstab_result_destroy(mstab_result* res) { delete res; }
 
 int mstab_result_report(const mstab_result* res, mstab_report* out) {

@@ -205,6 +205,13 @@ void launch_tri_solve(cudaStream_t st, const DevTri& f, const double* b, double*
 void launch_ph_fin(cudaStream_t st, int64_t n, int64_t ld, int s, const double* w, double* y, const double* p,
                    const double* b, const FinParams& fin, const Reducer& red);
 
+// ---- comparison baselines (kbase.cu, baselines.cpp:49-262) ------------------------------------
+// out = x + a * y (out may alias x)
+void launch_xpay(cudaStream_t st, int64_t n, const double* x, const double* y, double a, double* out);
+// p = r + beta * (p - omega * ap)
+void launch_bicgstab_p(cudaStream_t st, int64_t n, const double* r, const double* ap, double beta, double omega,
+                       double* p);
+
 // ---- SRIDR recycled phase (ksridr.cu, sridr.cpp:57-81) ------------------------------------
 // rt = r - V gamma, xt = x + U gamma (gamma = ds->gamma[0..s))
 void launch_sridr_corr(cudaStream_t st, int64_t n, int64_t ld, int s, const double* r, const double* x,

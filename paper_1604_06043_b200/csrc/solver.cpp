@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <complex>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -1251,6 +1252,239 @@ std::unique_ptr<SolveResultImpl> sridr(Context& ctx, const Operator& op, const d
   ctx.sync();
   rep.wall_ns_total = ns_since(t0);
   return res;
+}
+
+// ---- comparison baselines (baselines.cpp:49-262) ---------------------------
+// BiCGStab and full-memory GMRES (MGS) on the device: every length-N step is a kernel (SpMV,
+// dots, updates); the scalar recurrences (alpha, omega, beta, the Givens rotations and the
+// Hessenberg back-substitution) run on the host in std::complex<double> exactly as the reference
+// writes them, so for real data every element-wise update rounds like the reference's and only the
+// length-N reductions differ (tree sums).
+namespace {
+
+struct BaselineStart {
+  std::unique_ptr<SolveResultImpl> res;
+  DevPtr b, x, r;
+  Clock::time_point t0;
+};
+
+BaselineStart baseline_start(Context& ctx, const Operator& op, const double* b_in, const double* x0_in, int mem) {
+  BaselineStart st0;
+  const int64_t n = op.n;
+  cudaStream_t st = ctx.stream();
+  reset_status(ctx);
+  st0.t0 = Clock::now();
+  st0.res = std::make_unique<SolveResultImpl>();
+  st0.res->n = n;
+  std::memset(&st0.res->report, 0, sizeof(mstab_report));
+  st0.res->report.ell = 1;
+  const cudaMemcpyKind kind = mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  st0.b = ctx.alloc_vecs(n, 1);
+  st0.x = ctx.alloc_vecs(n, 1);
+  st0.r = ctx.alloc_vecs(n, 1);
+  CUDA_OK(cudaMemcpyAsync(st0.b->d(), b_in, sizeof(double) * n, kind, st));
+  launch_vec_stats(st, n, st0.b->d(), scal(ctx, 0), ctx.reducer());
+  check_launch();
+  st0.res->report.bnorm = std::sqrt(read_scal(ctx, 3)[0]);
+  bool x_zero = true;
+  if (x0_in) {
+    CUDA_OK(cudaMemcpyAsync(st0.x->d(), x0_in, sizeof(double) * n, kind, st));
+    launch_vec_stats(st, n, st0.x->d(), scal(ctx, 0), ctx.reducer());
+    check_launch();
+    x_zero = read_scal(ctx, 3)[2] == 0.0;
+  } else {
+    CUDA_OK(cudaMemsetAsync(st0.x->ptr, 0, sizeof(double) * ctx.ld(n), st));
+  }
+  CUDA_OK(cudaMemcpyAsync(st0.r->d(), st0.b->d(), sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  if (!x_zero) {  // initial_residual (baselines.cpp:22-32)
+    spmv_dev(ctx, op, st0.x->d(), st0.r->d());
+    launch_rsub(st, n, st0.b->d(), st0.r->d());
+    check_launch();
+    st0.res->report.h_mv_aux++;
+  }
+  return st0;
+}
+
+// dst[0] = dot(a, y) (when a), dst[last] = ||y||^2; returns the host copy of the first `count` scal.
+const double* dots_host(Context& ctx, int64_t n, const double* a, const double* y) {
+  launch_dots(ctx.stream(), n, ctx.ld(n), a, a ? 1 : 0, y, true, scal(ctx, 0), ctx.reducer());
+  check_launch();
+  return read_scal(ctx, a ? 2 : 1);
+}
+
+void baseline_finish(Context& ctx, BaselineStart& s0, int64_t it, double resnorm, double threshold, bool broke) {
+  mstab_report& rep = s0.res->report;
+  rep.cycles = it;
+  rep.h_rd = it;
+  if (!broke) rep.status = resnorm <= threshold ? MSTAB_STATUS_CONVERGED : MSTAB_STATUS_MAXMV;
+  rep.final_resnorm = resnorm;
+  s0.res->x = s0.x;
+  rep.history_len = (int64_t)s0.res->history.size();
+  ctx.sync();
+  rep.wall_ns_total = ns_since(s0.t0);
+}
+
+}  // namespace
+
+std::unique_ptr<SolveResultImpl> bicgstab(Context& ctx, const Operator& op, const double* b_in, const double* x0_in,
+                                          int mem, double tol, int64_t max_mv, const double* shadow) {
+  using C = std::complex<double>;
+  const int64_t n = op.n;
+  cudaStream_t st = ctx.stream();
+  BaselineStart s0 = baseline_start(ctx, op, b_in, x0_in, mem);
+  mstab_report& rep = s0.res->report;
+  auto& hist = s0.res->history;
+  double* x = s0.x->d();
+  double* r = s0.r->d();
+  double resnorm = std::sqrt(dots_host(ctx, n, nullptr, r)[0]);
+  hist.push_back({0, rep.h_mv + rep.h_mv_aux, 0, resnorm, ns_since(s0.t0)});
+  const double threshold = tol * rep.bnorm;
+  DevPtr rs = ctx.alloc_vecs(n, 1), p = ctx.alloc_vecs(n, 1), sv = ctx.alloc_vecs(n, 1), ap = ctx.alloc_vecs(n, 1),
+         as = ctx.alloc_vecs(n, 1);
+  CUDA_OK(cudaMemcpyAsync(rs->d(), shadow ? shadow : r, sizeof(double) * n,
+                          shadow && mem != MSTAB_MEM_DEVICE ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+  CUDA_OK(cudaMemcpyAsync(p->d(), r, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  C rho = dots_host(ctx, n, rs->d(), r)[0];
+  int64_t it = 0;
+  bool broke = false;
+  auto breakdown = [&](const char* why) {
+    rep.status = MSTAB_STATUS_BREAKDOWN;
+    std::snprintf(rep.breakdown_reason, sizeof(rep.breakdown_reason), "%s", why);
+    broke = true;
+  };
+  while (resnorm > threshold && rep.h_mv < max_mv) {  // baselines.cpp:219-254
+    if (std::abs(rho) == 0.0) { breakdown("bicgstab: rho collapsed"); break; }
+    spmv_dev(ctx, op, p->d(), ap->d());
+    rep.h_mv++;
+    const C denom = dots_host(ctx, n, rs->d(), ap->d())[0];
+    if (std::abs(denom) == 0.0) { breakdown("bicgstab: shadow projection collapsed"); break; }
+    const C alpha = rho / denom;
+    launch_xpay(st, n, r, ap->d(), -alpha.real(), sv->d());
+    if (std::sqrt(dots_host(ctx, n, nullptr, sv->d())[0]) <= threshold) {  // converged after the BiCG half-step
+      launch_xpay(st, n, x, p->d(), alpha.real(), x);
+      CUDA_OK(cudaMemcpyAsync(r, sv->d(), sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      ++it;
+      resnorm = std::sqrt(dots_host(ctx, n, nullptr, r)[0]);
+      hist.push_back({it, rep.h_mv + rep.h_mv_aux, it, resnorm, ns_since(s0.t0)});
+      break;
+    }
+    spmv_dev(ctx, op, sv->d(), as->d());
+    rep.h_mv++;
+    const double* h = dots_host(ctx, n, sv->d(), as->d());  // dot(s, as), ||as||^2
+    const C sdot = h[0];
+    const double nas = std::sqrt(h[1]);
+    const double as2 = std::pow(nas, 2);
+    if (as2 == 0.0) { breakdown("bicgstab: stagnated update"); break; }
+    const C omega = sdot / as2;
+    launch_xpay(st, n, x, p->d(), alpha.real(), x);
+    launch_xpay(st, n, x, sv->d(), omega.real(), x);
+    launch_xpay(st, n, sv->d(), as->d(), -omega.real(), r);
+    const C rho_next = dots_host(ctx, n, rs->d(), r)[0];
+    const C beta = (rho_next / rho) * (alpha / omega);
+    rho = rho_next;
+    launch_bicgstab_p(st, n, r, ap->d(), beta.real(), omega.real(), p->d());
+    check_launch();
+    ++it;
+    resnorm = std::sqrt(dots_host(ctx, n, nullptr, r)[0]);
+    hist.push_back({it, rep.h_mv + rep.h_mv_aux, it, resnorm, ns_since(s0.t0)});
+  }
+  baseline_finish(ctx, s0, it, resnorm, threshold, broke);
+  return std::move(s0.res);
+}
+
+std::unique_ptr<SolveResultImpl> gmres(Context& ctx, const Operator& op, const double* b_in, const double* x0_in,
+                                       int mem, double tol, int64_t max_it) {
+  using C = std::complex<double>;
+  const int64_t n = op.n, ld = ctx.ld(n);
+  cudaStream_t st = ctx.stream();
+  BaselineStart s0 = baseline_start(ctx, op, b_in, x0_in, mem);
+  mstab_report& rep = s0.res->report;
+  auto& hist = s0.res->history;
+  double* x = s0.x->d();
+  double* r = s0.r->d();
+  const double r2 = dots_host(ctx, n, nullptr, r)[0];
+  const double r0norm = std::sqrt(r2);
+  hist.push_back({0, rep.h_mv + rep.h_mv_aux, 0, r0norm, ns_since(s0.t0)});
+  const double threshold = tol * rep.bnorm;
+  if (r0norm <= threshold || max_it == 0) {  // baselines.cpp:63-68
+    baseline_finish(ctx, s0, 0, r0norm, threshold, false);
+    s0.res->report.h_rd = 0;
+    return std::move(s0.res);
+  }
+  const int64_t m_cap = std::min<int64_t>(max_it, n);
+  std::vector<DevPtr> q;  // basis columns, allocated as the iteration needs them
+  q.push_back(ctx.alloc_vecs(n, 1));
+  DevPtr hbuf = ctx.alloc(sizeof(double) * (size_t)(m_cap + 2));
+  double* hd = hbuf->d();
+  CUDA_OK(cudaMemcpyAsync(hd, &r2, sizeof(double), cudaMemcpyHostToDevice, st));
+  launch_div_by_sqrt(st, n, r, hd, q[0]->d());  // q0 = r / ||r||
+  std::vector<std::vector<C>> hess;              // column-major: hess[it][i]
+  std::vector<double> cs;
+  std::vector<C> sn, g(1, C(r0norm));
+  std::vector<double> hcol;
+  double resnorm = r0norm;
+  int64_t it = 0;
+  DevPtr w = ctx.alloc_vecs(n, 1);
+  while (it < m_cap && resnorm > threshold) {  // baselines.cpp:86-132
+    spmv_dev(ctx, op, q[it]->d(), w->d());
+    rep.h_mv++;
+    for (int64_t i = 0; i <= it; ++i) {  // modified Gram-Schmidt: h(i,it) = <q_i, w>; w -= h q_i
+      launch_dots(st, n, ld, q[i]->d(), 1, w->d(), false, hd + i, ctx.reducer());
+      launch_axpy_neg(st, n, ld, q[i]->d(), 1, hd + i, w->d());
+    }
+    launch_dots(st, n, ld, nullptr, 0, w->d(), true, hd + it + 1, ctx.reducer());
+    check_launch();
+    hcol.resize((size_t)it + 2);
+    CUDA_OK(cudaMemcpyAsync(hcol.data(), hd, sizeof(double) * (size_t)(it + 2), cudaMemcpyDeviceToHost, st));
+    ctx.sync();
+    const double hnext = std::sqrt(hcol[(size_t)it + 1]);
+    if (hnext > 0.0) {
+      q.push_back(ctx.alloc_vecs(n, 1));
+      launch_div_by_sqrt(st, n, w->d(), hd + it + 1, q[(size_t)it + 1]->d());  // q_{it+1} = w / ||w||
+      check_launch();
+    }
+    std::vector<C> col((size_t)it + 2);
+    for (int64_t i = 0; i <= it; ++i) col[(size_t)i] = C(hcol[(size_t)i]);
+    col[(size_t)it + 1] = C(hnext);
+    for (int64_t i = 0; i < it; ++i) {  // previous rotations, then the new one
+      const C t1 = col[(size_t)i], t2 = col[(size_t)i + 1];
+      col[(size_t)i] = cs[(size_t)i] * t1 + std::conj(sn[(size_t)i]) * t2;
+      col[(size_t)i + 1] = -sn[(size_t)i] * t1 + cs[(size_t)i] * t2;
+    }
+    const C h1 = col[(size_t)it], h2 = col[(size_t)it + 1];
+    const double denom = std::sqrt(std::norm(h1) + std::norm(h2));
+    if (denom == 0.0) {
+      cs.push_back(1.0);
+      sn.push_back(0.0);
+    } else {
+      cs.push_back(std::abs(h1) / denom);
+      const C phase = h1 == C(0.0) ? C(1.0) : h1 / std::abs(h1);
+      sn.push_back(h2 * std::conj(phase) / denom);
+      col[(size_t)it] = phase * denom;
+      col[(size_t)it + 1] = 0.0;
+    }
+    hess.push_back(col);
+    const C g1 = g[(size_t)it];
+    g[(size_t)it] = cs[(size_t)it] * g1;
+    g.push_back(-sn[(size_t)it] * g1);
+    resnorm = std::abs(g[(size_t)it + 1]);
+    ++it;
+    hist.push_back({it, rep.h_mv + rep.h_mv_aux, it, resnorm, ns_since(s0.t0)});
+    if (hnext == 0.0) break;  // lucky breakdown
+  }
+  std::vector<C> y((size_t)it);
+  for (int64_t k = it; k-- > 0;) {
+    C acc = g[(size_t)k];
+    for (int64_t j = k + 1; j < it; ++j) acc -= hess[(size_t)j][(size_t)k] * y[(size_t)j];
+    y[(size_t)k] = acc / hess[(size_t)k][(size_t)k];
+  }
+  for (int64_t k = 0; k < it; ++k) {
+    if (y[(size_t)k].imag() != 0.0) throw Error(MSTAB_E_NOTREAL, "gmres: complex coefficients (real fp64 path)");
+    launch_xpay(st, n, x, q[(size_t)k]->d(), y[(size_t)k].real(), x);  // axpy(y_k, q_k, x)
+  }
+  check_launch();
+  baseline_finish(ctx, s0, it, resnorm, threshold, false);
+  return std::move(s0.res);
 }
 
 }  // namespace mstab_b200

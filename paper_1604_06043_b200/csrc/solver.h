@@ -182,6 +182,12 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
 std::unique_ptr<SolveResultImpl> sridr(Context& ctx, const Operator& op, const double* b, const double* x0, int mem,
                                        const mstab_solver_config& cfg, const Recycle& recycle);
 
+// bicgstab_solve / gmres_solve (baselines.cpp:49-262) on the device; x and the report only.
+std::unique_ptr<SolveResultImpl> bicgstab(Context& ctx, const Operator& op, const double* b, const double* x0, int mem,
+                                          double tol, int64_t max_mv, const double* shadow);
+std::unique_ptr<SolveResultImpl> gmres(Context& ctx, const Operator& op, const double* b, const double* x0, int mem,
+                                       double tol, int64_t max_it);
+
 // validate (recycle.cpp:40-83). Throws Error with the reference's class code.
 mstab_validation_report validate(Context& ctx, const Recycle& rd, const Operator& op);
 

@@ -727,6 +727,40 @@ def sridr_solve(a: CsrOperator, b, x0, cfg: SolverConfig, recycle: RecycleData):
     return res.x, res.report
 
 
+def _baseline_result(ctx, n, h):
+    res = SolveResult(ctx, h)
+    res.n = n
+    return res.x, res.report
+
+
+def bicgstab_solve(a: CsrOperator, b, x0, tol: float, max_mv: int, shadow=None):
+    """Textbook BiCGStab (baselines.hpp, baselines.cpp:198-262); returns (x, report)."""
+    n = a.size()
+    b = _f64(b)
+    if b.size != n:
+        raise DimensionMismatch("bicgstab: rhs size")
+    x0 = _f64(x0) if x0 is not None and len(x0) > 0 else None
+    sh = _f64(shadow) if shadow is not None else None
+    h = C.c_void_p()
+    _check(a.lib, a.lib.dll.mstab_bicgstab_solve(a.ctx.h, a.h, b.ctypes.data, x0.ctypes.data if x0 is not None else None,
+                                                 _capi.MEM_HOST, tol, max_mv,
+                                                 sh.ctypes.data if sh is not None else None, C.byref(h)))
+    return _baseline_result(a.ctx, n, h)
+
+
+def gmres_solve(a: CsrOperator, b, x0, tol: float, max_it: int):
+    """Full-memory GMRES with modified Gram-Schmidt (baselines.cpp:49-143); returns (x, report)."""
+    n = a.size()
+    b = _f64(b)
+    if b.size != n:
+        raise DimensionMismatch("gmres: rhs size")
+    x0 = _f64(x0) if x0 is not None and len(x0) > 0 else None
+    h = C.c_void_p()
+    _check(a.lib, a.lib.dll.mstab_gmres_solve(a.ctx.h, a.h, b.ctypes.data, x0.ctypes.data if x0 is not None else None,
+                                              _capi.MEM_HOST, tol, max_it, C.byref(h)))
+    return _baseline_result(a.ctx, n, h)
+
+
 # ---- kernel-level helpers (include/mstab_b200_kernels.h) --------------------------------------
 def solve_small(m, rhs, ctx: Optional[Context] = None) -> np.ndarray:
     ctx = ctx if ctx is not None else default_context()

@@ -33,6 +33,7 @@
 #include "mstab/precond.hpp"
 #include "mstab/recycle.hpp"
 #include "mstab/solvers/idrstab.hpp"
+#include "mstab/solvers/baselines.hpp"
 #include "mstab/solvers/report.hpp"
 #include "mstab/solvers/sridr.hpp"
 #include "mstab/types.hpp"
@@ -333,6 +334,45 @@ std::pair<Vector, SolveReport> sridr_solve(const LinearOperator& a, const Vector
   std::unique_ptr<mstab_result, void (*)(mstab_result*)> guard(res, mstab_result_destroy);
   std::pair<Vector, SolveReport> out;
   read_result(ss, res, n, 1, out.first, out.second);
+  return out;
+}
+
+// The comparison baselines (baselines.hpp, baselines.cpp:49-262) on the device.
+std::pair<Vector, SolveReport> gmres_solve(const LinearOperator& a, const Vector& b, const Vector& x0, double tol,
+                                           std::int64_t max_it) {
+  const std::size_t n = a.size();
+  if (b.size() != n) throw DimensionMismatch("gmres: rhs size");
+  Session& ss = session();
+  mstab_operator* op = device_operator(ss, a);
+  const std::vector<double> bh = real_parts(b, "rhs");
+  const std::vector<double> xh = real_parts(x0, "guess");
+  mstab_result* res = nullptr;
+  check(::mstab_gmres_solve(ss.ctx, op, bh.data(), x0.empty() ? nullptr : xh.data(), MSTAB_MEM_HOST, tol, max_it,
+                            &res));
+  std::unique_ptr<mstab_result, void (*)(mstab_result*)> guard(res, mstab_result_destroy);
+  std::pair<Vector, SolveReport> out;
+  read_result(ss, res, n, 1, out.first, out.second);
+  out.second.omega_history.clear();
+  return out;
+}
+
+std::pair<Vector, SolveReport> bicgstab_solve(const LinearOperator& a, const Vector& b, const Vector& x0, double tol,
+                                              std::int64_t max_mv, const Vector* shadow) {
+  const std::size_t n = a.size();
+  if (b.size() != n) throw DimensionMismatch("bicgstab: rhs size");
+  Session& ss = session();
+  mstab_operator* op = device_operator(ss, a);
+  const std::vector<double> bh = real_parts(b, "rhs");
+  const std::vector<double> xh = real_parts(x0, "guess");
+  std::vector<double> sh;
+  if (shadow) sh = real_parts(*shadow, "shadow");
+  mstab_result* res = nullptr;
+  check(::mstab_bicgstab_solve(ss.ctx, op, bh.data(), x0.empty() ? nullptr : xh.data(), MSTAB_MEM_HOST, tol, max_mv,
+                               shadow ? sh.data() : nullptr, &res));
+  std::unique_ptr<mstab_result, void (*)(mstab_result*)> guard(res, mstab_result_destroy);
+  std::pair<Vector, SolveReport> out;
+  read_result(ss, res, n, 1, out.first, out.second);
+  out.second.omega_history.clear();
   return out;
 }
 

@@ -349,3 +349,41 @@ def test_sridr_matches_reference(s, fetch_cycle, gpu_ctx, ref_ctx):
         assert np.linalg.norm(xg - xr) <= 1e-6 * np.linalg.norm(xr)
     else:
         assert rg.breakdown_reason.split(":")[0] == rr.breakdown_reason.split(":")[0]
+
+
+# ---- comparison baselines (baselines.cpp:49-262) vs the reference ---------------------------------
+@pytest.mark.parametrize("method", ["gmres", "bicgstab", "bicgstab_shadow"])
+def test_baselines_match_reference(method, gpu_ctx, ref_ctx):
+    a = pb.convdiff(2, 48, 5, (100.0, 100.0, 0.0), 1e-2)
+    cfg = pb.config("c1", grid=48)
+    x0, f = cfg.sources()
+    b = cfg.first_rhs(x0, f)
+    out = []
+    for ctx in (gpu_ctx, ref_ctx):
+        op = m.CsrOperator(a, ctx)
+        if method == "gmres":
+            out.append(m.gmres_solve(op, b, None, 1e-8, 400))
+        else:
+            shadow = m.make_cut_space(a.n_rows, 1, 3, ref_ctx)[:, 0] if method == "bicgstab_shadow" else None
+            out.append(m.bicgstab_solve(op, b, None, 1e-8, 4000, shadow))
+    (xg, rg), (xr, rr) = out
+    assert rg.status == rr.status == m.CONVERGED
+    assert abs(rg.cycles - rr.cycles) <= 2 and abs(rg.h_mv - rr.h_mv) <= 4
+    assert np.linalg.norm(xg - xr) <= 1e-6 * np.linalg.norm(xr)
+    # the first iterations agree closely (tree vs sequential sums only)
+    for i in range(min(5, len(rr.residual_history))):
+        a_, b_ = rg.residual_history[i].resnorm, rr.residual_history[i].resnorm
+        assert abs(a_ - b_) <= 1e-9 * b_, (i, a_, b_)
+
+
+def test_gmres_identity_and_monotone(gpu_ctx):
+    """Gmres.IdentityOneIterationAndMonotoneResiduals (test_solvers.cpp:460-480)."""
+    op = m.CsrOperator(m.CsrMatrix.identity(10), gpu_ctx)
+    x, rep = m.gmres_solve(op, pb.normal(16, 10), None, 1e-10, 100)
+    assert rep.status == m.CONVERGED and rep.cycles == 1
+    top = m.CsrOperator(tri(40), gpu_ctx)
+    x, rep = m.gmres_solve(top, np.ones(40), None, 1e-8, 100)
+    assert rep.status == m.CONVERGED and rep.cycles <= 40
+    h = [p.resnorm for p in rep.residual_history]
+    assert all(h[i] <= h[i - 1] * (1 + 1e-12) for i in range(1, len(h)))
+    assert np.linalg.norm(true_res(top, np.ones(40), x)) <= 10 * 1e-8 * np.sqrt(40)
