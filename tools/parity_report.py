@@ -57,3 +57,5 @@ if __name__ == "__main__":
     chain("c2 48^3", pb.config("c2", grid=48), 3, true_res=True)
     c3 = pb.config("c3", grid=262144)
     chain("c3 262k", c3, 4)
+    chain("c4 40^3", pb.config("c4", grid=40), 3, true_res=True)  # 27-point stencil, reduced size
+    chain("c5 48^3", pb.config("c5", grid=48), 4, true_res=True)
