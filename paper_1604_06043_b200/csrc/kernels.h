@@ -196,6 +196,10 @@ struct DevTri {
   const int32_t* ci = nullptr;
   const double* val = nullptr;
   const double* diag = nullptr;
+  // Level schedule (triangular factors): rows sorted by dependency level, each level padded with
+  // -1 to a multiple of 32 slots so a warp's 32 rows are mutually independent.
+  const int32_t* order = nullptr;
+  int64_t nslots = 0, nlevels = 0;
   bool lower = true;
 };
 // x = F^-1 b (lower_solve / upper_solve, precond.cpp:101-133), bit-identical; `sync` is n + 1

@@ -7,6 +7,9 @@
 // lower_solve / upper_solve (precond.cpp:101-133) for real data:
 //   x_i = b_i;  x_i -= f_ik * x_j  for the off-diagonal entries of row i in CSR order;  x_i /= diag
 // (complex products and quotients with zero imaginary parts round like the real ones).
+#include <cstdlib>
+#include <string>
+
 #include "kcommon.cuh"
 
 namespace mstab_b200 {
@@ -86,6 +89,81 @@ __global__ void __launch_bounds__(kBlock) k_tri_solve(int64_t n, const int32_t* 
   }
 }
 
+// Level-scheduled sync-free substitution (the default): the host sorts the rows by dependency
+// level (solver.cpp level_schedule), so the 32 rows of a work item are mutually independent and
+// each lane substitutes its own row, applying the row's products serially in CSR order — exactly
+// the reference's operation order. Items are taken from a global ticket in level order, so every
+// row a lane waits on belongs to an earlier item, held by a running warp: no deadlock.
+// The solution vector is its own done flag: x is filled with kTriPending (an all-ones NaN pattern,
+// which no division produces: the GPU's NaN results are the canonical positive quiet NaN) before
+// the launch, a row's value is published with one relaxed 64-bit store, and a dependent lane polls
+// the value itself — one L2 round trip per level handoff instead of flag + fence + value. The
+// entries of a row are loaded and its dependencies polled in batches of 8 independent loads.
+constexpr unsigned long long kTriPending = 0xffffffffffffffffull;
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(double* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kBlock) k_tri_levels(int64_t nslots, const int32_t* __restrict__ order,
+                                                       const int32_t* __restrict__ rp,
+                                                       const int32_t* __restrict__ ci,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ b, double* x, int lower,
+                                                       int* ticket) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t nitems = nslots / 32;
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= nitems) break;
+    const int i = __ldg(order + (int64_t)t * 32 + lane);
+    if (i < 0) continue;
+    const int beg = __ldg(rp + i), end = __ldg(rp + i + 1);
+    double xi = __ldg(b + i);
+    double diag = 0.0;
+    for (int k0 = beg; k0 < end; k0 += 8) {
+      int jj[8];
+      double ff[8];
+      unsigned long long xb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool in = k0 + u < end;
+        jj[u] = in ? __ldg(ci + k0 + u) : i;
+        ff[u] = in ? __ldg(val + k0 + u) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool dep = lower ? jj[u] < i : jj[u] > i;
+        xb[u] = dep ? ld_relaxed_u64(x + jj[u]) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool dep = lower ? jj[u] < i : jj[u] > i;
+        if (dep) {
+          while (xb[u] == kTriPending) {
+            __nanosleep(32);
+            xb[u] = ld_relaxed_u64(x + jj[u]);
+          }
+          xi = xi - ff[u] * __longlong_as_double((long long)xb[u]);
+        } else if (k0 + u < end && jj[u] == i) {
+          diag = ff[u];
+        }
+      }
+    }
+    unsigned long long out = (unsigned long long)__double_as_longlong(xi / diag);
+    if (out == kTriPending) out = 0x7fffffffffffffffull;  // never a result; belt and braces
+    st_relaxed_u64(x + i, out);
+  }
+}
+
 // Diagonal factor (split Jacobi: L = R = diag(sqrt(a_ii)), precond.cpp:23-37): x = b ./ d.
 __global__ void __launch_bounds__(kBlock) k_diag_solve(int64_t n, const double* __restrict__ d,
                                                        const double* __restrict__ b, double* __restrict__ x) {
@@ -132,6 +210,23 @@ void launch_tri_solve(cudaStream_t st, const DevTri& f, const double* b, double*
   LaunchScope ls(st, kKOther, (double)f.nnz * 12.0 + vbytes(f.n, 2.0));
   if (f.diag) {
     launch_pdl(k_diag_solve, grid_for(f.n), kBlock, 0, st, f.n, (const double*)f.diag, b, x);
+    return;
+  }
+  static const bool chain = [] {
+    const char* e = std::getenv("MSTAB_TRI_SCHEDULE");
+    return e && std::string(e) == "rows";
+  }();
+  static const int ctas_per_sm = [] {
+    const char* e = std::getenv("MSTAB_TRI_CTAS_PER_SM");
+    return e ? std::max(1, std::atoi(e)) : 2;
+  }();
+  if (f.order && !chain) {
+    cudaMemsetAsync(x, 0xff, sizeof(double) * (size_t)f.n, st);  // every row kTriPending
+    cudaMemsetAsync(sync, 0, sizeof(int), st);                     // ticket
+    const int64_t nitems = f.nslots / 32;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)g_num_sms * ctas_per_sm,
+                                                                 (nitems + (kBlock / 32) - 1) / (kBlock / 32)));
+    launch_pdl(k_tri_levels, grid, kBlock, 0, st, f.nslots, f.order, f.rp, f.ci, f.val, b, x, f.lower ? 1 : 0, sync);
     return;
   }
   cudaMemsetAsync(sync, 0, sizeof(int) * (size_t)(f.n + 1), st);

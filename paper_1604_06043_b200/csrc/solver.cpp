@@ -644,8 +644,37 @@ void emit_rows(int64_t n, const std::vector<std::vector<std::pair<int64_t, doubl
   }
 }
 
+// Dependency levels of a triangular factor (the wavefront schedule of lower_solve / upper_solve,
+// precond.cpp:95-127): level(i) = 1 + max level(j) over the entries lower_solve reads (j < i; j > i
+// for an upper factor), 0 for a row without any. Rows of one level are independent, so the device
+// solve gives each lane its own row. Returns the level-sorted slot list (ascending rows within a
+// level, every level padded with -1 to a multiple of 32) and the level count.
+std::vector<int32_t> level_schedule(int64_t n, const int64_t* rp, const int64_t* ci, bool lower, int64_t& nlevels) {
+  std::vector<int32_t> lev(n, 0);
+  int32_t maxlev = -1;
+  for (int64_t t = 0; t < n; ++t) {
+    const int64_t i = lower ? t : n - 1 - t;
+    int32_t l = 0;
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      const int64_t j = ci[k];
+      if (lower ? j < i : j > i) l = std::max(l, lev[j] + 1);
+    }
+    lev[i] = l;
+    maxlev = std::max(maxlev, l);
+  }
+  nlevels = maxlev + 1;
+  std::vector<int64_t> cnt(nlevels + 1, 0);
+  for (int64_t i = 0; i < n; ++i) ++cnt[lev[i] + 1];
+  std::vector<int64_t> start(nlevels + 1, 0);  // padded slot offset of each level
+  for (int64_t l = 0; l < nlevels; ++l) start[l + 1] = start[l] + (cnt[l + 1] + 31) / 32 * 32;
+  std::vector<int32_t> order(start[nlevels], -1);
+  std::vector<int64_t> fill(start.begin(), start.end() - 1);
+  for (int64_t i = 0; i < n; ++i) order[fill[lev[i]]++] = (int32_t)i;
+  return order;
+}
+
 DevTri upload_factor(Context& ctx, int64_t n, const int64_t* rp, const int64_t* ci, const double* val, bool lower,
-                     DevPtr& d_rp, DevPtr& d_ci, DevPtr& d_val, DevPtr& d_diag) {
+                     DevPtr& d_rp, DevPtr& d_ci, DevPtr& d_val, DevPtr& d_diag, DevPtr& d_ord) {
   DevTri f;
   f.n = n;
   f.nnz = rp[n];
@@ -672,6 +701,11 @@ DevTri upload_factor(Context& ctx, int64_t n, const int64_t* rp, const int64_t* 
   f.rp = static_cast<const int32_t*>(d_rp->ptr);
   f.ci = static_cast<const int32_t*>(d_ci->ptr);
   f.val = d_val->d();
+  const std::vector<int32_t> order = level_schedule(n, rp, ci, lower, f.nlevels);
+  f.nslots = (int64_t)order.size();
+  d_ord = ctx.alloc(sizeof(int32_t) * std::max<size_t>(order.size(), 1));
+  CUDA_OK(cudaMemcpyAsync(d_ord->ptr, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice, st));
+  f.order = static_cast<const int32_t*>(d_ord->ptr);
   ctx.sync();
   return f;
 }
@@ -768,8 +802,8 @@ std::shared_ptr<Operator> make_operator_precond(Context& ctx, int64_t n, const i
   op->fingerprint = h;
   auto pc = std::make_shared<Precond>();
   pc->kind = kind;
-  pc->L = upload_factor(ctx, n, l_rp, l_ci, l_val, true, pc->l_rp, pc->l_ci, pc->l_val, pc->l_diag);
-  pc->R = upload_factor(ctx, n, r_rp, r_ci, r_val, false, pc->r_rp, pc->r_ci, pc->r_val, pc->r_diag);
+  pc->L = upload_factor(ctx, n, l_rp, l_ci, l_val, true, pc->l_rp, pc->l_ci, pc->l_val, pc->l_diag, pc->l_ord);
+  pc->R = upload_factor(ctx, n, r_rp, r_ci, r_val, false, pc->r_rp, pc->r_ci, pc->r_val, pc->r_diag, pc->r_ord);
   pc->t1 = ctx.alloc_vecs(n, 1);
   pc->t2 = ctx.alloc_vecs(n, 1);
   pc->t3 = ctx.alloc_vecs(n, 1);
@@ -782,6 +816,10 @@ void precond_solve(Context& ctx, const Operator& op, int which, const double* x_
   if (!op.pc) {  // build_none: both factors are the identity
     CUDA_OK(cudaMemcpyAsync(y_dev, x_dev, sizeof(double) * op.n, cudaMemcpyDeviceToDevice, ctx.stream()));
     return;
+  }
+  if (x_dev == y_dev) {  // the level-scheduled solve uses its output as the done flags
+    CUDA_OK(cudaMemcpyAsync(op.pc->t3->d(), x_dev, sizeof(double) * op.n, cudaMemcpyDeviceToDevice, ctx.stream()));
+    x_dev = op.pc->t3->d();
   }
   launch_tri_solve(ctx.stream(), which == 0 ? op.pc->L : op.pc->R, x_dev, y_dev,
                    reinterpret_cast<int*>(op.pc->sync->ptr));

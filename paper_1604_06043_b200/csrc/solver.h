@@ -102,7 +102,7 @@ struct Context {
 // PreconditionedOperator), the factors on the device plus the scratch its applies use.
 struct Precond {
   int kind = 0;  // MSTAB_PRECOND_*
-  DevPtr l_rp, l_ci, l_val, l_diag, r_rp, r_ci, r_val, r_diag;
+  DevPtr l_rp, l_ci, l_val, l_diag, l_ord, r_rp, r_ci, r_val, r_diag, r_ord;
   DevTri L, R;
   DevPtr t1, t2, t3, sync, au;  // chain temporaries, tri-solve flags, A U block of validate
   int au_s = 0;
