@@ -184,6 +184,11 @@ uint64_t mstab_operator_fingerprint(const mstab_operator* op); /* operator.cpp:3
 /* y = A x (CsrOperator::apply, operator.cpp:25-28 -> spmv csr.cpp:103-113). */
 int mstab_operator_apply(mstab_context* ctx, const mstab_operator* op, const double* x, double* y,
                          int32_t mem);
+/* y = A^H x (CsrOperator::apply_adjoint, operator.cpp:30-33 -> spmv_adjoint csr.cpp:115-124),
+ * bit-identical for real data. A^H is built once per operator on first use. ConfigError for a
+ * preconditioned operator or a row slab. */
+int mstab_operator_apply_adjoint(mstab_context* ctx, const mstab_operator* op, const double* x, double* y,
+                                 int32_t mem);
 
 /* ---- recycle data (recycle.hpp:18-64) ----------------------------------------------------- */
 /* fetch(): deep copy of column-major P, U, V (N x s) plus omega history (re,im pairs),
@@ -225,6 +230,10 @@ int mstab_sridr_solve(mstab_context* ctx, const mstab_operator* op, const double
  * (full-memory, modified Gram-Schmidt, no restarts). The result holds x and the report. */
 int mstab_bicgstab_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
                          int32_t mem, double tol, int64_t max_mv, const double* shadow, mstab_result** out);
+/* bicg_solve (include/mstab/solvers/baselines.hpp, src/baselines.cpp:145-196): BiCG with the
+ * adjoint products on the device (two products per iteration); shadow as in bicgstab_solve. */
+int mstab_bicg_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
+                     int32_t mem, double tol, int64_t max_mv, const double* shadow, mstab_result** out);
 int mstab_gmres_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
                       int32_t mem, double tol, int64_t max_it, mstab_result** out);
 void mstab_result_destroy(mstab_result* res);

@@ -275,6 +275,16 @@ int mstab_operator_apply(mstab_context*, const mstab_operator* op, const double*
   });
 }
 
+int mstab_operator_apply_adjoint(mstab_context*, const mstab_operator* op, const double* x, double* y,
+                                 int32_t mem) {
+  return guarded([&] {
+    host_only(mem);
+    const int64_t n = (int64_t)op->m.n_rows;
+    mstab::Vector out = op->op->apply_adjoint(to_vec(x, n));
+    for (int64_t i = 0; i < n; ++i) y[i] = out[(size_t)i].real();
+  });
+}
+
 int mstab_recycle_create(mstab_context*, int64_t n, int64_t s, const double* p, const double* u,
                          const double* v, int32_t mem, const double* omega_re_im,
                          int64_t omega_count, int64_t level_j, uint64_t fingerprint,
@@ -389,6 +399,23 @@ int mstab_bicgstab_solve(mstab_context*, const mstab_operator* op, const double*
     const mstab::Vector xv = x0 ? to_vec(x0, n) : mstab::Vector{};
     const mstab::Vector sv = shadow ? to_vec(shadow, n) : mstab::Vector{};
     auto [x, rep] = mstab::bicgstab_solve(*op->op, bv, xv, tol, max_mv, shadow ? &sv : nullptr);
+    auto r = std::make_unique<mstab_result>();
+    r->r.x = std::move(x);
+    r->r.report = std::move(rep);
+    r->sridr = true;
+    *out = r.release();
+  });
+}
+
+int mstab_bicg_solve(mstab_context*, const mstab_operator* op, const double* b, const double* x0, int32_t mem,
+                     double tol, int64_t max_mv, const double* shadow, mstab_result** out) {
+  return guarded([&] {
+    host_only(mem);
+    const int64_t n = (int64_t)op->m.n_rows;
+    const mstab::Vector bv = to_vec(b, n);
+    const mstab::Vector xv = x0 ? to_vec(x0, n) : mstab::Vector{};
+    const mstab::Vector sv = shadow ? to_vec(shadow, n) : mstab::Vector{};
+    auto [x, rep] = mstab::bicg_solve(*op->op, bv, xv, tol, max_mv, shadow ? &sv : nullptr);
     auto r = std::make_unique<mstab_result>();
     r->r.x = std::move(x);
     r->r.report = std::move(rep);

@@ -84,6 +84,7 @@ ABI = [
     ("mstab_operator_nnz", C.c_int64, [_P]),
     ("mstab_operator_fingerprint", C.c_uint64, [_P]),
     ("mstab_operator_apply", C.c_int, [_P, _P, _P, _P, C.c_int32]),
+    ("mstab_operator_apply_adjoint", C.c_int, [_P, _P, _P, _P, C.c_int32]),
     ("mstab_precond_build", C.c_int, [C.c_int32, C.c_int64, _I64, _I64, _D, _I64, _I64, _D, _I64, _I64, _I64, _D,
                                       _I64]),
     ("mstab_operator_create_precond", C.c_int, [_P, C.c_int64, _I64, _I64, _D, C.c_int32, _I64, _I64, _D, _I64,
@@ -101,6 +102,7 @@ ABI = [
     ("mstab_solve", C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(SolverConfigC), _P,
                               C.POINTER(FetchPolicyC), C.POINTER(_P)]),
     ("mstab_sridr_solve", C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(SolverConfigC), _P, C.POINTER(_P)]),
+    ("mstab_bicg_solve", C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_double, C.c_int64, _P, C.POINTER(_P)]),
     ("mstab_bicgstab_solve", C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_double, C.c_int64, _P, C.POINTER(_P)]),
     ("mstab_gmres_solve", C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_double, C.c_int64, C.POINTER(_P)]),
     ("mstab_result_destroy", None, [_P]),

@@ -139,18 +139,20 @@ int64_t mstab_operator_size(const mstab_operator* op) { return op->impl->n; }
 int64_t mstab_operator_nnz(const mstab_operator* op) { return op->impl->nnz; }
 uint64_t mstab_operator_fingerprint(const mstab_operator* op) { return op->impl->fingerprint; }
 
-int mstab_operator_apply(mstab_context* ctx, const mstab_operator* op, const double* x, double* y,
-                         int32_t mem) {
-  return guarded([&] {
+namespace {
+
+// y = A x (adjoint: A^H x) with caller buffers in `mem`.
+void apply_mem(mstab_context* ctx, const mstab_operator* op, const double* x, double* y, int32_t mem, bool adjoint) {
     bind(ctx);
     Context& c = *ctx->impl;
-    const int64_t n = op->impl->n;
+    const Operator& a = adjoint ? adjoint_of(c, *op->impl) : *op->impl;
+    const int64_t n = a.n;
     // The SpMV kernels move row pairs with 16-byte accesses: caller buffers are used in place
     // only when 16-byte aligned and of even length, otherwise staged through padded buffers.
     const bool direct = !c.sharded() && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15u) == 0 &&
                         (n % 2) == 0;
     if (mem == MSTAB_MEM_DEVICE && direct) {
-      spmv(c, *op->impl, x, y);
+      spmv(c, a, x, y);
       c.sync();
       return;
     }
@@ -159,11 +161,22 @@ int mstab_operator_apply(mstab_context* ctx, const mstab_operator* op, const dou
     DevPtr dx = c.alloc_vecs(n, 1), dy = c.alloc_vecs(n, 1);
     if (cudaMemcpyAsync(dx->d(), x, sizeof(double) * n, in, c.stream()) != cudaSuccess)
       throw Error(MSTAB_E_CUDA, "upload x");
-    spmv(c, *op->impl, dx->d(), dy->d());
+    spmv(c, a, dx->d(), dy->d());
     if (cudaMemcpyAsync(y, dy->d(), sizeof(double) * n, out, c.stream()) != cudaSuccess)
       throw Error(MSTAB_E_CUDA, "download y");
     c.sync();
-  });
+}
+
+}  // namespace
+
+int mstab_operator_apply(mstab_context* ctx, const mstab_operator* op, const double* x, double* y,
+                         int32_t mem) {
+  return guarded([&] { apply_mem(ctx, op, x, y, mem, false); });
+}
+
+int mstab_operator_apply_adjoint(mstab_context* ctx, const mstab_operator* op, const double* x, double* y,
+                                 int32_t mem) {
+  return guarded([&] { apply_mem(ctx, op, x, y, mem, true); });
 }
 
 int mstab_precond_build(int32_t kind, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
@@ -363,6 +376,16 @@ int mstab_bicgstab_solve(mstab_context* ctx, const mstab_operator* op, const dou
     bind(ctx);
     auto r = std::make_unique<mstab_result>();
     r->impl = bicgstab(*ctx->impl, *op->impl, b, x0, mem, tol, max_mv, shadow);
+    *out = r.release();
+  });
+}
+
+int mstab_bicg_solve(mstab_context* ctx, const mstab_operator* op, const double* b, const double* x0,
+                     int32_t mem, double tol, int64_t max_mv, const double* shadow, mstab_result** out) {
+  return guarded([&] {
+    bind(ctx);
+    auto r = std::make_unique<mstab_result>();
+    r->impl = bicg(*ctx->impl, *op->impl, b, x0, mem, tol, max_mv, shadow);
     *out = r.release();
   });
 }

@@ -218,7 +218,7 @@ void launch_tri_solve(cudaStream_t st, const DevTri& f, const double* b, double*
   }();
   static const int ctas_per_sm = [] {
     const char* e = std::getenv("MSTAB_TRI_CTAS_PER_SM");
-    return e ? std::max(1, std::atoi(e)) : 2;
+    return e ? std::max(1, std::atoi(e)) : 1;
   }();
   if (f.order && !chain) {
     cudaMemsetAsync(x, 0xff, sizeof(double) * (size_t)f.n, st);  // every row kTriPending

@@ -1364,6 +1364,96 @@ void baseline_finish(Context& ctx, BaselineStart& s0, int64_t it, double resnorm
 
 }  // namespace
 
+// A^H of a plain CSR operator as a second operator (real data: A^T). spmv_adjoint scatters
+// y[col] += conj(a_ik) x_i over rows i ascending and entries k in CSR order (csr.cpp:115-124), so
+// y_j is the sum, from +0.0, of its terms in (i, k) order. The transpose built here lists row j's
+// entries in exactly that order (a stable bucket pass over the original entries), and every SpMV
+// kernel accumulates a row from +0.0 in CSR order: the device product is bit-identical to the
+// reference's scatter. The transpose goes through the normal upload, so a stencil's transpose gets
+// the same constant-diagonal / DIA forms. Built once per operator, on first use.
+const Operator& adjoint_of(Context& ctx, const Operator& op) {
+  std::lock_guard<std::mutex> lk(op.adj_mu);
+  if (op.adj) return *op.adj;
+  if (op.pc) throw Error(MSTAB_E_CONFIG, "b200: apply_adjoint of a preconditioned operator is not supported");
+  if (op.n_global != op.n) throw Error(MSTAB_E_CONFIG, "b200: apply_adjoint of a row slab is not supported");
+  const int64_t n = op.n, nnz = op.nnz;
+  std::vector<int32_t> rp(n + 1), ci(std::max<int64_t>(nnz, 1));
+  std::vector<double> val(std::max<int64_t>(nnz, 1));
+  cudaStream_t st = ctx.stream();
+  CUDA_OK(cudaMemcpyAsync(rp.data(), op.rp->ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+  if (nnz > 0) {
+    CUDA_OK(cudaMemcpyAsync(ci.data(), op.ci->ptr, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(val.data(), op.val->ptr, sizeof(double) * nnz, cudaMemcpyDeviceToHost, st));
+  }
+  ctx.sync();
+  std::vector<int64_t> trp(n + 1, 0), tci(std::max<int64_t>(nnz, 1));
+  std::vector<double> tval(std::max<int64_t>(nnz, 1));
+  for (int64_t k = 0; k < nnz; ++k) ++trp[ci[k] + 1];
+  for (int64_t j = 0; j < n; ++j) trp[j + 1] += trp[j];
+  std::vector<int64_t> fill(trp.begin(), trp.end() - 1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      const int64_t at = fill[ci[k]]++;
+      tci[at] = i;
+      tval[at] = val[k];  // conj of a real value
+    }
+  op.adj = make_operator(ctx, n, trp.data(), tci.data(), tval.data());
+  return *op.adj;
+}
+
+std::unique_ptr<SolveResultImpl> bicg(Context& ctx, const Operator& op, const double* b_in, const double* x0_in,
+                                      int mem, double tol, int64_t max_mv, const double* shadow) {
+  using C = std::complex<double>;
+  const int64_t n = op.n;
+  cudaStream_t st = ctx.stream();
+  const Operator& adj = adjoint_of(ctx, op);
+  BaselineStart s0 = baseline_start(ctx, op, b_in, x0_in, mem);
+  mstab_report& rep = s0.res->report;
+  auto& hist = s0.res->history;
+  double* x = s0.x->d();
+  double* r = s0.r->d();
+  double resnorm = std::sqrt(dots_host(ctx, n, nullptr, r)[0]);
+  hist.push_back({0, rep.h_mv + rep.h_mv_aux, 0, resnorm, ns_since(s0.t0)});
+  const double threshold = tol * rep.bnorm;
+  DevPtr rs = ctx.alloc_vecs(n, 1), p = ctx.alloc_vecs(n, 1), ps = ctx.alloc_vecs(n, 1), ap = ctx.alloc_vecs(n, 1),
+         aps = ctx.alloc_vecs(n, 1);
+  CUDA_OK(cudaMemcpyAsync(rs->d(), shadow ? shadow : r, sizeof(double) * n,
+                          shadow && mem != MSTAB_MEM_DEVICE ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+  CUDA_OK(cudaMemcpyAsync(p->d(), r, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  CUDA_OK(cudaMemcpyAsync(ps->d(), rs->d(), sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  C rho = dots_host(ctx, n, rs->d(), r)[0];
+  int64_t it = 0;
+  bool broke = false;
+  auto breakdown = [&](const char* why) {
+    rep.status = MSTAB_STATUS_BREAKDOWN;
+    std::snprintf(rep.breakdown_reason, sizeof(rep.breakdown_reason), "%s", why);
+    broke = true;
+  };
+  while (resnorm > threshold && rep.h_mv < max_mv) {  // baselines.cpp:166-186
+    if (std::abs(rho) == 0.0) { breakdown("bicg: rho collapsed"); break; }
+    spmv_dev(ctx, op, p->d(), ap->d());
+    spmv_dev(ctx, adj, ps->d(), aps->d());
+    rep.h_mv += 2;
+    const C sigma = dots_host(ctx, n, ps->d(), ap->d())[0];
+    if (std::abs(sigma) == 0.0) { breakdown("bicg: sigma collapsed"); break; }
+    const C alpha = rho / sigma;
+    launch_xpay(st, n, x, p->d(), alpha.real(), x);                       // axpy(alpha, p, x)
+    launch_xpay(st, n, r, ap->d(), (-alpha).real(), r);                  // axpy(-alpha, ap, r)
+    launch_xpay(st, n, rs->d(), aps->d(), (-std::conj(alpha)).real(), rs->d());  // axpy(-conj(alpha), aps, rs)
+    const C rho_next = dots_host(ctx, n, rs->d(), r)[0];
+    const C beta = rho_next / rho;
+    rho = rho_next;
+    launch_xpay(st, n, r, p->d(), beta.real(), p->d());                  // p = r + beta p
+    launch_xpay(st, n, rs->d(), ps->d(), std::conj(beta).real(), ps->d());  // ps = rs + conj(beta) ps
+    check_launch();
+    ++it;
+    resnorm = std::sqrt(dots_host(ctx, n, nullptr, r)[0]);
+    hist.push_back({it, rep.h_mv + rep.h_mv_aux, it, resnorm, ns_since(s0.t0)});
+  }
+  baseline_finish(ctx, s0, it, resnorm, threshold, broke);
+  return std::move(s0.res);
+}
+
 std::unique_ptr<SolveResultImpl> bicgstab(Context& ctx, const Operator& op, const double* b_in, const double* x0_in,
                                           int mem, double tol, int64_t max_mv, const double* shadow) {
   using C = std::complex<double>;

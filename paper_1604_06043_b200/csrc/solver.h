@@ -3,6 +3,7 @@
 #include <complex>
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -153,6 +154,9 @@ struct Operator {
   std::vector<double> cvals;
   DevPtr dia_mask;
   std::shared_ptr<Precond> pc;  // preconditioned operator L^-1 A R^-1 (nullptr: plain CSR)
+  // A^H as its own operator (CsrOperator::apply_adjoint), built on first use (adjoint_of)
+  mutable std::shared_ptr<Operator> adj;
+  mutable std::mutex adj_mu;
 };
 
 struct Recycle {
@@ -183,6 +187,11 @@ std::unique_ptr<SolveResultImpl> sridr(Context& ctx, const Operator& op, const d
                                        const mstab_solver_config& cfg, const Recycle& recycle);
 
 // bicgstab_solve / gmres_solve (baselines.cpp:49-262) on the device; x and the report only.
+// y = A^H x (CsrOperator::apply_adjoint -> spmv_adjoint, csr.cpp:115-124), bit-identical.
+const Operator& adjoint_of(Context& ctx, const Operator& op);
+// bicg_solve (baselines.cpp:145-196) on the device; x and the report only.
+std::unique_ptr<SolveResultImpl> bicg(Context& ctx, const Operator& op, const double* b, const double* x0, int mem,
+                                      double tol, int64_t max_mv, const double* shadow);
 std::unique_ptr<SolveResultImpl> bicgstab(Context& ctx, const Operator& op, const double* b, const double* x0, int mem,
                                           double tol, int64_t max_mv, const double* shadow);
 std::unique_ptr<SolveResultImpl> gmres(Context& ctx, const Operator& op, const double* b, const double* x0, int mem,

@@ -412,6 +412,21 @@ class CsrOperator:
                                                            _capi.MEM_HOST))
         return out
 
+    def apply_adjoint(self, x, y=None):
+        """A^H x (CsrOperator::apply_adjoint, operator.cpp:30-33; spmv_adjoint csr.cpp:115-124)."""
+        ptr, mem = _dev_ptr(x)
+        if mem == _capi.MEM_DEVICE:
+            yptr, _ = _dev_ptr(y)
+            _check(self.lib, self.lib.dll.mstab_operator_apply_adjoint(self.ctx.h, self.h, ptr, yptr, mem))
+            return y
+        x = _f64(x)
+        if x.size != self.size():
+            raise DimensionMismatch("spmv_adjoint: dimension mismatch")
+        out = np.empty_like(x)
+        _check(self.lib, self.lib.dll.mstab_operator_apply_adjoint(self.ctx.h, self.h, x.ctypes.data,
+                                                                   out.ctypes.data, _capi.MEM_HOST))
+        return out
+
     def __del__(self):
         if getattr(self, "h", None):
             self.lib.dll.mstab_operator_destroy(self.h)
@@ -731,6 +746,21 @@ def _baseline_result(ctx, n, h):
     res = SolveResult(ctx, h)
     res.n = n
     return res.x, res.report
+
+
+def bicg_solve(a: CsrOperator, b, x0, tol: float, max_mv: int, shadow=None):
+    """BiCG with adjoint products (baselines.hpp, baselines.cpp:145-196); returns (x, report)."""
+    n = a.size()
+    b = _f64(b)
+    if b.size != n:
+        raise DimensionMismatch("bicg: rhs size")
+    x0 = _f64(x0) if x0 is not None and len(x0) > 0 else None
+    sh = _f64(shadow) if shadow is not None else None
+    h = C.c_void_p()
+    _check(a.lib, a.lib.dll.mstab_bicg_solve(a.ctx.h, a.h, b.ctypes.data, x0.ctypes.data if x0 is not None else None,
+                                             _capi.MEM_HOST, tol, max_mv,
+                                             sh.ctypes.data if sh is not None else None, C.byref(h)))
+    return _baseline_result(a.ctx, n, h)
 
 
 def bicgstab_solve(a: CsrOperator, b, x0, tol: float, max_mv: int, shadow=None):

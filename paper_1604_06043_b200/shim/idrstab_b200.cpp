@@ -356,6 +356,26 @@ std::pair<Vector, SolveReport> gmres_solve(const LinearOperator& a, const Vector
   return out;
 }
 
+std::pair<Vector, SolveReport> bicg_solve(const LinearOperator& a, const Vector& b, const Vector& x0, double tol,
+                                          std::int64_t max_mv, const Vector* shadow) {
+  const std::size_t n = a.size();
+  if (b.size() != n) throw DimensionMismatch("bicg: rhs size");
+  Session& ss = session();
+  mstab_operator* op = device_operator(ss, a);
+  const std::vector<double> bh = real_parts(b, "rhs");
+  const std::vector<double> xh = real_parts(x0, "guess");
+  std::vector<double> sh;
+  if (shadow) sh = real_parts(*shadow, "shadow");
+  mstab_result* res = nullptr;
+  check(::mstab_bicg_solve(ss.ctx, op, bh.data(), x0.empty() ? nullptr : xh.data(), MSTAB_MEM_HOST, tol, max_mv,
+                           shadow ? sh.data() : nullptr, &res));
+  std::unique_ptr<mstab_result, void (*)(mstab_result*)> guard(res, mstab_result_destroy);
+  std::pair<Vector, SolveReport> out;
+  read_result(ss, res, n, 1, out.first, out.second);
+  out.second.omega_history.clear();
+  return out;
+}
+
 std::pair<Vector, SolveReport> bicgstab_solve(const LinearOperator& a, const Vector& b, const Vector& x0, double tol,
                                               std::int64_t max_mv, const Vector* shadow) {
   const std::size_t n = a.size();

@@ -88,3 +88,25 @@ def test_reference_impl_runs_through_the_same_abi(ref_ctx):
     assert (r.report.cycles, r.report.h_mv, r.report.status) == (20, 62, m.CONVERGED)
     # the host-only implementation rejects device pointers with ConfigError
     assert ref_ctx.lib.dll.mstab_operator_apply(ref_ctx.h, op.h, None, None, 1) == -3
+
+
+def test_reference_adjoint_and_bicg_through_the_abi(ref_ctx):
+    """apply_adjoint and bicg_solve on the reference side of the ABI (the oracle the B200 path is
+    checked against): A^H x equals the sequential scatter of csr.cpp:115-124, and BiCG on an SPD
+    diagonal system converges in at most n iterations like CG (test_solvers.cpp:483-500)."""
+    import numpy as np
+
+    import paper_1604_06043_b200 as m
+    A = m.CsrMatrix.from_triplets(5, 5, [(0, 0, 2.0), (0, 3, -1.0), (1, 1, 3.0), (2, 0, 0.5), (2, 2, 4.0),
+                                         (3, 1, 1.5), (3, 3, 1.0), (4, 2, -2.0), (4, 4, 5.0)])
+    op = m.CsrOperator(A, ref_ctx)
+    x = np.array([1.0, -2.0, 0.25, 3.0, -0.5])
+    y = np.zeros(5)
+    for i in range(5):  # y[col] += a_ik x_i, rows ascending
+        for k in range(int(A.row_ptr[i]), int(A.row_ptr[i + 1])):
+            y[int(A.col_idx[k])] += A.values[k] * x[i]
+    assert np.array_equal(op.apply_adjoint(x), y)
+    d = m.CsrMatrix.from_triplets(8, 8, [(i, i, float(i + 1)) for i in range(8)])
+    xs, rep = m.bicg_solve(m.CsrOperator(d, ref_ctx), np.ones(8), None, 1e-12, 1000)
+    assert rep.status == m.CONVERGED and rep.cycles <= 8
+    assert np.allclose(xs, 1.0 / np.arange(1, 9), rtol=1e-10)

@@ -49,6 +49,18 @@ def test_spmv_bit_exact_and_fingerprint(gpu_ctx, name, A):
         assert np.array_equal(op.apply(x), c.apply(x))
 
 
+@pytest.mark.parametrize("name,A", list(matrices()), ids=[n for n, _ in matrices()])
+def test_spmv_adjoint_bit_exact(gpu_ctx, ref_ctx, name, A):
+    """A^H x through the device transpose vs the reference's scatter (csr.cpp:115-124), bit for bit."""
+    op = m.CsrOperator(A, gpu_ctx)
+    ref = m.CsrOperator(A, ref_ctx)
+    rng = np.random.default_rng(4)
+    for _ in range(2):
+        x = rng.standard_normal(A.n_rows)
+        assert np.array_equal(op.apply_adjoint(x), ref.apply_adjoint(x))
+    assert np.array_equal(op.apply(x), ref.apply(x))  # the forward product is untouched
+
+
 def test_solve_small_bit_exact(gpu_ctx, golden_kernels):
     g = golden_kernels
     for s in (1, 2, 3, 4, 8, 16):

@@ -352,7 +352,7 @@ def test_sridr_matches_reference(s, fetch_cycle, gpu_ctx, ref_ctx):
 
 
 # ---- comparison baselines (baselines.cpp:49-262) vs the reference ---------------------------------
-@pytest.mark.parametrize("method", ["gmres", "bicgstab", "bicgstab_shadow"])
+@pytest.mark.parametrize("method", ["gmres", "bicgstab", "bicgstab_shadow", "bicg", "bicg_shadow"])
 def test_baselines_match_reference(method, gpu_ctx, ref_ctx):
     a = pb.convdiff(2, 48, 5, (100.0, 100.0, 0.0), 1e-2)
     cfg = pb.config("c1", grid=48)
@@ -364,11 +364,19 @@ def test_baselines_match_reference(method, gpu_ctx, ref_ctx):
         if method == "gmres":
             out.append(m.gmres_solve(op, b, None, 1e-8, 400))
         else:
-            shadow = m.make_cut_space(a.n_rows, 1, 3, ref_ctx)[:, 0] if method == "bicgstab_shadow" else None
-            out.append(m.bicgstab_solve(op, b, None, 1e-8, 4000, shadow))
+            shadow = m.make_cut_space(a.n_rows, 1, 3, ref_ctx)[:, 0] if method.endswith("_shadow") else None
+            solve = m.bicg_solve if method.startswith("bicg_") or method == "bicg" else m.bicgstab_solve
+            out.append(solve(op, b, None, 1e-8, 4000, shadow))
     (xg, rg), (xr, rr) = out
     assert rg.status == rr.status == m.CONVERGED
-    assert abs(rg.cycles - rr.cycles) <= 2 and abs(rg.h_mv - rr.h_mv) <= 4
+    if method.startswith("bicg") and not method.startswith("bicgstab"):
+        # BiCG's residual is erratic (no minimisation), so over ~150 iterations the tree-vs-
+        # sequential rounding of the dots shifts the exit by several iterations: the bar is the
+        # converged solution, a 10% iteration window and close agreement of the early history.
+        assert abs(rg.cycles - rr.cycles) <= max(2, rr.cycles // 10)
+        assert rg.h_mv == 2 * rg.cycles and rr.h_mv == 2 * rr.cycles
+    else:
+        assert abs(rg.cycles - rr.cycles) <= 2 and abs(rg.h_mv - rr.h_mv) <= 4
     assert np.linalg.norm(xg - xr) <= 1e-6 * np.linalg.norm(xr)
     # the first iterations agree closely (tree vs sequential sums only)
     for i in range(min(5, len(rr.residual_history))):
