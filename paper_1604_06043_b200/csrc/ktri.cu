@@ -99,6 +99,8 @@ __global__ void __launch_bounds__(kBlock) k_tri_solve(int64_t n, const int32_t* 
 // the launch, a row's value is published with one relaxed 64-bit store, and a dependent lane polls
 // the value itself — one L2 round trip per level handoff instead of flag + fence + value. The
 // entries of a row are loaded and its dependencies polled in batches of 8 independent loads.
+// Polling spins without a back-off by default (measured on c2: 1.64 ms per apply against 2.4 ms
+// with a 32 ns __nanosleep; MSTAB_TRI_SLEEP_NS sets one) with one 256-thread CTA per SM.
 constexpr unsigned long long kTriPending = 0xffffffffffffffffull;
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const double* p) {
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(kBlock) k_tri_levels(int64_t nslots, const int
                                                        const int32_t* __restrict__ ci,
                                                        const double* __restrict__ val,
                                                        const double* __restrict__ b, double* x, int lower,
-                                                       int* ticket) {
+                                                       int* ticket, int sleep_ns) {
   pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t nitems = nslots / 32;
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(kBlock) k_tri_levels(int64_t nslots, const int
         const bool dep = lower ? jj[u] < i : jj[u] > i;
         if (dep) {
           while (xb[u] == kTriPending) {
-            __nanosleep(32);
+            if (sleep_ns) __nanosleep(sleep_ns);
             xb[u] = ld_relaxed_u64(x + jj[u]);
           }
           xi = xi - ff[u] * __longlong_as_double((long long)xb[u]);
@@ -220,13 +222,17 @@ void launch_tri_solve(cudaStream_t st, const DevTri& f, const double* b, double*
     const char* e = std::getenv("MSTAB_TRI_CTAS_PER_SM");
     return e ? std::max(1, std::atoi(e)) : 1;
   }();
+  static const int sleep_ns = [] {
+    const char* e = std::getenv("MSTAB_TRI_SLEEP_NS");
+    return e ? std::max(0, std::atoi(e)) : 0;
+  }();
   if (f.order && !chain) {
     cudaMemsetAsync(x, 0xff, sizeof(double) * (size_t)f.n, st);  // every row kTriPending
     cudaMemsetAsync(sync, 0, sizeof(int), st);                     // ticket
     const int64_t nitems = f.nslots / 32;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)g_num_sms * ctas_per_sm,
                                                                  (nitems + (kBlock / 32) - 1) / (kBlock / 32)));
-    launch_pdl(k_tri_levels, grid, kBlock, 0, st, f.nslots, f.order, f.rp, f.ci, f.val, b, x, f.lower ? 1 : 0, sync);
+    launch_pdl(k_tri_levels, grid, kBlock, 0, st, f.nslots, f.order, f.rp, f.ci, f.val, b, x, f.lower ? 1 : 0, sync, sleep_ns);
     return;
   }
   cudaMemsetAsync(sync, 0, sizeof(int) * (size_t)(f.n + 1), st);
