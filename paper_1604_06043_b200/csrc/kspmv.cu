@@ -341,7 +341,7 @@ void launch_dia_tma(cudaStream_t st, const DevCsr& a, const double* x, double* y
 // (csr.cpp:107-110: acc = acc + v * x), so the result is bit-identical.
 constexpr int kRing = 16384;          // doubles (128 KB)
 constexpr int kRingBlock = 1024;      // threads = rows per tile
-constexpr int kRingStage = 256;       // CSR entries per warp chunk (8 per lane)
+constexpr int kRingStage = 128;       // CSR entries per warp chunk (4 per lane; 8 measured slower: registers)
 constexpr size_t kRingSmem = (size_t)kRing * 8 + (size_t)(kRingBlock / 32) * kRingStage * 8;
 
 template <int S, bool TRUE_RES>
@@ -390,10 +390,6 @@ __global__ void __launch_bounds__(kRingBlock, 1) k_spmv_ring(DevCsr a, const dou
       const int end = valid ? __ldg(rp + row + 1) : 0;
       const int wbeg = __shfl_sync(0xffffffffu, beg, 0);
       const int wend = __ldg(rp + last);
-      double pv[S];
-#pragma unroll
-      for (int c = 0; c < S; ++c) pv[c] = valid ? __ldg(p + c * ld + row) : 0.0;
-      const double bv = (TRUE_RES && valid) ? b[row] : 0.0;
       double acc = 0.0;
       // chunk loads are issued one chunk ahead: the next chunk's (value, column) pairs are in
       // flight while the lanes add up the current chunk's products
@@ -423,7 +419,13 @@ __global__ void __launch_bounds__(kRingBlock, 1) k_spmv_ring(DevCsr a, const dou
         __syncwarp();
       }
       if (valid) {
-        if (TRUE_RES) acc = bv - acc;
+        // P and b are read after the row sums: holding them across the chunk loop cost the
+        // summation the registers it needs to keep several shared-memory loads in flight
+        // (64 registers per thread at 1024 threads; ncu: short-scoreboard stalls dominate)
+        double pv[S];
+#pragma unroll
+        for (int c = 0; c < S; ++c) pv[c] = __ldg(p + c * ld + row);
+        if (TRUE_RES) acc = b[row] - acc;
         y[row] = acc;
 #pragma unroll
         for (int c = 0; c < S; ++c) part[c] = part[c] + pv[c] * acc;
