@@ -237,9 +237,12 @@ __device__ bool dev_lu_solve(int s, double* a, const double* rhs, double* x) {
 // dependent chain is ~s steps of a few shuffles (the earlier row-per-lane version needed an
 // argmax butterfly and a row broadcast per step: ~7 us at s = 8). The substitutions run on lane 0
 // from shared memory. Call with all 32 lanes; a (col-major), rhs, x live in shared memory.
-template <int MAXS>
-__device__ bool warp_lu_solve(int s, double* a, const double* rhs, double* x) {
+// FIXED: s == MAXS at compile time (the finalisers' case: S is dispatched from s), so every size
+// test folds away and the factorisation is straight-line code.
+template <int MAXS, bool FIXED>
+__device__ bool warp_lu_impl(int s_rt, double* a, const double* rhs, double* x) {
   constexpr unsigned FULL = 0xffffffffu;
+  const int s = FIXED ? MAXS : s_rt;
   const int lane = threadIdx.x & 31;
   const bool mine = lane < s;
   double col[MAXS];
@@ -261,6 +264,7 @@ __device__ bool warp_lu_solve(int s, double* a, const double* rhs, double* x) {
     // pivot search on column k (lane k), rows k.. in order: first strictly larger magnitude
     int piv = k;
     double best = fabs(col[k]);
+    double pval = col[k];
     if (lane == k) {
 #pragma unroll
       for (int i = k + 1; i < MAXS; ++i) {
@@ -269,10 +273,14 @@ __device__ bool warp_lu_solve(int s, double* a, const double* rhs, double* x) {
           if (m > best) {
             best = m;
             piv = i;
+            pval = col[i];
           }
         }
       }
     }
+    // the pivot's reciprocal (the same 1 / a_kk the reference forms after the swap) is started on
+    // the pivot lane before the broadcasts, off the shuffle chain
+    const double inv = 1.0 / pval;
     piv = __shfl_sync(FULL, piv, k);
     best = __shfl_sync(FULL, best, k);
     if (best < 1e-14 * scale || scale == 0.0) return false;
@@ -295,7 +303,6 @@ __device__ bool warp_lu_solve(int s, double* a, const double* rhs, double* x) {
     }
     // multipliers m_i = a_ik * (1 / a_kk), stored in place (L), by the pivot-column lane
     if (lane == k) {
-      const double inv = 1.0 / col[k];
 #pragma unroll
       for (int i = k + 1; i < MAXS; ++i)
         if (i < s) col[i] = col[i] * inv;
@@ -338,6 +345,12 @@ __device__ bool warp_lu_solve(int s, double* a, const double* rhs, double* x) {
   }
   __syncwarp();
   return true;
+}
+
+template <int MAXS>
+__device__ bool warp_lu_solve(int s, double* a, const double* rhs, double* x) {
+  if (s == MAXS) return warp_lu_impl<MAXS, true>(s, a, rhs, x);
+  return warp_lu_impl<MAXS, false>(s, a, rhs, x);
 }
 
 __device__ void set_breakdown(DevState* ds, int code, int mv) {
