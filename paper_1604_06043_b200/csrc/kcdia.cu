@@ -56,15 +56,31 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
                               : __ldg(static_cast<const uint32_t*>(a.dia_mask) + r));
   };
   const int32_t rstride = gridDim.x * blockDim.x;
+  const int32_t row0 = blockIdx.x * blockDim.x + threadIdx.x;
+  // The masks never change and, inside a cycle, neither do P and b: the first row's mask, P row
+  // and b are loaded before waiting on the producer of x (programmatic dependent launch), so that
+  // DRAM round trip overlaps the predecessor's tail. A plain product (kFinStore) may pass a
+  // producer-written vector as p, so it loads after the wait.
+  const bool early = fin.op != kFinStore;
+  uint32_t mnext = load_mask(row0);
+  double pv[S];
+  double bv = 0.0;
+  if (early && row0 < (int32_t)n) {
+#pragma unroll
+    for (int c = 0; c < S; ++c) pv[c] = __ldg(p + c * ld + row0);
+    if (TRUE_RES) bv = __ldg(b + row0);
+  }
   pdl_wait();
-  uint32_t mnext = load_mask(blockIdx.x * blockDim.x + threadIdx.x);
-  for (int32_t row = blockIdx.x * blockDim.x + threadIdx.x; row < (int32_t)n; row += rstride) {
+  bool first = early;
+  for (int32_t row = row0; row < (int32_t)n; row += rstride) {
     const uint32_t m = mnext;
     mnext = load_mask(row + rstride);
-    double pv[S];
+    if (!first) {
 #pragma unroll
-    for (int c = 0; c < S; ++c) pv[c] = __ldg(p + c * ld + row);
-    const double bv = TRUE_RES ? __ldg(b + row) : 0.0;
+      for (int c = 0; c < S; ++c) pv[c] = __ldg(p + c * ld + row);
+      if (TRUE_RES) bv = __ldg(b + row);
+    }
+    first = false;
     double acc = 0.0;
     if (ND > 0) {
       double xv[ND > 0 ? ND : 1];
