@@ -69,8 +69,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// 4 CTAs per SM (64 registers) at S = 6..8: kbench c2 (S = 8) 26.7 -> 26.3 us, 0.80 -> 0.83 in the
+// sequence; at S = 4 (c5) the register cap measured slower (116 -> 122 us), so other S keep the default.
 template <int S>
-__global__ void __launch_bounds__(kBlock) k_rebuild_top(int64_t n, int64_t ld, int q,
+__global__ void __launch_bounds__(kBlock, (S >= 6 && S <= 8) ? 4 : 1) k_rebuild_top(int64_t n, int64_t ld, int q,
                                                         const double* __restrict__ rnext,
                                                         const double* __restrict__ vk_in,
                                                         double* __restrict__ vk_out,
