@@ -185,8 +185,9 @@ uint64_t mstab_operator_fingerprint(const mstab_operator* op); /* operator.cpp:3
 int mstab_operator_apply(mstab_context* ctx, const mstab_operator* op, const double* x, double* y,
                          int32_t mem);
 /* y = A^H x (CsrOperator::apply_adjoint, operator.cpp:30-33 -> spmv_adjoint csr.cpp:115-124),
- * bit-identical for real data. A^H is built once per operator on first use. ConfigError for a
- * preconditioned operator or a row slab. */
+ * bit-identical for real data; for a preconditioned operator (L^-1 A R^-1)^H = R^-H A^H L^-H
+ * (PreconditionedOperator::apply_adjoint, precond.cpp:190-200), bit-identical to the reference's
+ * adjoint solves. Built once per operator on first use. ConfigError for a row slab. */
 int mstab_operator_apply_adjoint(mstab_context* ctx, const mstab_operator* op, const double* x, double* y,
                                  int32_t mem);
 

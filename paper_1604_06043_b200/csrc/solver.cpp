@@ -1371,33 +1371,94 @@ void baseline_finish(Context& ctx, BaselineStart& s0, int64_t it, double resnorm
 // kernel accumulates a row from +0.0 in CSR order: the device product is bit-identical to the
 // reference's scatter. The transpose goes through the normal upload, so a stencil's transpose gets
 // the same constant-diagonal / DIA forms. Built once per operator, on first use.
+namespace {
+
+struct HostCsr {
+  std::vector<int64_t> rp, ci;
+  std::vector<double> val;
+};
+
+HostCsr download_csr(Context& ctx, int64_t n, int64_t nnz, const void* rp_d, const void* ci_d, const double* val_d) {
+  std::vector<int32_t> rp(n + 1), ci(std::max<int64_t>(nnz, 1));
+  HostCsr h;
+  h.val.resize(std::max<int64_t>(nnz, 1));
+  cudaStream_t st = ctx.stream();
+  CUDA_OK(cudaMemcpyAsync(rp.data(), rp_d, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+  if (nnz > 0) {
+    CUDA_OK(cudaMemcpyAsync(ci.data(), ci_d, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(h.val.data(), val_d, sizeof(double) * nnz, cudaMemcpyDeviceToHost, st));
+  }
+  ctx.sync();
+  h.rp.assign(rp.begin(), rp.end());
+  h.ci.assign(ci.begin(), ci.begin() + std::max<int64_t>(nnz, 0));
+  return h;
+}
+
+// Transpose (real data: the conjugate transpose) with row j listing its entries in the order the
+// reference's scatter loops add them into x[j]: source rows ascending, or descending when
+// `descending` (lower_solve_adjoint walks L's rows back to front, precond.cpp:129-143).
+HostCsr transpose(int64_t n, const HostCsr& a, bool descending) {
+  const int64_t nnz = a.rp[n];
+  HostCsr t;
+  t.rp.assign(n + 1, 0);
+  t.ci.resize(std::max<int64_t>(nnz, 1));
+  t.val.resize(std::max<int64_t>(nnz, 1));
+  for (int64_t k = 0; k < nnz; ++k) ++t.rp[a.ci[k] + 1];
+  for (int64_t j = 0; j < n; ++j) t.rp[j + 1] += t.rp[j];
+  std::vector<int64_t> fill(t.rp.begin(), t.rp.end() - 1);
+  for (int64_t s = 0; s < n; ++s) {
+    const int64_t i = descending ? n - 1 - s : s;
+    for (int64_t k = a.rp[i]; k < a.rp[i + 1]; ++k) {
+      const int64_t at = fill[a.ci[k]]++;
+      t.ci[at] = i;
+      t.val[at] = a.val[k];
+    }
+  }
+  return t;
+}
+
+}  // namespace
+
+// A^H of an operator as a second operator (real data: A^T), built once on first use.
+// CSR: spmv_adjoint scatters y[col] += conj(a_ik) x_i over rows i ascending and entries k in CSR
+// order (csr.cpp:115-124), so y_j is the sum, from +0.0, of its terms in (i, k) order; the
+// transpose lists row j's entries in exactly that order and every SpMV kernel accumulates a row
+// from +0.0 in CSR order: bit-identical to the reference's scatter. The transpose goes through
+// the normal upload, so a stencil's transpose gets the same constant-diagonal / DIA forms.
+// Preconditioned (precond.cpp:190-200): (L^-1 A R^-1)^H = R^-H A^H L^-H. lower_solve_adjoint is
+// x_j = (b_j - sum over rows i > j, descending, of l_ij x_i) / l_jj and upper_solve_adjoint the
+// same over rows i < j ascending: exactly upper_solve / lower_solve on the transposed factors with
+// those entry orders, so the adjoint chain reuses the triangular-solve kernels (the upper solve
+// first, like the forward chain) and stays bit-identical. Diagonal factors are their own adjoint.
 const Operator& adjoint_of(Context& ctx, const Operator& op) {
   std::lock_guard<std::mutex> lk(op.adj_mu);
   if (op.adj) return *op.adj;
-  if (op.pc) throw Error(MSTAB_E_CONFIG, "b200: apply_adjoint of a preconditioned operator is not supported");
   if (op.n_global != op.n) throw Error(MSTAB_E_CONFIG, "b200: apply_adjoint of a row slab is not supported");
-  const int64_t n = op.n, nnz = op.nnz;
-  std::vector<int32_t> rp(n + 1), ci(std::max<int64_t>(nnz, 1));
-  std::vector<double> val(std::max<int64_t>(nnz, 1));
-  cudaStream_t st = ctx.stream();
-  CUDA_OK(cudaMemcpyAsync(rp.data(), op.rp->ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
-  if (nnz > 0) {
-    CUDA_OK(cudaMemcpyAsync(ci.data(), op.ci->ptr, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, st));
-    CUDA_OK(cudaMemcpyAsync(val.data(), op.val->ptr, sizeof(double) * nnz, cudaMemcpyDeviceToHost, st));
+  const int64_t n = op.n;
+  const HostCsr a = download_csr(ctx, n, op.nnz, op.rp->ptr, op.ci->ptr, op.val->d());
+  const HostCsr at = transpose(n, a, false);
+  auto adj = make_operator(ctx, n, at.rp.data(), at.ci.data(), at.val.data());
+  if (op.pc) {
+    const Precond& pc = *op.pc;
+    auto apc = std::make_shared<Precond>();
+    apc->kind = pc.kind;
+    auto factor_t = [&](const DevTri& f, bool desc, bool lower, DevPtr& d_rp, DevPtr& d_ci, DevPtr& d_val,
+                        DevPtr& d_diag, DevPtr& d_ord) -> DevTri {
+      if (f.diag) return f;  // diagonal: its own adjoint (the device memory stays owned by `op`)
+      const HostCsr h = download_csr(ctx, n, f.nnz, f.rp, f.ci, f.val);
+      const HostCsr t = transpose(n, h, desc);
+      return upload_factor(ctx, n, t.rp.data(), t.ci.data(), t.val.data(), lower, d_rp, d_ci, d_val, d_diag, d_ord);
+    };
+    // the chain solves with R first (upper), then L (lower): R slot <- L^T, L slot <- R^T
+    apc->R = factor_t(pc.L, true, false, apc->r_rp, apc->r_ci, apc->r_val, apc->r_diag, apc->r_ord);
+    apc->L = factor_t(pc.R, false, true, apc->l_rp, apc->l_ci, apc->l_val, apc->l_diag, apc->l_ord);
+    apc->t1 = ctx.alloc_vecs(n, 1);
+    apc->t2 = ctx.alloc_vecs(n, 1);
+    apc->t3 = ctx.alloc_vecs(n, 1);
+    apc->sync = ctx.alloc(sizeof(int) * (size_t)(n + 1));
+    adj->pc = apc;
   }
-  ctx.sync();
-  std::vector<int64_t> trp(n + 1, 0), tci(std::max<int64_t>(nnz, 1));
-  std::vector<double> tval(std::max<int64_t>(nnz, 1));
-  for (int64_t k = 0; k < nnz; ++k) ++trp[ci[k] + 1];
-  for (int64_t j = 0; j < n; ++j) trp[j + 1] += trp[j];
-  std::vector<int64_t> fill(trp.begin(), trp.end() - 1);
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
-      const int64_t at = fill[ci[k]]++;
-      tci[at] = i;
-      tval[at] = val[k];  // conj of a real value
-    }
-  op.adj = make_operator(ctx, n, trp.data(), tci.data(), tval.data());
+  op.adj = adj;
   return *op.adj;
 }
 
