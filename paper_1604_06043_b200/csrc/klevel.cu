@@ -146,7 +146,7 @@ struct DeferredArgs {
 // Deferred lower levels of level k (see kernels.h). Level k is final; levels i = k-1 .. -1 are
 // rebuilt top-down, each needing only level i+1 (final) and level i (being updated in q order).
 template <int S>
-__global__ void __launch_bounds__(kBlock, S <= 8 ? 4 : 3) k_rebuild_deferred(int64_t n, int64_t ld, int k,
+__global__ void __launch_bounds__(kBlock, S <= 8 ? 4 : 1) k_rebuild_deferred(int64_t n, int64_t ld, int k,
                                                              DeferredArgs a, DevState* ds) {
   pdl_wait();
   __shared__ double et[S * S];

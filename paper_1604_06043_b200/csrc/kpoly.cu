@@ -94,7 +94,7 @@ __device__ void poly_tail(const double* redv, DevState* ds) {
 // POLY = false: prologue (reductions of the given V and r only).
 // Slots: [0] ||r||^2, [1..S] P^H r, [1+S ..] P^H V (col-major s x s).
 template <int S, bool POLY>
-__global__ void __launch_bounds__(kBlock, S <= 8 ? 3 : 2) k_poly(int64_t n, int64_t ld, int ell, PolyArgs a,
+__global__ void __launch_bounds__(kBlock, S <= 8 ? 3 : 1) k_poly(int64_t n, int64_t ld, int ell, PolyArgs a,
                                                  Reducer red) {
   DevState* ds = red.ds;
   pdl_wait();
