@@ -302,16 +302,21 @@ def run_b200(args):
             "bytes_per_launch": s.total_bytes / s.launches, "achieved_gbs": round(gbs, 1),
             "frac": round(gbs / hbm, 4), "share_of_kernel_time": round(s.total_ms / total_ms, 4)}
     dom = "spmv_ph"
-    traffic = None
+    traffic = ncu_us = None
     if NCU_FILE.exists():
         try:
-            traffic = json.loads(NCU_FILE.read_text()).get(args.config, {}).get(dom)
+            rec = json.loads(NCU_FILE.read_text()).get(args.config, {})
+            traffic, ncu_us = rec.get(dom), rec.get(dom + "_us")
         except Exception:
-            traffic = None
+            traffic = ncu_us = None
+    bpl = kernels.get(dom, {}).get("bytes_per_launch")
     roof = {"bound": "hbm", "kernel": dom, "achieved": kernels.get(dom, {}).get("achieved_gbs"),
             "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
             "frac": kernels.get(dom, {}).get("frac"), "traffic": traffic,
-            "bytes_per_launch": kernels.get(dom, {}).get("bytes_per_launch")}
+            "bytes_per_launch": bpl}
+    if ncu_us and bpl:  # the same algorithmic bytes over the committed ncu launch duration (profiles/)
+        roof["ncu"] = {"us": ncu_us, "frac": round(bpl / (ncu_us * 1e-6) / (hbm * 1e9), 4),
+                       "source": "profiles/ncu_traffic.json"}
 
     mean_cycles = float(np.mean([r["cycles"] for r in timed])) if timed else None
     cpu = None
