@@ -131,7 +131,13 @@ typedef struct mstab_validation_report {
 
 /* ---- library / context -------------------------------------------------------------------- */
 const char* mstab_last_error(void);
+/* Row of the last MSTAB_E_ZEROPIVOT on this thread (ZeroPivot::row(), errors.hpp:39-45), -1 when
+ * the last error carried no row. */
+int64_t mstab_last_error_row(void);
 const char* mstab_impl_name(void); /* "b200" or "reference" */
+/* Build provenance: "<impl> <git sha>[-dirty] <compiler flags>", fixed at compile time, so every
+ * bench line / smoke record names the binary it ran. */
+const char* mstab_build_id(void);
 
 /* Binds a device and creates the solver's CUDA stream. device < 0 selects the current device. */
 int mstab_context_create(int32_t device, mstab_context** out);

@@ -38,6 +38,11 @@ int mstab_kernel_arnoldi(mstab_context* ctx, const mstab_operator* op, const dou
 int mstab_kernel_bench(mstab_context* ctx, const mstab_operator* op, int32_t kind, int64_t s,
                        int64_t ell, int32_t iters, double* us, double* bytes);
 
+/* Developer probes: op 0 resets and binds the in-kernel timeline slots, op 1 unbinds and copies
+ * the 32 slots to out (globaltimer ns / clock64). Only a timeline build (make timeline) records;
+ * the product build leaves out untouched. (Reference implementation: MSTAB_E_CONFIG.) */
+int mstab_timeline(mstab_context* ctx, int32_t op, uint64_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,6 +43,7 @@ struct mstab_result {
 namespace {
 
 thread_local std::string g_err;
+thread_local int64_t g_row = -1;
 
 struct ConfigErr : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -53,6 +54,7 @@ struct NotRealErr : std::runtime_error {
 
 template <typename F>
 int guarded(F&& f) {
+  g_row = -1;
   try {
     f();
     return MSTAB_OK;
@@ -85,6 +87,7 @@ int guarded(F&& f) {
     return MSTAB_E_MISSING_OMEGAS;
   } catch (const mstab::ZeroPivot& e) {
     g_err = e.what();
+    g_row = (int64_t)e.row();
     return MSTAB_E_ZEROPIVOT;
   } catch (const mstab::Error& e) {
     g_err = e.what();
@@ -151,7 +154,9 @@ void from_dense(const mstab::DenseMatrix& m, double* out) {
 extern "C" {
 
 const char* mstab_last_error(void) { return g_err.c_str(); }
+int64_t mstab_last_error_row(void) { return g_row; }
 const char* mstab_impl_name(void) { return "reference"; }
+const char* mstab_build_id(void) { return "reference (unmodified /root/reference sources, oracle/Makefile)"; }
 
 int mstab_context_create(int32_t device, mstab_context** out) {
   return guarded([&] {
@@ -651,5 +656,10 @@ const char* mstab_kernel_class_name(int32_t) { return "?"; }
 extern "C" int mstab_kernel_bench(mstab_context*, const mstab_operator*, int32_t, int64_t, int64_t, int32_t,
                                   double*, double*) {
   g_err = "reference implementation: no kernels to benchmark";
+  return MSTAB_E_CONFIG;
+}
+
+extern "C" int mstab_timeline(mstab_context*, int32_t, uint64_t*) {
+  g_err = "reference implementation: no kernel timeline";
   return MSTAB_E_CONFIG;
 }

@@ -74,6 +74,8 @@ _I64 = C.POINTER(C.c_int64)
 ABI = [
     ("mstab_last_error", C.c_char_p, []),
     ("mstab_impl_name", C.c_char_p, []),
+    ("mstab_last_error_row", C.c_int64, []),
+    ("mstab_build_id", C.c_char_p, []),
     ("mstab_context_create", C.c_int, [C.c_int32, C.POINTER(_P)]),
     ("mstab_context_destroy", None, [_P]),
     ("mstab_context_synchronize", C.c_int, [_P]),
@@ -196,6 +198,7 @@ class Lib:
         _bind(self.dll, ABI)
         _bind(self.dll, KERNEL_ABI)
         self.name = self.dll.mstab_impl_name().decode()
+        self.build_id = self.dll.mstab_build_id().decode()
         cls._cache[path] = self
         return self
 

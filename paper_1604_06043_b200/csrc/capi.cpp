@@ -29,20 +29,32 @@ struct mstab_result {
 namespace {
 
 thread_local std::string g_last_error;
+thread_local int64_t g_last_row = -1;
+
+#ifndef MSTAB_GIT_SHA
+#define MSTAB_GIT_SHA "unknown"
+#endif
+#ifndef MSTAB_BUILD_FLAGS
+#define MSTAB_BUILD_FLAGS ""
+#endif
 
 template <typename F>
 int guarded(F&& f) {
+  g_last_row = -1;
   try {
     f();
     return MSTAB_OK;
   } catch (const Error& e) {
     g_last_error = e.what();
+    g_last_row = e.row;
     return e.code;
   } catch (const std::bad_alloc&) {
     g_last_error = "out of host memory";
+    g_last_row = -1;
     return MSTAB_E_ERROR;
   } catch (const std::exception& e) {
     g_last_error = e.what();
+    g_last_row = -1;
     return MSTAB_E_ERROR;
   }
 }
@@ -57,7 +69,9 @@ void bind(mstab_context* ctx) {
 extern "C" {
 
 const char* mstab_last_error(void) { return g_last_error.c_str(); }
+int64_t mstab_last_error_row(void) { return g_last_row; }
 const char* mstab_impl_name(void) { return "b200"; }
+const char* mstab_build_id(void) { return "b200 " MSTAB_GIT_SHA " " MSTAB_BUILD_FLAGS; }
 
 int mstab_context_create(int32_t device, mstab_context** out) {
   return guarded([&] {
@@ -739,6 +753,18 @@ int mstab_kernel_bench(mstab_context* ctx, const mstab_operator* op, int32_t kin
         case 7:  // the s x s LU solve alone (one warp): latency of the finalizers' dense step
           launch_small_solve(st, s, ds->Ma, ds->rhs, ds->scal, reinterpret_cast<int32_t*>(ds->scal + 32));
           break;
+        case 8: {  // the column-loop pair: SpMV of column q (P^H + LU for eta_{q+1}), then rebuild q+1
+          const int q = s / 2 - 1 < 0 ? 0 : s / 2 - 1;
+          FinParams f;
+          f.op = kFinColEta;
+          f.s = s;
+          f.ell = ell;
+          f.k = 0;
+          f.q = q;
+          launch_spmv_ph(st, csr, B.V->d() + q * ld, VL[1]->d() + q * ld, P->d(), ld, s, nullptr, f, red);
+          launch_rebuild_top(st, n, ld, s, q + 1, R[1]->d(), A.V->d(), B.V->d(), VL[1]->d(), ds);
+          break;
+        }
         default:
           throw Error(MSTAB_E_CONFIG, "bench: unknown kind");
       }
@@ -772,6 +798,27 @@ int mstab_kernel_bench(mstab_context* ctx, const mstab_operator* op, int32_t kin
     if (cudaGetLastError() != cudaSuccess) throw Error(MSTAB_E_CUDA, "bench launch failed");
     *us = 1e3 * ms / iters;
     *bytes = b1;
+  });
+}
+
+// Developer probes (ktimeline.cuh): with a timeline build, bind a 32-slot device buffer, run one
+// kernel_bench kind, then read the slots (globaltimer ns / clock64). Product build: no-op + 0.
+int mstab_timeline(mstab_context* ctx, int32_t op, uint64_t* out) {
+  return guarded([&] {
+    bind(ctx);
+    static unsigned long long* buf = nullptr;
+    if (!buf) cudaMalloc(&buf, 32 * sizeof(unsigned long long));
+    if (op == 0) {  // reset + bind
+      std::vector<unsigned long long> init(32, 0ull);
+      for (int i = 0; i < 32; i += 2) init[i] = ~0ull;  // even slots are minima
+      cudaMemcpy(buf, init.data(), 32 * sizeof(unsigned long long), cudaMemcpyHostToDevice);
+      kcdia_timeline_bind(buf);
+      klevel_timeline_bind(buf);
+    } else if (op == 1) {  // unbind + read
+      kcdia_timeline_bind(nullptr);
+      klevel_timeline_bind(nullptr);
+      cudaMemcpy(out, buf, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    }
   });
 }
 

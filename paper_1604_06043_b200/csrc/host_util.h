@@ -13,7 +13,8 @@ namespace mstab_b200 {
 // Error carrying the C-ABI code of the reference exception class it stands for (errors.hpp).
 struct Error : std::runtime_error {
   int code;
-  Error(int c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+  int64_t row = -1;  // ZeroPivot::row() (errors.hpp:39-45) for MSTAB_E_ZEROPIVOT
+  Error(int c, const std::string& msg, int64_t r = -1) : std::runtime_error(msg), code(c), row(r) {}
 };
 
 // FNV-1a over the reference CsrMatrix byte layout (csr.cpp:28-43): dims {n_rows, n_cols, nnz}

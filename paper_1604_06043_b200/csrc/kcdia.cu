@@ -4,6 +4,7 @@
 #include <type_traits>
 
 #include "kcommon.cuh"
+#include "ktimeline.cuh"
 
 namespace mstab_b200 {
 
@@ -62,6 +63,10 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
   // DRAM round trip overlaps the predecessor's tail. A plain product (kFinStore) may pass a
   // producer-written vector as p, so it loads after the wait.
   const bool early = fin.op != kFinStore;
+  if (threadIdx.x == 0) {
+    TL_MIN(0);
+    TL_MAX(1);
+  }
   uint32_t mnext = load_mask(row0);
   double pv[S];
   double bv = 0.0;
@@ -71,6 +76,10 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
     if (TRUE_RES) bv = __ldg(b + row0);
   }
   pdl_wait();
+  if (threadIdx.x == 0) {
+    TL_MIN(2);
+    TL_MAX(3);
+  }
   bool first = early;
   for (int32_t row = row0; row < (int32_t)n; row += rstride) {
     const uint32_t m = mnext;
@@ -114,9 +123,26 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
   __shared__ FinStage fs;
   if (!red.xred) fin_prestage(fin, ds, fs);
   block_totals<NS>(part, blk, scratch);
+  if (threadIdx.x == 0) {
+    TL_MIN(4);
+    TL_MAX(5);
+  }
   if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv, red.xred)) return;
+  if (threadIdx.x == 0) {
+    TL_SET(7);
+    TL_CLK(11);
+  }
   finalize_spmv<S>(fin, redv, ds, fs);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    TL_SET(9);
+    TL_CLK(13);
+  }
 }
+
+}  // namespace
+TL_BIND_FN(kcdia_timeline_bind)
+namespace {
 
 template <int S, bool TRUE_RES, int ND>
 void launch_cdia_nd(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,

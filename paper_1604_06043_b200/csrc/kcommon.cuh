@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "kernels.h"
+#include "ktimeline.cuh"
 
 namespace mstab_b200 {
 
@@ -114,6 +115,10 @@ __device__ bool cta_commit(const double* blk, int nslots, double* partials, uint
   if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == (uint32_t)(G - 1));
   __syncthreads();
   if (!s_last) return false;
+  if (threadIdx.x == 0) {
+    TL_SET(6);
+    TL_CLK(10);
+  }
   __threadfence();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   // This reduction is on the critical path of every fused dense step (the whole grid waits for
@@ -443,7 +448,11 @@ __device__ void finalize_spmv(const FinParams& f, const double* red, DevState* d
   if (!solve) return;
   if (t < 32) {
     const bool r = warp_lu_solve<MAXS>(s, fs.lu, fs.vin, fs.vout);
-    if (t == 0) fs.ok = r ? 1 : 0;
+    if (t == 0) {
+      fs.ok = r ? 1 : 0;
+      TL_SET(8);
+      TL_CLK(12);
+    }
   }
   __syncthreads();
   if (t < s) dst[t] = fs.vout[t];

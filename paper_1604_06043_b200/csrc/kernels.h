@@ -118,6 +118,9 @@ void prof_release(std::vector<ProfEvent>& list);  // return a destroyed graph's 
 void prof_enable(bool on);
 void prof_collect();  // folds completed events into the per-class totals (call after a sync)
 void prof_read(KernelClassStats* out);  // kKNumClasses entries
+// ktimeline.cuh probes (no-ops unless built with MSTAB_TIMELINE): bind the slot buffer per TU
+void kcdia_timeline_bind(unsigned long long* p);
+void klevel_timeline_bind(unsigned long long* p);
 void prof_reset();
 
 // ---- the Mstab cycle ----------------------------------------------------------------------

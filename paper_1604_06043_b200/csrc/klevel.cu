@@ -84,6 +84,10 @@ __global__ void __launch_bounds__(kBlock, (S >= 6 && S <= 8) ? 4 : 1) k_rebuild_
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const bool first = early && pr0 < npair && 2 * pr0 + 1 < n;
   const int t = threadIdx.x, bd = blockDim.x;
+  if (t == 0) {
+    TL_MIN(16);
+    TL_MAX(17);
+  }
   if (first) {
     const int64_t row = 2 * pr0;
     if (q > 0) cp_async16(&pre[S * bd + t], rnext + row);
@@ -92,6 +96,10 @@ __global__ void __launch_bounds__(kBlock, (S >= 6 && S <= 8) ? 4 : 1) k_rebuild_
       if (c != q - 1) cp_async16(&pre[c * bd + t], ((c < q) ? vk1 : vk_in) + c * ld + row);
   }
   pdl_wait();
+  if (t == 0) {
+    TL_MIN(18);
+    TL_MAX(19);
+  }
   double et[S];
 #pragma unroll
   for (int c = 0; c < S; ++c) et[c] = ds->eta[q * S + c];
@@ -132,7 +140,15 @@ __global__ void __launch_bounds__(kBlock, (S >= 6 && S <= 8) ? 4 : 1) k_rebuild_
       vk_out[q * ld + row] = nc;
     }
   }
+  if (t == 0) {
+    TL_MIN(20);
+    TL_MAX(21);
+  }
 }
+
+}  // namespace
+TL_BIND_FN(klevel_timeline_bind)
+namespace {
 
 struct DeferredArgs {
   const double* lv_in[kMaxEll + 2];

@@ -196,6 +196,7 @@ template <int S>
 __global__ void __launch_bounds__(kBlock) k_fin_poly(DevState* ds) {
   constexpr int NSL = 1 + S + S * S;
   __shared__ double redv[NSL];
+  pdl_wait();  // ds->xred is written by the collective that precedes this launch
   for (int i = threadIdx.x; i < NSL; i += blockDim.x) redv[i] = ds->xred[i];
   __syncthreads();
   poly_tail<S>(redv, ds);

@@ -473,6 +473,7 @@ template <int S>
 __global__ void __launch_bounds__(kBlock) k_fin_spmv(FinParams fin, DevState* ds) {
   __shared__ double redv[S + 1];
   __shared__ FinStage fs;
+  pdl_wait();  // ds->xred is written by the collective that precedes this launch
   if (threadIdx.x <= S) redv[threadIdx.x] = ds->xred[threadIdx.x];
   fin_prestage(fin, ds, fs);
   __syncthreads();

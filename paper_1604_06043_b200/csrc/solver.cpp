@@ -723,7 +723,7 @@ void precond_build(int kind, int64_t n, const int64_t* row_ptr, const int64_t* c
       double d = 0.0;
       for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k)
         if (col_idx[k] == i) d = values[k];
-      if (std::abs(d) < 1e-14 * scale || scale == 0.0) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(i));
+      if (std::abs(d) < 1e-14 * scale || scale == 0.0) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(i), i);
       // std::sqrt of a complex with a negative real part is imaginary: not a real operator
       if (d < 0.0) throw Error(MSTAB_E_NOTREAL, "jacobi: negative diagonal gives a complex square root");
       lrows[i].push_back({i, std::sqrt(d)});
@@ -736,13 +736,13 @@ void precond_build(int kind, int64_t n, const int64_t* row_ptr, const int64_t* c
       for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k)
         if (col_idx[k] == i) diag_pos[i] = k;
     for (int64_t i = 0; i < n; ++i)
-      if (diag_pos[i] < 0) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(i));
+      if (diag_pos[i] < 0) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(i), i);
     for (int64_t i = 0; i < n; ++i) {
       for (int64_t ki = row_ptr[i]; ki < row_ptr[i + 1]; ++ki) {
         const int64_t k = col_idx[ki];
         if (k >= i) break;
         const double piv = val[diag_pos[k]];
-        if (std::abs(piv) < 1e-14 * scale || scale == 0.0) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(k));
+        if (std::abs(piv) < 1e-14 * scale || scale == 0.0) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(k), k);
         const double lik = val[ki] / piv;
         val[ki] = lik;
         int64_t pk = diag_pos[k] + 1, pi = ki + 1;
@@ -758,7 +758,7 @@ void precond_build(int kind, int64_t n, const int64_t* row_ptr, const int64_t* c
           }
         }
       }
-      if (std::abs(val[diag_pos[i]]) < 1e-14 * scale || scale == 0.0) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(i));
+      if (std::abs(val[diag_pos[i]]) < 1e-14 * scale || scale == 0.0) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(i), i);
     }
     // unit lower L (explicit 1.0 diagonal, last in its row) and upper R carrying the pivots
     for (int64_t i = 0; i < n; ++i) {
@@ -791,7 +791,7 @@ std::shared_ptr<Operator> make_operator_precond(Context& ctx, int64_t n, const i
     bool dl = false, dr = false;
     for (int64_t k = l_rp[i]; k < l_rp[i + 1]; ++k) dl = dl || (l_ci[k] == i && l_val[k] != 0.0);
     for (int64_t k = r_rp[i]; k < r_rp[i + 1]; ++k) dr = dr || (r_ci[k] == i && r_val[k] != 0.0);
-    if (!dl || !dr) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(i));
+    if (!dl || !dr) throw Error(MSTAB_E_ZEROPIVOT, zero_pivot(i), i);
   }
   // PreconditionedOperator::fingerprint (precond.cpp:203-210)
   uint64_t h = op->fingerprint;
@@ -1073,9 +1073,9 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
     arnoldi_init(ctx, op, c0.r->d(), s, cfg.seed ^ 0x9e3779b97f4a7c15ull, c0.U->d(), c0.V->d());
     rep.h_mv += s;
   }
-  if (w.p_src != P->ptr) {  // the graphs read P from the workspace copy
+  if (w.p_src != P) {  // the graphs read P from the workspace copy
     CUDA_OK(cudaMemcpyAsync(w.P->ptr, P->ptr, sizeof(double) * ld * s, cudaMemcpyDeviceToDevice, st));
-    w.p_src = P->ptr;
+    w.p_src = P;
   }
 
   // P^H V, P^H r, ||r|| and gamma_0 of the first cycle
@@ -1209,9 +1209,9 @@ std::unique_ptr<SolveResultImpl> sridr(Context& ctx, const Operator& op, const d
     check_launch();
     rep.h_mv_aux++;
   }
-  if (w.p_src != rc.p->ptr) {
+  if (w.p_src != rc.p) {
     CUDA_OK(cudaMemcpyAsync(w.P->ptr, rc.p->ptr, sizeof(double) * ld * s, cudaMemcpyDeviceToDevice, st));
-    w.p_src = rc.p->ptr;
+    w.p_src = rc.p;
   }
   const double* P = w.P->d();
   // P^H V (kept in ds->Ma for the whole recycled phase), P^H r, ||r||, gamma = (P^H V)^-1 P^H r

@@ -65,7 +65,9 @@ struct Workspace {
   WSet set[2];
   std::vector<DevPtr> R, VL;  // r^(1..ell), V^(1..ell)
   DevPtr b, P;
-  const void* p_src = nullptr;  // device buffer P was last copied from
+  // the buffer P was last copied from, held so its address cannot be recycled by the pool while
+  // the copy is trusted (a freed-and-reallocated P at the same address must be copied again)
+  DevPtr p_src;
   CycleGraph graph[2];          // graph[p]: set[p] -> set[1-p]
 };
 

@@ -70,7 +70,8 @@ class NotReal(ConfigError):
 
 
 class ZeroPivot(Error):
-    """errors.hpp:39-45 (build_jacobi / build_ilu0)."""
+    """errors.hpp:39-45 (build_jacobi / build_ilu0); `row` is ZeroPivot::row()."""
+    row: int = -1
 
 
 class MissingOmegas(Error):
@@ -84,7 +85,10 @@ _ERR = {-1: Error, -2: DimensionMismatch, -3: ConfigError, -4: FingerprintMismat
 
 def _check(lib: Lib, rc: int):
     if rc != 0:
-        raise _ERR.get(rc, Error)(lib.last_error())
+        e = _ERR.get(rc, Error)(lib.last_error())
+        if rc == -10:
+            e.row = int(lib.dll.mstab_last_error_row())
+        raise e
 
 
 # ---- config / report (report.hpp) -------------------------------------------------------------
@@ -291,12 +295,36 @@ def _f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
-def _dev_ptr(a):
-    """(pointer, mem) for a numpy array or a CUDA tensor."""
-    if hasattr(a, "__cuda_array_interface__"):
-        return a.__cuda_array_interface__["data"][0], _capi.MEM_DEVICE
+def _dev_ptr(a, n=None, ctx=None, what="vector"):
+    """(pointer, mem) for a numpy array (pointer None: the caller converts it) or a CUDA array.
+
+    A device array must be a contiguous float64 vector of `n` entries (the C-ABI takes a raw
+    pointer, so a float32 or short tensor would be read out of bounds). When `ctx` is given the
+    library's stream is ordered after torch's current stream, so a vector that a torch kernel is
+    still producing is not read early (the library syncs its own stream before returning)."""
+    if a is None:
+        return None, _capi.MEM_HOST
     if hasattr(a, "is_cuda") and a.is_cuda:
+        import torch
+        if a.dtype != torch.float64:
+            raise ConfigError(f"{what}: device tensor must be float64, got {a.dtype}")
+        if not a.is_contiguous():
+            raise ConfigError(f"{what}: device tensor must be contiguous")
+        if n is not None and a.numel() != n:
+            raise DimensionMismatch(f"{what}: {a.numel()} entries, expected {n}")
+        if ctx is not None and ctx.stream:
+            torch.cuda.ExternalStream(ctx.stream, device=a.device).wait_stream(torch.cuda.current_stream(a.device))
         return a.data_ptr(), _capi.MEM_DEVICE
+    if hasattr(a, "__cuda_array_interface__"):
+        cai = a.__cuda_array_interface__
+        if cai.get("typestr") != "<f8":
+            raise ConfigError(f"{what}: device array must be float64, got {cai.get('typestr')}")
+        if cai.get("strides") not in (None, (8,)):
+            raise ConfigError(f"{what}: device array must be contiguous")
+        cnt = int(np.prod(cai["shape"]))
+        if n is not None and cnt != n:
+            raise DimensionMismatch(f"{what}: {cnt} entries, expected {n}")
+        return cai["data"][0], _capi.MEM_DEVICE
     return None, _capi.MEM_HOST
 
 
@@ -399,9 +427,11 @@ class CsrOperator:
         return True
 
     def apply(self, x, y=None):
-        ptr, mem = _dev_ptr(x)
+        ptr, mem = _dev_ptr(x, self.size(), self.ctx, "spmv x")
         if mem == _capi.MEM_DEVICE:
-            yptr, _ = _dev_ptr(y)
+            yptr, ymem = _dev_ptr(y, self.size(), self.ctx, "spmv y")
+            if ymem != _capi.MEM_DEVICE:
+                raise ConfigError("spmv: x on the device needs a device output y")
             _check(self.lib, self.lib.dll.mstab_operator_apply(self.ctx.h, self.h, ptr, yptr, mem))
             return y
         x = _f64(x)
@@ -414,9 +444,11 @@ class CsrOperator:
 
     def apply_adjoint(self, x, y=None):
         """A^H x (CsrOperator::apply_adjoint, operator.cpp:30-33; spmv_adjoint csr.cpp:115-124)."""
-        ptr, mem = _dev_ptr(x)
+        ptr, mem = _dev_ptr(x, self.size(), self.ctx, "spmv_adjoint x")
         if mem == _capi.MEM_DEVICE:
-            yptr, _ = _dev_ptr(y)
+            yptr, ymem = _dev_ptr(y, self.size(), self.ctx, "spmv_adjoint y")
+            if ymem != _capi.MEM_DEVICE:
+                raise ConfigError("spmv_adjoint: x on the device needs a device output y")
             _check(self.lib, self.lib.dll.mstab_operator_apply_adjoint(self.ctx.h, self.h, ptr, yptr, mem))
             return y
         x = _f64(x)
@@ -653,8 +685,11 @@ class SolveResult:
 
     def x_into(self, dst) -> None:
         """Copy x into a CUDA tensor / host array without materialising it in Python."""
-        ptr, mem = _dev_ptr(dst)
+        ptr, mem = _dev_ptr(dst, self.n, self.ctx, "x")
         if mem == _capi.MEM_HOST:
+            if not (isinstance(dst, np.ndarray) and dst.dtype == np.float64 and dst.flags.c_contiguous
+                    and dst.size == self.n):
+                raise ConfigError("x_into: host destination must be a contiguous float64 array of n entries")
             ptr = dst.ctypes.data
         _check(self.lib, self.lib.dll.mstab_result_x(self.ctx.h, self.h, ptr, mem))
 
@@ -686,7 +721,7 @@ def idrstab_solve(a: CsrOperator, b, x0=None, cfg: Optional[SolverConfig] = None
     cfg = cfg if cfg is not None else SolverConfig()
     ctx, lib = a.ctx, a.lib
     n = a.size()
-    bptr, mem = _dev_ptr(b)
+    bptr, mem = _dev_ptr(b, n, ctx, "rhs")
     keep = []
     if mem == _capi.MEM_HOST:
         b = _f64(b)
@@ -697,13 +732,17 @@ def idrstab_solve(a: CsrOperator, b, x0=None, cfg: Optional[SolverConfig] = None
     xptr = None
     if x0 is not None and (not hasattr(x0, "__len__") or len(x0) > 0):
         if mem == _capi.MEM_HOST:
+            if _dev_ptr(x0)[1] == _capi.MEM_DEVICE:
+                raise ConfigError("idrstab: x0 is on the device but b is not (both must be in the same memory space)")
             x0 = _f64(x0)
             if x0.size != n:
                 raise DimensionMismatch("idrstab: guess size")
             keep.append(x0)
             xptr = x0.ctypes.data
         else:
-            xptr, _ = _dev_ptr(x0)
+            xptr, xmem = _dev_ptr(x0, n, ctx, "guess")
+            if xmem != _capi.MEM_DEVICE:
+                raise ConfigError("idrstab: b is on the device but x0 is not (both must be in the same memory space)")
     c = cfg._c()
     fp = None
     if fetch_policy is not None:

@@ -55,7 +55,11 @@ namespace {
     case MSTAB_E_SINGULAR: throw SingularProjection(msg);
     case MSTAB_E_RANK: throw RankDeficient(msg);
     case MSTAB_E_NOTREAL: throw ConfigError(msg);
-    case MSTAB_E_ZEROPIVOT: throw Error(msg);
+    case MSTAB_E_ZEROPIVOT: {  // ZeroPivot(row) builds its own message, like precond.cpp
+      const int64_t row = mstab_last_error_row();
+      if (row >= 0) throw ZeroPivot(static_cast<std::size_t>(row));
+      throw Error(msg);
+    }
     case MSTAB_E_MISSING_OMEGAS: throw MissingOmegas(msg);
     default: throw Error(msg);
   }

@@ -45,8 +45,11 @@ def test_zero_pivot_and_not_real_on_the_host():
     d = np.eye(6)
     d[3, 3] = 0.0
     a = m.CsrMatrix.from_dense(d + np.diag(np.ones(5), -1))
+    rows = []
     for lib in (prod, ref):
-        with pytest.raises(m.ZeroPivot):
+        with pytest.raises(m.ZeroPivot) as ei:
             m.build_ilu0(a, lib)
+        rows.append(ei.value.row)
+    assert rows[0] == rows[1] == 3  # ZeroPivot::row() carried through the C-ABI (errors.hpp:39-45)
     with pytest.raises(m.NotReal):
         m.build_jacobi(m.CsrMatrix.tridiag(1.0, -4.0, 1.0, 8), prod)
