@@ -88,7 +88,11 @@ class Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append([time.perf_counter()] + [c.strip() for c in line.split(",")])
+
+    def mark(self):
+        """Host time stamp for windowing the samples (perf_counter, like the rows)."""
+        return time.perf_counter()
 
     def __exit__(self, *a):
         if self.proc:
@@ -98,15 +102,19 @@ class Clocks:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
-        if not self.rows:
+    def summary(self, t0=None, t1=None):
+        """Median SM clock and throttle reasons of the samples taken inside [t0, t1] (the timed region;
+        the sampler itself is started before the warm-up so that nvidia-smi's start-up — which can stall
+        the device for 100+ ms — stays out of the timed region)."""
+        rows = [r[1:] for r in self.rows if (t0 is None or r[0] >= t0) and (t1 is None or r[0] <= t1 + 0.25)]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 # ---- the sequence driver (caller side of the hot path; reference harness.cpp:192-265) ----------
@@ -240,21 +248,23 @@ def run_b200(args):
     # ---- value: device-resident inputs -------------------------------------------------------
     seq = Sequence(m, cfg, op, ctx, seed=0, device_mode=True, torch=torch, rows=rows,
                    n_steps=args.warmup + 2 * args.steps + 1)
-    for _ in range(args.warmup):
-        seq.step()
-    barrier()
-    torch.cuda.synchronize()
-    ctx.synchronize()
-    lib.dll.mstab_profiling_reset()
-    lib.dll.mstab_profiling_enable(1 if args.profile == "timed" else 0)
-    l0 = lib.dll.mstab_launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
+    with Clocks(local) as clk:  # sampling from before the warm-up; only the timed window is summarised
+        for _ in range(args.warmup):
+            seq.step()
+        barrier()
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        lib.dll.mstab_profiling_reset()
+        lib.dll.mstab_profiling_enable(1 if args.profile == "timed" else 0)
+        l0 = lib.dll.mstab_launch_count()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk_t0 = clk.mark()
         ev0.record(stream)
         for _ in range(args.steps):
             seq.step()
         ev1.record(stream)
         ev1.synchronize()
+        clk_t1 = clk.mark()
     launches = int(lib.dll.mstab_launch_count() - l0)
     if args.profile == "after":  # per-kernel events on K more steps of the same sequence
         lib.dll.mstab_profiling_enable(1)
@@ -360,7 +370,7 @@ def run_b200(args):
                                                               f"halo + allreduce" if world > 1 else "single GPU"),
                            rhs_range=[args.warmup + 1, args.warmup + args.steps]),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "kernels": kernels,
+            "clocks": clk.summary(clk_t0, clk_t1), "kernels": kernels,
             "sequence": {"mean_cycles_per_rhs": mean_cycles, "restarts": seq.restarts,
                          "restarts_in_timed_window": timed_restarts,
                          "max_true_relres": max(r["relres"] for r in timed) if timed else None,

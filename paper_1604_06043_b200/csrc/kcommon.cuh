@@ -352,9 +352,134 @@ __device__ bool warp_lu_impl(int s_rt, double* a, const double* rhs, double* x) 
   return true;
 }
 
+// The fixed-size form the finalisers run (s == S at compile time). The dense step sits on the
+// critical path of every SpMV of the column loop (37 per cycle at c2), executed by ONE warp, so
+// what counts is that warp's instruction count and dependent chain (tools/ubench/lat.cu on sm_100a:
+// DADD/DMUL/DFMA 8 cycles, 1/x 61, x/y 112; the column-per-lane form above is ~2300 SASS
+// instructions at s = 8, issue-bound at ~6000 cycles, a fifth of them the selects of the row
+// swaps). Here lane i holds ROW i of the system (replicated in every S-wide segment of the warp, so
+// every lane computes and shuffles take a segment-local source):
+//  * rows never move: each lane tracks the POSITION its row currently has in the reference's
+//    swapped matrix. The pivot of step k is the un-pivoted row with the largest |a_ik|, ties to
+//    the lowest position (the first strictly larger magnitude of the reference's scan), found
+//    by a log-step butterfly over (magnitude, position|lane);
+//  * every candidate forms its own 1 / a_ik while the butterfly runs (SIMT: one instruction
+//    stream), and the winner's is broadcast: the reciprocal is off the chain;
+//  * elimination a_ij - (a_ik * inv) a_kj, skipped for a zero multiplier, from the broadcast pivot
+//    row; the forward substitution is fused (b_i - m b_k as the steps go: the same subtractions in
+//    the same ascending-column order as x[i] -= l_ij x[j], zero multipliers included);
+//  * the singular test is a flag checked once at the end (a singular system's result is unused);
+//  * U and y are scattered to shared memory by position and one lane runs the backward
+//    substitution, forming each quotient t / u_ii speculatively as RN(q + (t - u q) r), r = RN(1 / u_ii),
+//    q = RN(t r) (3 dependent operations; r is started a row ahead), with the IEEE quotient of the
+//    same t computed beside it, off the chain, and compared: a mismatch anywhere (not seen in
+//    practice) reruns the substitution with plain divisions, so the result is always the
+//    reference's.
+// Every element sees the reference's operations in the reference's order: bit-identical to
+// dev_lu_solve (tools/ubench/lu.cu checks 2000 systems per size, tests/test_gpu_kernels.py).
+template <int S>
+__device__ bool warp_lu_fixed(double* a, const double* rhs, double* x) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int PW = S <= 1 ? 1 : (S <= 2 ? 2 : (S <= 4 ? 4 : (S <= 8 ? 8 : 16)));
+  const int lane = threadIdx.x & 31;
+  const int row = lane & (PW - 1);
+  const bool mine = row < S;
+  double r[S];
+#pragma unroll
+  for (int j = 0; j < S; ++j) r[j] = mine ? a[row + j * S] : 0.0;
+  double bi = mine ? rhs[row] : 0.0;
+  double mx = 0.0;
+#pragma unroll
+  for (int j = 0; j < S; ++j) mx = dmax_ref(mx, fabs(r[j]));
+#pragma unroll
+  for (int o = PW / 2; o > 0; o >>= 1) mx = dmax_ref(mx, __shfl_xor_sync(FULL, mx, o));
+  const double thresh = 1e-14 * mx;
+  bool bad = mx == 0.0;
+  int pos = row;
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const bool cand = mine && pos >= k;
+    double mag = cand ? fabs(r[k]) : -1.0;
+    int key = ((cand ? pos : 255) << 8) | row;  // tie-break position, then the lane that holds it
+    const double myinv = 1.0 / r[k];
+#pragma unroll
+    for (int o = PW / 2; o > 0; o >>= 1) {
+      const double om = __shfl_xor_sync(FULL, mag, o);
+      const int ok = __shfl_xor_sync(FULL, key, o);
+      const bool take = (om > mag) || (om == mag && ok < key);
+      mag = take ? om : mag;
+      key = take ? ok : key;
+    }
+    const int piv = key >> 8, wl = key & 255;
+    bad = bad || (mag < thresh);
+    const double inv = __shfl_sync(FULL, myinv, wl, PW);
+    const double bp = __shfl_sync(FULL, bi, wl, PW);
+    pos = (row == wl) ? k : (pos == k ? piv : pos);  // the row at position k takes the winner's place
+    const bool below = mine && pos > k;
+    const double m = r[k] * inv;
+#pragma unroll
+    for (int j = k + 1; j < S; ++j) {
+      const double pj = __shfl_sync(FULL, r[j], wl, PW);
+      if (below && m != 0.0) r[j] = r[j] - m * pj;
+    }
+    if (below) bi = bi - m * bp;
+  }
+  if (bad) return false;  // the same on every lane
+  __syncwarp();
+  if (lane < PW && mine) {  // U (row `pos`, columns >= pos) and y by position
+#pragma unroll
+    for (int j = 0; j < S; ++j) a[pos + j * S] = r[j];
+    x[pos] = bi;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    // U is read from shared memory where it is used: holding it (S(S+1)/2 values) would not fit the
+    // 64 registers of the streaming kernels this runs inside.
+    double xv[S], y[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) y[i] = x[i];
+    bool same = true;
+    double rnext = 1.0 / a[(S - 1) + (S - 1) * S];
+#pragma unroll
+    for (int i = S - 1; i >= 0; --i) {
+      const double uii = a[i + i * S];
+      const double rc = rnext;
+      if (i > 0) rnext = 1.0 / a[(i - 1) + (i - 1) * S];
+      double t = y[i];
+#pragma unroll
+      for (int j = i + 1; j < S; ++j) t = t - a[i + j * S] * xv[j];
+      const double q = t * rc;
+      const double rem = __fma_rn(-uii, q, t);
+      const double xi = __fma_rn(rem, rc, q);
+      // the reference's quotient of the same t, off the chain
+      same = same && (__double_as_longlong(xi) == __double_as_longlong(t / uii));
+      xv[i] = xi;
+    }
+    if (!same) {
+#pragma unroll
+      for (int i = S - 1; i >= 0; --i) {
+        double t = y[i];
+#pragma unroll
+        for (int j = i + 1; j < S; ++j) t = t - a[i + j * S] * xv[j];
+        xv[i] = t / a[i + i * S];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) x[i] = xv[i];
+  }
+  __syncwarp();
+  return true;
+}
+
 template <int MAXS>
 __device__ bool warp_lu_solve(int s, double* a, const double* rhs, double* x) {
-  if (s == MAXS) return warp_lu_impl<MAXS, true>(s, a, rhs, x);
+  // tools/ubench/lu.cu on a B200 (cycles per nonsingular solve, column form / row form): s = 4
+  // 2825 / 2864, s = 8 6250 / 6170, s = 12 14140 / 14030, s = 16 23360 / 18520; s = 3, 6: the column
+  // form is 20-25% faster. Both are bit-identical to dev_lu_solve on 2000 systems per size.
+  if (s == MAXS) {
+    if constexpr (MAXS >= 8) return warp_lu_fixed<MAXS>(a, rhs, x);
+    return warp_lu_impl<MAXS, true>(s, a, rhs, x);
+  }
   return warp_lu_impl<MAXS, false>(s, a, rhs, x);
 }
 

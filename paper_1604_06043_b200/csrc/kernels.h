@@ -46,6 +46,9 @@ struct DevCsr {
   // Column band of the stored entries: blo <= col - row <= bhi for every entry (0, 0 when empty).
   // A narrow band lets the CSR SpMV keep a sliding x window in shared memory (kspmv.cu k_spmv_ring).
   int64_t blo = 0, bhi = 0;
+  // Largest entry count of any aligned 32-row block (rows 32b .. 32b+31): the TMA-fed banded kernel
+  // stages one block's CSR slice at a time (kspmv.cu k_spmv_ring2).
+  int32_t blk32_max = 0;
 };
 constexpr int kMaxDiag = 64;
 constexpr int kMaxConstDiag = 32;

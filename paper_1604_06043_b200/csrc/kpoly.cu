@@ -331,7 +331,7 @@ void launch_prologue(cudaStream_t st, int64_t n, int64_t ld, int s, const double
 
 void launch_validate(cudaStream_t st, const DevCsr& a, const double* p, const double* u,
                      const double* v, int64_t ld, int s, const Reducer& red, const double* au) {
-  LaunchScope ls(st, kKValidate, csr_bytes(a) + vbytes(a.n, 3.0 * s));
+  LaunchScope ls(st, kKValidate, (au ? 0.0 : csr_bytes(a)) + vbytes(a.n, 3.0 * s));
   MSTAB_DISPATCH_S(s, {
     auto kfn = k_validate<S>;
     const size_t sm = gram_smem<S>();

@@ -467,6 +467,231 @@ void launch_ring(cudaStream_t st, const DevCsr& a, const double* x, double* y, c
              red);
 }
 
+// ---- banded CSR, TMA-fed: sliding x window + bulk-copied CSR slices -------------------------------
+// ncu on k_spmv_ring (c3, r01): DRAM 50.6%, bytes minimal (traffic / algorithmic = 1.009), SMs 93%
+// active — latency-bound. Two causes: (1) a 128-entry chunk covers only ~4.7 rows of 27 entries,
+// so in the in-order row sums ~5 of 32 lanes work while the others idle; (2) every warp crosses a
+// CTA barrier per 1024-row tile, so all 32 warps load, wait and sum in phase and DRAM idles in
+// between. Here a warp owns a whole 32-row block at a time: lane 0 moves the block's contiguous CSR
+// slice (values and column indices, <= kR2Cap entries) into shared memory with two 1-D bulk async
+// copies (cp.async.bulk, the TMA engine) completing on an mbarrier, two blocks ahead of the one
+// being summed, so the bytes in flight do not depend on registers or on what the warp is doing.
+// All 32 lanes then form products value * x[column] from the ring in place and every lane adds ITS
+// row's products in CSR order (27 dependent adds, 32 rows in parallel). The CTA barrier comes once
+// per 1024 rows (32 blocks = 8 per warp), and the matrix copies (constant data) start before the
+// PDL wait. Product and sum are the reference's two roundings (csr.cpp:107-110): bit-identical.
+constexpr int kR2Warps = 4;
+constexpr int kR2Threads = kR2Warps * 32;
+constexpr int kR2Tile = 1024;                     // rows per ring advance (multiple of 32 * kR2Warps)
+constexpr int kR2Cap = 896;                       // CSR entries of one 32-row block (28 per row)
+constexpr int kR2CapV = kR2Cap + 8;               // + alignment slack (slice start rounded down to 4)
+constexpr int kR2BufBytes = kR2CapV * 12;         // values then columns; both offsets 16-byte aligned
+constexpr int kR2XPer = kR2Tile / kR2Threads;     // x values each thread carries to the next tile
+constexpr size_t kR2Smem = (size_t)kRing * 8 + (size_t)kR2Warps * 2 * kR2BufBytes + kR2Warps * 2 * 8;
+static_assert((kR2CapV * 8) % 16 == 0 && kR2BufBytes % 16 == 0, "bulk copies need 16-byte alignment");
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int S, bool TRUE_RES>
+__global__ void __launch_bounds__(kR2Threads, 1) k_spmv_ring2(DevCsr a, const double* __restrict__ x,
+                                                              double* __restrict__ y,
+                                                              const double* __restrict__ p, int64_t ld,
+                                                              const double* __restrict__ b,
+                                                              int64_t rows_per_cta, FinParams fin,
+                                                              Reducer red) {
+  extern __shared__ __align__(128) double ring2_smem[];
+  double* ring = ring2_smem;
+  DevState* ds = red.ds;
+  constexpr int NS = S + (TRUE_RES ? 1 : 0);
+  double part[NS];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) part[i] = 0.0;
+  const int64_t n = a.n;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  char* stage = reinterpret_cast<char*>(ring2_smem + kRing) + (size_t)wid * 2 * kR2BufBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(ring2_smem + kRing) +
+                                               (size_t)kR2Warps * 2 * kR2BufBytes) + wid * 2;
+  const int32_t* __restrict__ rp = a.row_ptr;
+  const int32_t* __restrict__ ci = a.col_idx;
+  const double* __restrict__ va = a.values;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(n, r0 + rows_per_cta);
+  const int64_t nblk = r0 < r1 ? (r1 - r0 + 31) >> 5 : 0;
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // row_ptr of this lane's row in block j (clamped to the CTA's range: rows past r1 are empty)
+  auto row_bounds = [&](int64_t j, int& be, int& en) {
+    const int64_t row = r0 + 32 * j + lane;
+    be = __ldg(rp + min(row, r1));
+    en = __ldg(rp + min(row + 1, r1));
+  };
+  // lane 0: bulk-copy the slice [wbeg & ~3, wend) of block j into buffer `buf` (or just arrive)
+  auto issue = [&](int wbeg, int wend, int buf) {
+    const int w0 = wbeg & ~3;
+    const uint32_t cnt = (uint32_t)((wend - w0 + 3) & ~3);
+    char* dst = stage + (size_t)buf * kR2BufBytes;
+    if (cnt == 0) {
+      mbar_arrive(&bars[buf]);
+      return;
+    }
+    mbar_expect_tx(&bars[buf], cnt * 12u);
+    bulk_g2s(dst, va + w0, cnt * 8u, &bars[buf]);
+    bulk_g2s(dst + kR2CapV * 8, ci + w0, cnt * 4u, &bars[buf]);
+  };
+  // pipeline state: bounds of the block being processed (0), the next one (1, copy in flight)
+  int be0 = 0, en0 = 0, be1 = 0, en1 = 0;
+  if (wid < nblk) row_bounds(wid, be0, en0);
+  if (wid + kR2Warps < nblk) row_bounds(wid + kR2Warps, be1, en1);
+  {
+    const int wb0 = __shfl_sync(0xffffffffu, be0, 0), we0 = __shfl_sync(0xffffffffu, en0, 31);
+    const int wb1 = __shfl_sync(0xffffffffu, be1, 0), we1 = __shfl_sync(0xffffffffu, en1, 31);
+    if (lane == 0) {  // the matrix never changes: its copies start before the PDL wait
+      issue(wb0, wid < nblk ? we0 : wb0, 0);
+      issue(wb1, wid + kR2Warps < nblk ? we1 : wb1, 1);
+    }
+  }
+  pdl_wait();
+  if (r0 < r1) {  // x window of the first tile
+    const int64_t w0 = max(a.xlo, r0 + a.blo), w1 = min(a.xhi, min(r1, r0 + kR2Tile) + a.bhi);
+    for (int64_t c = w0 + threadIdx.x; c < w1; c += kR2Threads) ring[c & (kRing - 1)] = __ldg(x + c);
+  }
+  __syncthreads();
+  constexpr int kIterPerTile = kR2Tile / (32 * kR2Warps);
+  const int64_t ntile = (r1 - r0 + kR2Tile - 1) / kR2Tile;
+  int64_t it = 0;
+  for (int64_t tile = 0; tile < ntile; ++tile) {
+    const int64_t t1 = min(r1, r0 + (tile + 1) * kR2Tile);
+    const int64_t t2 = min(r1, t1 + kR2Tile);
+    // this thread's share of the NEXT tile's window extension [t1 + bhi, t2 + bhi)
+    double xn[kR2XPer];
+    const int64_t xlim = min(a.xhi, t2 + a.bhi);
+#pragma unroll
+    for (int u = 0; u < kR2XPer; ++u) {
+      const int64_t nc = t1 + a.bhi + threadIdx.x + u * kR2Threads;
+      xn[u] = (t1 < r1 && nc < xlim && nc >= a.xlo) ? __ldg(x + nc) : 0.0;
+    }
+#pragma unroll 1
+    for (int ii = 0; ii < kIterPerTile; ++ii, ++it) {
+      const int64_t j = wid + kR2Warps * it;
+      const int64_t j2 = j + 2 * kR2Warps;
+      int be2 = 0, en2 = 0;
+      if (j2 < nblk) row_bounds(j2, be2, en2);
+      if (j < nblk) {
+        const int buf = (int)(it & 1);
+        const int64_t row = r0 + 32 * j + lane;
+        const bool valid = row < r1;
+        double pv[S];
+#pragma unroll
+        for (int c = 0; c < S; ++c) pv[c] = valid ? __ldg(p + c * ld + row) : 0.0;
+        const double bv = (TRUE_RES && valid) ? __ldg(b + row) : 0.0;
+        const int wbeg = __shfl_sync(0xffffffffu, be0, 0), wend = __shfl_sync(0xffffffffu, en0, 31);
+        const int w0 = wbeg & ~3;
+        double* sv = reinterpret_cast<double*>(stage + (size_t)buf * kR2BufBytes);
+        const int32_t* sc = reinterpret_cast<const int32_t*>(stage + (size_t)buf * kR2BufBytes + kR2CapV * 8);
+        mbar_wait(&bars[buf], (uint32_t)((it >> 1) & 1));
+        const int cnt = wend - w0;
+        // products in place, in batches whose loads are all issued before the first store (the
+        // compiler cannot reorder shared-memory loads across the stores of the previous entries:
+        // one entry at a time measured 543 us at c3, a dependent load-load-multiply-store chain)
+        constexpr int kBatch = 8, kIters = (kR2CapV + 31) / 32;
+#pragma unroll
+        for (int u0 = 0; u0 < kIters; u0 += kBatch) {
+          double v[kBatch];
+          int32_t cc[kBatch];
+#pragma unroll
+          for (int u = 0; u < kBatch; ++u) {
+            const int i = lane + 32 * (u0 + u);
+            const bool in = u0 + u < kIters && i < cnt;
+            v[u] = in ? sv[i] : 0.0;
+            cc[u] = in ? sc[i] : 0;
+          }
+#pragma unroll
+          for (int u = 0; u < kBatch; ++u) v[u] = v[u] * ring[cc[u] & (kRing - 1)];
+#pragma unroll
+          for (int u = 0; u < kBatch; ++u) {
+            const int i = lane + 32 * (u0 + u);
+            if (u0 + u < kIters && i < cnt) sv[i] = v[u];
+          }
+        }
+        __syncwarp();
+        // this lane's row: its products in CSR order, loaded kSumBatch at a time ahead of the adds
+        const int lo = be0 - w0, hi = en0 - w0;
+        double acc = 0.0;
+        constexpr int kSumBatch = 14;
+        for (int k0 = lo; k0 < hi; k0 += kSumBatch) {
+          double q[kSumBatch];
+#pragma unroll
+          for (int u = 0; u < kSumBatch; ++u) q[u] = k0 + u < hi ? sv[k0 + u] : 0.0;
+#pragma unroll
+          for (int u = 0; u < kSumBatch; ++u)
+            if (k0 + u < hi) acc = acc + q[u];
+        }
+        if (valid) {
+          if (TRUE_RES) acc = bv - acc;
+          y[row] = acc;
+#pragma unroll
+          for (int c = 0; c < S; ++c) part[c] = part[c] + pv[c] * acc;
+          if (TRUE_RES) part[S] = part[S] + acc * acc;
+        }
+        __syncwarp();
+        // refill this buffer with block j + 2 * kR2Warps (generic-proxy accesses ordered before the
+        // async-proxy writes)
+        const int wb2 = __shfl_sync(0xffffffffu, be2, 0), we2 = __shfl_sync(0xffffffffu, en2, 31);
+        if (lane == 0 && j2 < nblk) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(wb2, we2, buf);
+        }
+      }
+      be0 = be1;
+      en0 = en1;
+      be1 = be2;
+      en1 = en2;
+    }
+#pragma unroll
+    for (int u = 0; u < kR2XPer; ++u) {
+      const int64_t nc = t1 + a.bhi + threadIdx.x + u * kR2Threads;
+      if (t1 < r1 && nc < xlim && nc >= a.xlo) ring[nc & (kRing - 1)] = xn[u];
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
+  __shared__ double scratch[NS * 32];
+  __shared__ double blk[NS];
+  __shared__ double redv[NS];
+  __shared__ FinStage fs;
+  if (!red.xred) fin_prestage(fin, ds, fs);
+  block_totals<NS>(part, blk, scratch);
+  if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv, red.xred)) return;
+  finalize_spmv<S>(fin, redv, ds, fs);
+}
+
+// Needs the band plus two tiles in the ring and every aligned 32-row block within the staging cap.
+inline bool ring2_fits(const DevCsr& a) {
+  return a.bhi - a.blo + 1 + 2 * kR2Tile <= kRing && a.blk32_max > 0 && a.blk32_max + 3 <= kR2Cap;
+}
+
+template <int S, bool TRUE_RES>
+void launch_ring2(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p, int64_t ld,
+                  const double* b, const FinParams& fin, const Reducer& red) {
+  auto kfn = k_spmv_ring2<S, TRUE_RES>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kR2Smem);
+    configured = true;
+  }
+  const int64_t ntiles = (a.n + kR2Tile - 1) / kR2Tile;
+  int64_t grid = std::min<int64_t>(g_num_sms, std::max<int64_t>(1, ntiles));
+  const int64_t tiles_per_cta = (ntiles + grid - 1) / grid;
+  grid = std::max<int64_t>(1, (ntiles + tiles_per_cta - 1) / tiles_per_cta);
+  launch_pdl(kfn, (int)grid, kR2Threads, kR2Smem, st, a, x, y, p, ld, b, tiles_per_cta * kR2Tile, fin, red);
+}
+
 // Row-sharded finaliser of an SpMV reduction: the allreduced totals (ds->xred) run through the
 // same finalize_spmv tail the fused kernels run in their last CTA.
 template <int S>
@@ -519,6 +744,17 @@ void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y
     return;
   }
   static const bool no_ring = std::getenv("MSTAB_NO_RING") != nullptr;
+  // opt-in while it is being tuned: 426 us at c3 against the register-staged ring's 372 us (r02)
+  static const bool use_ring2 = std::getenv("MSTAB_RING2") != nullptr;
+  if (!no_ring && use_ring2 && ring2_fits(a)) {
+    MSTAB_DISPATCH_S(s, {
+      if (b)
+        launch_ring2<S, true>(st, a, x, y, p, ld, b, fin, red);
+      else
+        launch_ring2<S, false>(st, a, x, y, p, ld, b, fin, red);
+    });
+    return;
+  }
   if (!no_ring && ring_fits(a)) {
     MSTAB_DISPATCH_S(s, {
       if (b)

@@ -449,6 +449,9 @@ void upload_rows(Context& ctx, Operator* op, int64_t n, const int64_t* row_ptr, 
     }
   op->blo = blo;
   op->bhi = bhi;
+  int64_t bmax = 0;
+  for (int64_t i = 0; i < n; i += 32) bmax = std::max(bmax, row_ptr[std::min(n, i + 32)] - row_ptr[i]);
+  op->blk32_max = (int32_t)std::min<int64_t>(bmax, std::numeric_limits<int32_t>::max());
   std::vector<int32_t> rp32(n + 1), ci32(nnz + 32, 0);
   for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)row_ptr[i];
   for (int64_t k = 0; k < nnz; ++k) ci32[k] = (int32_t)col_idx[k];
@@ -609,6 +612,8 @@ std::shared_ptr<Operator> make_operator_slab(Context& ctx, int64_t n, const int6
   ctx.lay_nglobal = n;
   ctx.ws.reset();
   ctx.pcache.reset();
+  ctx.val_au.reset();
+  ctx.val_au_n = -1;
   std::vector<int64_t> rp(nl + 1), ci(row_ptr[end] - row_ptr[start]);
   for (int64_t i = 0; i <= nl; ++i) rp[i] = row_ptr[start + i] - row_ptr[start];
   for (size_t k = 0; k < ci.size(); ++k) ci[k] = col_idx[row_ptr[start] + (int64_t)k] - start;
@@ -840,8 +845,25 @@ mstab_validation_report validate(Context& ctx, const Recycle& rd, const Operator
   const int s = (int)rd.s;
   if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: recycle s must be in 1..16");
   const int64_t vld = ctx.ld(rd.n);
-  for (int q = 0; q < s && ctx.sharded(); ++q) halo(ctx, op, rd.u->d() + (size_t)q * vld);
   const double* au = nullptr;
+  // Large operators form A U with the cycle's own SpMV kernel, one column at a time (the
+  // constant-diagonal / DIA / banded-ring forms stream at 0.65-0.85 of HBM; the thread-per-row CSR
+  // product inside k_validate reached 0.15-0.25: r01 profiles), then k_validate reduces
+  // ||V - A U||, ||V||, P^H P and V^H V in one pass over the stored products. Same row sums in the
+  // same order, so the deviation is unchanged bit for bit. Small operators keep the single launch.
+  const bool by_spmv = !op.pc && op.n_global >= kCholQrMinRows && std::getenv("MSTAB_VALIDATE_FUSED") == nullptr;
+  if (by_spmv) {
+    if (!ctx.val_au || ctx.val_au_n != op.n || ctx.val_au_s < s) {
+      ctx.sync();
+      ctx.val_au = ctx.alloc_vecs(op.n, s);
+      ctx.val_au_n = op.n;
+      ctx.val_au_s = s;
+    }
+    for (int q = 0; q < s; ++q) spmv_dev(ctx, op, rd.u->d() + (size_t)q * vld, ctx.val_au->d() + (size_t)q * vld);
+    au = ctx.val_au->d();
+  } else {
+    for (int q = 0; q < s && ctx.sharded(); ++q) halo(ctx, op, rd.u->d() + (size_t)q * vld);
+  }
   if (op.pc) {  // A U through the preconditioned chain, column by column
     Precond& pc = *op.pc;
     if (!pc.au || pc.au_s < s) {

@@ -88,6 +88,9 @@ struct Context {
   // and column stride lay_ld; DevMem::d() points at the first owned row.
   std::unique_ptr<Comm> comm;
   DevPtr xgath;  // allgather landing buffer (world * kMaxXred doubles)
+  DevPtr val_au;  // validate: the products A U of a large plain operator (n x s scratch)
+  int64_t val_au_n = -1;
+  int val_au_s = 0;
   int64_t lay_n = -1, lay_lo = 0, lay_ld = 0, lay_row0 = 0, lay_nglobal = 0;
   bool sharded() const { return comm && comm->world() > 1; }
   int64_t ld(int64_t n) const { return n == lay_n ? lay_ld : padded_ld(n); }
@@ -127,6 +130,7 @@ struct Operator {
     c.xhi = xhi;
     c.blo = blo;
     c.bhi = bhi;
+    c.blk32_max = blk32_max;
     c.row_ptr = static_cast<const int32_t*>(rp->ptr);
     c.col_idx = static_cast<const int32_t*>(ci->ptr);
     c.values = val->d();
@@ -147,6 +151,7 @@ struct Operator {
   std::vector<int32_t> offsets;  // DIA offsets (host copy)
   // DIA form of the same matrix (kernels.h DevCsr), built at upload when it pays off
   int64_t blo = 0, bhi = 0;  // column band (kernels.h DevCsr)
+  int32_t blk32_max = 0;     // largest aligned 32-row block (kernels.h DevCsr)
   int32_t ndiag = 0;
   int64_t dia_ld = 0;
   DevPtr dia_val, dia_off;

@@ -5,7 +5,8 @@ test_solvers.cpp:514-541), on one B200.
 For every (s, ell) in {1,2,4,8,16} x {1,2,4,8}, both variants run the same 10-RHS implicit-Euler
 sequence (b_{i+1} = h^2 (x_i/dt + f), each variant chained on its own solutions) with device-resident
 b/x; the whole sequence is timed with CUDA events on the solver stream (first solve included: it
-is the fresh IDRstab that starts the recycling chain). Per (s, ell) it records RHS/s, cycles and
+is the fresh IDRstab that starts the recycling chain). The cut-space P(n, s, seed) is generated
+once per (s, ell) before BOTH arms (untimed, reported as fresh_start_s), so neither arm pays it. Per (s, ell) it records RHS/s, cycles and
 matrix-vector products per RHS, the worst true relative residual, and the per-kernel average
 duration / HBM GB/s of a second, profiled pass over the first 3 right-hand sides of the Mstab
 variant (CUDA events around every launch; they slow the step, so the timed pass runs without them).
@@ -107,6 +108,17 @@ def main():
                 cfg.s, cfg.ell = s, ell
                 row = {"s": s, "ell": ell}
                 try:
+                    # Both arms start from the same warm state: the context caches make_cut_space(n, s,
+                    # seed) (a pure function), and whichever arm ran first for a new s used to pay the
+                    # host draws alone (r01: the Mstab arm's l = 1 rows looked slower for that reason).
+                    # One untimed fresh start (P + Arnoldi, no cycle) per (s, l) fills the cache; its
+                    # cost is reported beside the arms instead of inside one of them.
+                    t1 = time.perf_counter()
+                    x0w, fw = cfg.sources()
+                    m.idrstab_solve(op, cfg.first_rhs(x0w, fw), None,
+                                    m.SolverConfig(s, ell, cfg.tol, s + 1, True, 0), None, None)
+                    ctx.synchronize()
+                    row["fresh_start_s"] = round(time.perf_counter() - t1, 4)
                     row["mstab"] = run_sequence(m, cfg, op, ctx, torch, stream, args.rhs, recycle=True)
                     row["idrstab"] = run_sequence(m, cfg, op, ctx, torch, stream, args.rhs, recycle=False)
                     if args.profile_rhs > 0:
