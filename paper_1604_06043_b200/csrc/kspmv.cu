@@ -473,22 +473,30 @@ void launch_ring(cudaStream_t st, const DevCsr& a, const double* x, double* y, c
 // so in the in-order row sums ~5 of 32 lanes work while the others idle; (2) every warp crosses a
 // CTA barrier per 1024-row tile, so all 32 warps load, wait and sum in phase and DRAM idles in
 // between. Here a warp owns a whole 32-row block at a time: lane 0 moves the block's contiguous CSR
-// slice (values and column indices, <= kR2Cap entries) into shared memory with two 1-D bulk async
-// copies (cp.async.bulk, the TMA engine) completing on an mbarrier, two blocks ahead of the one
-// being summed, so the bytes in flight do not depend on registers or on what the warp is doing.
-// All 32 lanes then form products value * x[column] from the ring in place and every lane adds ITS
-// row's products in CSR order (27 dependent adds, 32 rows in parallel). The CTA barrier comes once
-// per 1024 rows (32 blocks = 8 per warp), and the matrix copies (constant data) start before the
-// PDL wait. Product and sum are the reference's two roundings (csr.cpp:107-110): bit-identical.
-constexpr int kR2Warps = 4;
+// slice (values and column indices, <= kR2Cap entries) into the warp's shared-memory buffer with
+// two 1-D bulk async copies (cp.async.bulk, the TMA engine) completing on an mbarrier, so the bytes
+// in flight do not depend on registers. All 32 lanes then form products value * x[column] from the
+// ring in place and every lane adds ITS row's products in CSR order (27 dependent adds, 32 rows in
+// parallel). The copy of the warp's next block is issued as soon as the sums have freed the
+// buffer, before the P^H epilogue; the matrix copies (constant data) of the first block start
+// before the PDL wait. Product and sum are the reference's two roundings (csr.cpp:107-110):
+// bit-identical.
+// Sizing (ncu of the first version, 4 warps with two buffers each: 432 us, one warp per scheduler
+// issuing every 4.95 cycles, i.e. bound by each warp's own instruction latency): 12 warps with one
+// buffer each, and a ring of exactly band + two tiles (position = column + per-tile offset, one
+// conditional subtraction, instead of a power-of-two mask) to make the shared memory fit.
+constexpr int kR2Warps = 12;
 constexpr int kR2Threads = kR2Warps * 32;
-constexpr int kR2Tile = 1024;                     // rows per ring advance (multiple of 32 * kR2Warps)
+constexpr int kR2Tile = 768;                      // rows per ring advance: 2 blocks per warp
+constexpr int kR2Ring = 9984;                     // doubles: band (<= kR2Ring - 2 * kR2Tile) + two tiles
 constexpr int kR2Cap = 896;                       // CSR entries of one 32-row block (28 per row)
 constexpr int kR2CapV = kR2Cap + 8;               // + alignment slack (slice start rounded down to 4)
 constexpr int kR2BufBytes = kR2CapV * 12;         // values then columns; both offsets 16-byte aligned
 constexpr int kR2XPer = kR2Tile / kR2Threads;     // x values each thread carries to the next tile
-constexpr size_t kR2Smem = (size_t)kRing * 8 + (size_t)kR2Warps * 2 * kR2BufBytes + kR2Warps * 2 * 8;
-static_assert((kR2CapV * 8) % 16 == 0 && kR2BufBytes % 16 == 0, "bulk copies need 16-byte alignment");
+constexpr size_t kR2Smem = (size_t)kR2Ring * 8 + (size_t)kR2Warps * kR2BufBytes + kR2Warps * 8;
+static_assert((kR2CapV * 8) % 16 == 0 && kR2BufBytes % 16 == 0 && (kR2Ring * 8) % 16 == 0,
+              "bulk copies need 16-byte alignment");
+static_assert(kR2Tile % (32 * kR2Warps) == 0 && kR2Tile % kR2Threads == 0, "tile = whole blocks per warp");
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -510,9 +518,11 @@ __global__ void __launch_bounds__(kR2Threads, 1) k_spmv_ring2(DevCsr a, const do
   for (int i = 0; i < NS; ++i) part[i] = 0.0;
   const int64_t n = a.n;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  char* stage = reinterpret_cast<char*>(ring2_smem + kRing) + (size_t)wid * 2 * kR2BufBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(ring2_smem + kRing) +
-                                               (size_t)kR2Warps * 2 * kR2BufBytes) + wid * 2;
+  char* stage = reinterpret_cast<char*>(ring2_smem + kR2Ring) + (size_t)wid * kR2BufBytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(ring2_smem + kR2Ring) +
+                                              (size_t)kR2Warps * kR2BufBytes) + wid;
+  double* sv = reinterpret_cast<double*>(stage);
+  const int32_t* sc = reinterpret_cast<const int32_t*>(stage + kR2CapV * 8);
   const int32_t* __restrict__ rp = a.row_ptr;
   const int32_t* __restrict__ ci = a.col_idx;
   const double* __restrict__ va = a.values;
@@ -520,8 +530,7 @@ __global__ void __launch_bounds__(kR2Threads, 1) k_spmv_ring2(DevCsr a, const do
   const int64_t r1 = min(n, r0 + rows_per_cta);
   const int64_t nblk = r0 < r1 ? (r1 - r0 + 31) >> 5 : 0;
   if (lane == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -531,43 +540,45 @@ __global__ void __launch_bounds__(kR2Threads, 1) k_spmv_ring2(DevCsr a, const do
     be = __ldg(rp + min(row, r1));
     en = __ldg(rp + min(row + 1, r1));
   };
-  // lane 0: bulk-copy the slice [wbeg & ~3, wend) of block j into buffer `buf` (or just arrive)
-  auto issue = [&](int wbeg, int wend, int buf) {
+  // lane 0: bulk-copy the slice [wbeg & ~3, wend) into the warp's buffer (or just arrive)
+  auto issue = [&](int wbeg, int wend) {
     const int w0 = wbeg & ~3;
     const uint32_t cnt = (uint32_t)((wend - w0 + 3) & ~3);
-    char* dst = stage + (size_t)buf * kR2BufBytes;
     if (cnt == 0) {
-      mbar_arrive(&bars[buf]);
+      mbar_arrive(bar);
       return;
     }
-    mbar_expect_tx(&bars[buf], cnt * 12u);
-    bulk_g2s(dst, va + w0, cnt * 8u, &bars[buf]);
-    bulk_g2s(dst + kR2CapV * 8, ci + w0, cnt * 4u, &bars[buf]);
+    mbar_expect_tx(bar, cnt * 12u);
+    bulk_g2s(stage, va + w0, cnt * 8u, bar);
+    bulk_g2s(stage + kR2CapV * 8, ci + w0, cnt * 4u, bar);
   };
-  // pipeline state: bounds of the block being processed (0), the next one (1, copy in flight)
+  // bounds of the block being processed (0) and of the warp's next block (1)
   int be0 = 0, en0 = 0, be1 = 0, en1 = 0;
   if (wid < nblk) row_bounds(wid, be0, en0);
   if (wid + kR2Warps < nblk) row_bounds(wid + kR2Warps, be1, en1);
   {
     const int wb0 = __shfl_sync(0xffffffffu, be0, 0), we0 = __shfl_sync(0xffffffffu, en0, 31);
-    const int wb1 = __shfl_sync(0xffffffffu, be1, 0), we1 = __shfl_sync(0xffffffffu, en1, 31);
-    if (lane == 0) {  // the matrix never changes: its copies start before the PDL wait
-      issue(wb0, wid < nblk ? we0 : wb0, 0);
-      issue(wb1, wid + kR2Warps < nblk ? we1 : wb1, 1);
-    }
+    if (lane == 0 && wid < nblk) issue(wb0, we0);  // the matrix never changes: before the PDL wait
   }
   pdl_wait();
+  // ring position of column c while the tile starting at row t0 is current: c + koff, minus kR2Ring
+  // if that is past the end (columns of the tile's window and of the next tile's extension both
+  // land in [tbase, tbase + kR2Ring))
+  const int32_t origin = (int32_t)(r0 + a.blo);
   if (r0 < r1) {  // x window of the first tile
     const int64_t w0 = max(a.xlo, r0 + a.blo), w1 = min(a.xhi, min(r1, r0 + kR2Tile) + a.bhi);
-    for (int64_t c = w0 + threadIdx.x; c < w1; c += kR2Threads) ring[c & (kRing - 1)] = __ldg(x + c);
+    for (int64_t c = w0 + threadIdx.x; c < w1; c += kR2Threads) ring[(int32_t)c - origin] = __ldg(x + c);
   }
   __syncthreads();
   constexpr int kIterPerTile = kR2Tile / (32 * kR2Warps);
   const int64_t ntile = (r1 - r0 + kR2Tile - 1) / kR2Tile;
   int64_t it = 0;
+  uint32_t tbase = 0;  // ((t0 - r0) mod kR2Ring)
   for (int64_t tile = 0; tile < ntile; ++tile) {
-    const int64_t t1 = min(r1, r0 + (tile + 1) * kR2Tile);
+    const int64_t t0 = r0 + tile * kR2Tile;
+    const int64_t t1 = min(r1, t0 + kR2Tile);
     const int64_t t2 = min(r1, t1 + kR2Tile);
+    const int32_t koff = (int32_t)tbase - (int32_t)(t0 + a.blo);
     // this thread's share of the NEXT tile's window extension [t1 + bhi, t2 + bhi)
     double xn[kR2XPer];
     const int64_t xlim = min(a.xhi, t2 + a.bhi);
@@ -583,7 +594,6 @@ __global__ void __launch_bounds__(kR2Threads, 1) k_spmv_ring2(DevCsr a, const do
       int be2 = 0, en2 = 0;
       if (j2 < nblk) row_bounds(j2, be2, en2);
       if (j < nblk) {
-        const int buf = (int)(it & 1);
         const int64_t row = r0 + 32 * j + lane;
         const bool valid = row < r1;
         double pv[S];
@@ -592,31 +602,29 @@ __global__ void __launch_bounds__(kR2Threads, 1) k_spmv_ring2(DevCsr a, const do
         const double bv = (TRUE_RES && valid) ? __ldg(b + row) : 0.0;
         const int wbeg = __shfl_sync(0xffffffffu, be0, 0), wend = __shfl_sync(0xffffffffu, en0, 31);
         const int w0 = wbeg & ~3;
-        double* sv = reinterpret_cast<double*>(stage + (size_t)buf * kR2BufBytes);
-        const int32_t* sc = reinterpret_cast<const int32_t*>(stage + (size_t)buf * kR2BufBytes + kR2CapV * 8);
-        mbar_wait(&bars[buf], (uint32_t)((it >> 1) & 1));
-        const int cnt = wend - w0;
+        mbar_wait(bar, (uint32_t)(it & 1));
+        const int cnt = wend - w0, slack = wbeg - w0;  // entries [0, slack) belong to the row before
         // products in place, in batches whose loads are all issued before the first store (the
-        // compiler cannot reorder shared-memory loads across the stores of the previous entries:
-        // one entry at a time measured 543 us at c3, a dependent load-load-multiply-store chain)
+        // compiler cannot reorder shared-memory loads across the stores of the previous entries)
         constexpr int kBatch = 8, kIters = (kR2CapV + 31) / 32;
 #pragma unroll
         for (int u0 = 0; u0 < kIters; u0 += kBatch) {
           double v[kBatch];
-          int32_t cc[kBatch];
+          uint32_t pos[kBatch];
 #pragma unroll
           for (int u = 0; u < kBatch; ++u) {
             const int i = lane + 32 * (u0 + u);
-            const bool in = u0 + u < kIters && i < cnt;
+            const bool in = u0 + u < kIters && i >= slack && i < cnt;
             v[u] = in ? sv[i] : 0.0;
-            cc[u] = in ? sc[i] : 0;
+            const uint32_t ps = (uint32_t)((in ? sc[i] : (int32_t)(t0 + a.blo)) + koff);
+            pos[u] = min(ps, ps - (uint32_t)kR2Ring);
           }
 #pragma unroll
-          for (int u = 0; u < kBatch; ++u) v[u] = v[u] * ring[cc[u] & (kRing - 1)];
+          for (int u = 0; u < kBatch; ++u) v[u] = v[u] * ring[pos[u]];
 #pragma unroll
           for (int u = 0; u < kBatch; ++u) {
             const int i = lane + 32 * (u0 + u);
-            if (u0 + u < kIters && i < cnt) sv[i] = v[u];
+            if (u0 + u < kIters && i >= slack && i < cnt) sv[i] = v[u];
           }
         }
         __syncwarp();
@@ -632,20 +640,20 @@ __global__ void __launch_bounds__(kR2Threads, 1) k_spmv_ring2(DevCsr a, const do
           for (int u = 0; u < kSumBatch; ++u)
             if (k0 + u < hi) acc = acc + q[u];
         }
+        __syncwarp();
+        // the buffer is free: start the copy of the warp's next block (generic-proxy accesses
+        // ordered before the async-proxy writes), then finish this block's rows
+        const int wb1 = __shfl_sync(0xffffffffu, be1, 0), we1 = __shfl_sync(0xffffffffu, en1, 31);
+        if (lane == 0 && j + kR2Warps < nblk) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(wb1, we1);
+        }
         if (valid) {
           if (TRUE_RES) acc = bv - acc;
           y[row] = acc;
 #pragma unroll
           for (int c = 0; c < S; ++c) part[c] = part[c] + pv[c] * acc;
           if (TRUE_RES) part[S] = part[S] + acc * acc;
-        }
-        __syncwarp();
-        // refill this buffer with block j + 2 * kR2Warps (generic-proxy accesses ordered before the
-        // async-proxy writes)
-        const int wb2 = __shfl_sync(0xffffffffu, be2, 0), we2 = __shfl_sync(0xffffffffu, en2, 31);
-        if (lane == 0 && j2 < nblk) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(wb2, we2, buf);
         }
       }
       be0 = be1;
@@ -656,8 +664,13 @@ __global__ void __launch_bounds__(kR2Threads, 1) k_spmv_ring2(DevCsr a, const do
 #pragma unroll
     for (int u = 0; u < kR2XPer; ++u) {
       const int64_t nc = t1 + a.bhi + threadIdx.x + u * kR2Threads;
-      if (t1 < r1 && nc < xlim && nc >= a.xlo) ring[nc & (kRing - 1)] = xn[u];
+      if (t1 < r1 && nc < xlim && nc >= a.xlo) {
+        const uint32_t ps = (uint32_t)((int32_t)nc + koff);
+        ring[min(ps, ps - (uint32_t)kR2Ring)] = xn[u];
+      }
     }
+    tbase += (uint32_t)kR2Tile;
+    if (tbase >= (uint32_t)kR2Ring) tbase -= (uint32_t)kR2Ring;
     __syncthreads();
   }
   pdl_trigger();
@@ -673,7 +686,8 @@ __global__ void __launch_bounds__(kR2Threads, 1) k_spmv_ring2(DevCsr a, const do
 
 // Needs the band plus two tiles in the ring and every aligned 32-row block within the staging cap.
 inline bool ring2_fits(const DevCsr& a) {
-  return a.bhi - a.blo + 1 + 2 * kR2Tile <= kRing && a.blk32_max > 0 && a.blk32_max + 3 <= kR2Cap;
+  return a.bhi - a.blo + 1 + 2 * kR2Tile <= kR2Ring && a.blk32_max > 0 && a.blk32_max + 3 <= kR2Cap &&
+         a.n < (int64_t(1) << 30);
 }
 
 template <int S, bool TRUE_RES>
@@ -744,8 +758,8 @@ void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y
     return;
   }
   static const bool no_ring = std::getenv("MSTAB_NO_RING") != nullptr;
-  // opt-in while it is being tuned: 426 us at c3 against the register-staged ring's 372 us (r02)
-  static const bool use_ring2 = std::getenv("MSTAB_RING2") != nullptr;
+  // c3 (kbench, r02): 281 us, 0.857 of HBM, against the register-staged ring's 372 us (0.646)
+  static const bool use_ring2 = std::getenv("MSTAB_NO_RING2") == nullptr;
   if (!no_ring && use_ring2 && ring2_fits(a)) {
     MSTAB_DISPATCH_S(s, {
       if (b)

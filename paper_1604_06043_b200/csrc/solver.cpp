@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstddef>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -48,19 +49,65 @@ uint64_t next_operator_uid() {
   return next.fetch_add(1);
 }
 
+namespace {
+// blocks worth caching (vectors and n x s blocks, not the small dense state) and the cap per stream
+constexpr size_t kCacheMinBytes = size_t(1) << 20;
+size_t cache_cap_bytes() {
+  static const size_t cap = [] {
+    if (std::getenv("MSTAB_NO_BLOCK_CACHE")) return size_t(0);
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return size_t(0);
+    return total_b / 8;  // at most an eighth of the device per stream
+  }();
+  return cap;
+}
+}  // namespace
+
+void* StreamHolder::take(size_t bytes) {
+  if (bytes < kCacheMinBytes) return nullptr;
+  std::lock_guard<std::mutex> lk(cache_mu);
+  auto it = cache.find(bytes);
+  if (it == cache.end() || it->second.empty()) return nullptr;
+  void* p = it->second.back();
+  it->second.pop_back();
+  cached_bytes -= bytes;
+  return p;
+}
+
+bool StreamHolder::give(void* p, size_t bytes) {
+  if (bytes < kCacheMinBytes) return false;
+  std::lock_guard<std::mutex> lk(cache_mu);
+  if (cached_bytes + bytes > cache_cap_bytes()) return false;
+  cache[bytes].push_back(p);
+  cached_bytes += bytes;
+  return true;
+}
+
 StreamHolder::~StreamHolder() {
   if (stream) {
+    cudaStreamSynchronize(stream);
+    for (auto& kv : cache)
+      for (void* p : kv.second) cudaFreeAsync(p, stream);
+    cache.clear();
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
   }
 }
 
-DevMem::DevMem(std::shared_ptr<StreamHolder> st, size_t b) : bytes(b), stream(std::move(st)) {
-  CUDA_OK(cudaMallocAsync(&ptr, b == 0 ? 64 : b, stream->stream));
+DevMem::DevMem(std::shared_ptr<StreamHolder> st, size_t b) : bytes(b == 0 ? 64 : b), stream(std::move(st)) {
+  ptr = stream->take(bytes);
+  if (ptr) return;
+  static const bool dbg = std::getenv("MSTAB_DEBUG_ALLOC") != nullptr;
+  const auto t0 = Clock::now();
+  CUDA_OK(cudaMallocAsync(&ptr, bytes, stream->stream));
+  if (dbg) {
+    const double ms = ns_since(t0) / 1e6;
+    if (ms > 0.5) std::fprintf(stderr, "[mstab alloc] cudaMallocAsync(%zu MB) took %.2f ms\n", bytes >> 20, ms);
+  }
 }
 
 DevMem::~DevMem() {
-  if (ptr) cudaFreeAsync(ptr, stream->stream);
+  if (ptr && !stream->give(ptr, bytes)) cudaFreeAsync(ptr, stream->stream);
 }
 
 Context::Context(int dev) {

@@ -5,6 +5,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/mstab_b200.h"
@@ -34,6 +35,17 @@ using DevPtr = std::shared_ptr<DevMem>;
 struct StreamHolder {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // Size-bucketed cache of released blocks of this stream. A solve hands out fresh, independently
+  // owned blocks every time (x, the fetched and final U / V: 550 MB per solve at c2) and the caller
+  // drops the previous solve's; routed through cudaFreeAsync / cudaMallocAsync the driver's pool
+  // occasionally re-grows mid-solve (r02 step timing: sporadic 5-20 ms cycles at the fetch). A block
+  // released here is handed to the next request of the same size on the SAME stream, which is
+  // ordered after everything its previous owner enqueued, exactly like a stream-ordered free.
+  std::mutex cache_mu;
+  std::unordered_map<size_t, std::vector<void*>> cache;
+  size_t cached_bytes = 0;
+  void* take(size_t bytes);
+  bool give(void* p, size_t bytes);
   ~StreamHolder();
 };
 
