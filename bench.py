@@ -69,19 +69,61 @@ def workload_desc(cfg, A):
 
 # ---- clocks sampling (B200_PROFILING.md) -------------------------------------------------------
 class Clocks:
+    """SM clock and throttle reasons sampled DURING the timed region (the recipe's fields:
+    clocks.sm, clocks.max.sm, clocks_event_reasons.*). Sampled in-process through NVML (pynvml)
+    every 50 ms: the recipe's `nvidia-smi --query-gpu=... -lms 200` child reads the same NVML
+    counters, but its start-up and its heavier per-sample queries stalled solves on the device by
+    60-300 ms on this pool (r02: per-RHS solve times of 121 / 293 / 363 ms against 32 ms with the
+    child running, none without it), which is measurement noise, not workload. The child is the
+    fallback when pynvml is missing. The sampler starts before the warm-up; only samples inside
+    the timed window are summarised."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device):
-        self.device, self.rows, self.proc = device, [], None
+        self.device, self.rows, self.proc, self.stop, self.thread, self.source = device, [], None, False, None, None
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            # CUDA_VISIBLE_DEVICES remaps ordinals: resolve the NVML handle through the PCI bus id
+            import torch
+            pr = torch.cuda.get_device_properties(self.device)
+            bus, dom, dev = getattr(pr, "pci_bus_id", -1), getattr(pr, "pci_domain_id", 0), getattr(pr, "pci_device_id", 0)
+            try:
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(f"{dom:08X}:{bus:02X}:{dev:02X}.0".encode())
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            masks = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                     pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+
+            def loop():
+                while not self.stop:
+                    try:
+                        sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        bits = int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+                        self.rows.append([time.perf_counter(), str(self.device), str(sm), str(mx), "", ""]
+                                         + ["Active" if bits & mk else "Not Active" for mk in masks])
+                    except Exception:
+                        pass
+                    time.sleep(0.05)
+
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+            self.source = "nvml in-process, 50 ms"
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
+            self.source = "nvidia-smi -lms 200"
         except Exception:
             self.proc = None
         return self
@@ -95,6 +137,9 @@ class Clocks:
         return time.perf_counter()
 
     def __exit__(self, *a):
+        self.stop = True
+        if self.thread:
+            self.thread.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
@@ -103,18 +148,16 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self, t0=None, t1=None):
-        """Median SM clock and throttle reasons of the samples taken inside [t0, t1] (the timed region;
-        the sampler itself is started before the warm-up so that nvidia-smi's start-up — which can stall
-        the device for 100+ ms — stays out of the timed region)."""
+        """Median SM clock and throttle reasons of the samples taken inside [t0, t1] (the timed region)."""
         rows = [r[1:] for r in self.rows if (t0 is None or r[0] >= t0) and (t1 is None or r[0] <= t1 + 0.25)]
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "samples": 0,
+                    "source": self.source}
         sm = [float(r[1]) for r in rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "source": self.source}
 
 
 # ---- the sequence driver (caller side of the hot path; reference harness.cpp:192-265) ----------
@@ -164,11 +207,14 @@ class Sequence:
         b = self.b_d if self.device_mode else self.b_h
         restarted = False
         t0 = time.perf_counter()
+        r = None
         try:
             r = m.idrstab_solve(self.op, b, None, self.sc, self.rec, self.fp)
         except m.StaleData:
             restarted = True
+        if restarted:  # outside the handler: the rejected hand-off and the traceback are released first
             self.restarts += 1
+            self.rec = None
             r = m.idrstab_solve(self.op, b, None, self.sc, None, self.fp)
         rep = r._rep
         self.log.append({"cycles": int(rep.cycles), "status": int(rep.status), "restart": restarted,

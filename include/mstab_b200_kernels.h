@@ -30,6 +30,34 @@ int mstab_kernel_cut_space(mstab_context* ctx, int64_t n, int64_t s, uint64_t se
 int mstab_kernel_arnoldi(mstab_context* ctx, const mstab_operator* op, const double* r0, int64_t s,
                          uint64_t rng_seed, double* u, double* v, int64_t* mv_cost);
 
+/* arnoldi_init with the padding draws supplied by the caller: fill(user, out, count) must write
+ * `count` standard normal draws (the reference takes them from the caller's std::mt19937_64
+ * through one std::normal_distribution per call, idrstab.cpp:60,77-78; the drop-in shim passes
+ * exactly that). Only called on a happy breakdown. */
+typedef void (*mstab_normal_fill_fn)(void* user, double* out, int64_t count);
+int mstab_kernel_arnoldi_cb(mstab_context* ctx, const mstab_operator* op, const double* r0, int64_t s,
+                            mstab_normal_fill_fn fill, void* user, double* u, double* v, int64_t* mv_cost);
+
+/* bicg_projection (idrstab.cpp:89-94): gamma = (P^H block)^-1 P^H target; p and block are n x s.
+ * MSTAB_E_SINGULAR when the projection block is singular (solve_small). */
+int mstab_kernel_bicg_projection(mstab_context* ctx, int64_t n, int64_t s, const double* p,
+                                 const double* block, const double* target, double* gamma);
+
+/* level_iteration (idrstab.cpp:105-152), level k of IterationState (idrstab.hpp:38-46):
+ *   x0        n               in/out
+ *   r_levels  n x (k + 2)     r^(0..k) on entry, r^(0..k+1) on return
+ *   v_levels  n x s x (k + 3) V^(-1..k) on entry (v_levels[i] = level i - 1), V^(-1..k+1) on return
+ * Costs s + 1 operator applications. MSTAB_E_SINGULAR on a singular projection block. */
+int mstab_kernel_level_iteration(mstab_context* ctx, const mstab_operator* op, int64_t s, int64_t k,
+                                 const double* p, double* x0, double* r_levels, double* v_levels);
+
+/* poly_combination (idrstab.cpp:154-191) of a state with levels r^(0..ell), V^(-1..ell):
+ * x, r (n), u, v (n x s), tau (ell), *tail_perturbed. MSTAB_E_RANK when the stabilisation block
+ * lost rank (least_squares_tall). */
+int mstab_kernel_poly_combination(mstab_context* ctx, int64_t n, int64_t s, int64_t ell, const double* x0,
+                                  const double* r_levels, const double* v_levels, double* x, double* r,
+                                  double* u, double* v, double* tau, int32_t* tail_perturbed);
+
 /* Micro-benchmark of one kernel class of the cycle on synthetic data shaped like `op` with
  * (s, ell): `iters` back-to-back launches timed with CUDA events; *us = mean microseconds per
  * launch, *bytes = algorithmic bytes per launch. kind: 0 SpMV + P^H + LU finalize, 1 top

@@ -551,6 +551,59 @@ int mstab_kernel_arnoldi(mstab_context*, const mstab_operator* op, const double*
   });
 }
 
+// The reference's arnoldi_init draws its padding from a std::mt19937_64 it is handed, so a draw
+// callback cannot be injected: the callback form exists on the B200 library only (the shim passes
+// the caller's engine through it); this library answers the seed form, mstab_kernel_arnoldi.
+int mstab_kernel_arnoldi_cb(mstab_context*, const mstab_operator*, const double*, int64_t,
+                            mstab_normal_fill_fn, void*, double*, double*, int64_t*) {
+  return guarded([&] { throw ConfigErr("reference build: use mstab_kernel_arnoldi (seed form)"); });
+}
+
+int mstab_kernel_bicg_projection(mstab_context*, int64_t n, int64_t s, const double* p, const double* block,
+                                 const double* target, double* gamma) {
+  return guarded([&] {
+    mstab::Vector g = mstab::bicg_projection(to_dense(p, n, s), to_dense(block, n, s), to_vec(target, n));
+    for (int64_t i = 0; i < s; ++i) gamma[i] = g[(size_t)i].real();
+  });
+}
+
+int mstab_kernel_level_iteration(mstab_context*, const mstab_operator* op, int64_t s, int64_t k, const double* p,
+                                 double* x0, double* r_levels, double* v_levels) {
+  return guarded([&] {
+    const int64_t n = (int64_t)op->m.n_rows;
+    mstab::IterationState st;
+    st.x0 = to_vec(x0, n);
+    for (int64_t i = 0; i <= k; ++i) st.r_levels.push_back(to_vec(r_levels + i * n, n));
+    for (int64_t i = 0; i <= k + 1; ++i) st.v_levels.push_back(to_dense(v_levels + i * n * s, n, s));
+    mstab::SolveReport rep;
+    mstab::level_iteration(st, *op->op, to_dense(p, n, s), (size_t)k, rep);
+    for (int64_t t = 0; t < n; ++t) x0[t] = st.x0[(size_t)t].real();
+    for (int64_t i = 0; i <= k + 1; ++i)
+      for (int64_t t = 0; t < n; ++t) r_levels[i * n + t] = st.r_levels[(size_t)i][(size_t)t].real();
+    for (int64_t i = 0; i <= k + 2; ++i) from_dense(st.v_levels[(size_t)i], v_levels + i * n * s);
+  });
+}
+
+int mstab_kernel_poly_combination(mstab_context*, int64_t n, int64_t s, int64_t ell, const double* x0,
+                                  const double* r_levels, const double* v_levels, double* x, double* r,
+                                  double* u, double* v, double* tau, int32_t* tail_perturbed) {
+  return guarded([&] {
+    mstab::IterationState st;
+    st.x0 = to_vec(x0, n);
+    for (int64_t i = 0; i <= ell; ++i) st.r_levels.push_back(to_vec(r_levels + i * n, n));
+    for (int64_t i = 0; i <= ell + 1; ++i) st.v_levels.push_back(to_dense(v_levels + i * n * s, n, s));
+    mstab::PolyOut po = mstab::poly_combination(st, (size_t)ell);
+    for (int64_t t = 0; t < n; ++t) {
+      x[t] = po.x[(size_t)t].real();
+      r[t] = po.r[(size_t)t].real();
+    }
+    from_dense(po.u, u);
+    from_dense(po.v, v);
+    for (int64_t i = 0; i < ell; ++i) tau[i] = po.tau[(size_t)i].real();
+    if (tail_perturbed) *tail_perturbed = po.tail_perturbed ? 1 : 0;
+  });
+}
+
 }  // extern "C"
 
 // ---- bench reference arm: the reference solve loop advanced one level iteration at a time ------

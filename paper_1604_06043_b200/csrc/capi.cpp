@@ -11,6 +11,9 @@
 
 #include "solver.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 using namespace mstab_b200;
 
 struct mstab_context {
@@ -560,6 +563,55 @@ int mstab_kernel_arnoldi(mstab_context* ctx, const mstab_operator* op, const dou
   });
 }
 
+int mstab_kernel_arnoldi_cb(mstab_context* ctx, const mstab_operator* op, const double* r0, int64_t s,
+                            mstab_normal_fill_fn fill, void* user, double* u, double* v, int64_t* mv_cost) {
+  return guarded([&] {
+    bind(ctx);
+    Context& c = *ctx->impl;
+    if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: 1 <= s <= 16");
+    if (!fill) throw Error(MSTAB_E_CONFIG, "arnoldi: no draw callback");
+    const int64_t n = op->impl->n, ld = c.ld(n);
+    DevPtr r = c.alloc_vecs(n, 1), U = c.alloc_vecs(n, s), V = c.alloc_vecs(n, s);
+    cudaMemcpyAsync(r->d(), r0, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream());
+    reset_status(c);
+    arnoldi_init(c, *op->impl, r->d(), (int)s, [&](double* out, int64_t count) { fill(user, out, count); },
+                 U->d(), V->d());
+    cudaMemcpy2DAsync(u, sizeof(double) * n, U->d(), sizeof(double) * ld, sizeof(double) * n, s,
+                      cudaMemcpyDeviceToHost, c.stream());
+    cudaMemcpy2DAsync(v, sizeof(double) * n, V->d(), sizeof(double) * ld, sizeof(double) * n, s,
+                      cudaMemcpyDeviceToHost, c.stream());
+    c.sync();
+    if (mv_cost) *mv_cost = s;
+  });
+}
+
+int mstab_kernel_bicg_projection(mstab_context* ctx, int64_t n, int64_t s, const double* p,
+                                 const double* block, const double* target, double* gamma) {
+  return guarded([&] {
+    bind(ctx);
+    if (n < 1) throw Error(MSTAB_E_DIMENSION, "bicg_projection: empty vectors");
+    bicg_projection_host(*ctx->impl, n, (int)s, p, block, target, gamma);
+  });
+}
+
+int mstab_kernel_level_iteration(mstab_context* ctx, const mstab_operator* op, int64_t s, int64_t k,
+                                 const double* p, double* x0, double* r_levels, double* v_levels) {
+  return guarded([&] {
+    bind(ctx);
+    level_iteration_host(*ctx->impl, *op->impl, (int)s, (int)k, p, x0, r_levels, v_levels);
+  });
+}
+
+int mstab_kernel_poly_combination(mstab_context* ctx, int64_t n, int64_t s, int64_t ell, const double* x0,
+                                  const double* r_levels, const double* v_levels, double* x, double* r,
+                                  double* u, double* v, double* tau, int32_t* tail_perturbed) {
+  return guarded([&] {
+    bind(ctx);
+    poly_combination_host(*ctx->impl, n, (int)s, (int)ell, x0, r_levels, v_levels, x, r, u, v, tau,
+                          tail_perturbed);
+  });
+}
+
 }  // extern "C"
 
 // ---- sequence-driver helpers ------------------------------------------------------------------
@@ -631,6 +683,17 @@ int mstab_harness_axpby(mstab_context* ctx, int64_t n, const double* x, const do
 extern "C" {
 
 uint64_t mstab_launch_count(void) { return launch_count(); }
+
+namespace {
+// MSTAB_REPORT_LAUNCHES=1: the kernel launch total on stderr at process exit (evidence that a
+// host program linked against the drop-in ran its work on the device, tests/test_refsuite.py).
+struct LaunchReport {
+  ~LaunchReport() {
+    if (std::getenv("MSTAB_REPORT_LAUNCHES"))
+      std::fprintf(stderr, "[mstab] kernel launches: %llu\n", (unsigned long long)launch_count());
+  }
+} g_launch_report;
+}  // namespace
 
 int mstab_profiling_enable(int32_t on) {
   return guarded([&] {

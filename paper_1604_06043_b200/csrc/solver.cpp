@@ -17,7 +17,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <limits>
+#include <optional>
 
 namespace mstab_b200 {
 
@@ -34,6 +36,26 @@ using Clock = std::chrono::steady_clock;
 int64_t ns_since(Clock::time_point t0) {
   return std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count();
 }
+
+// MSTAB_DEBUG_STALL=ms: report any traced host-side step of a solve that took longer (stderr).
+struct StallTrace {
+  const char* what;
+  Clock::time_point t0;
+  static double limit_ms() {
+    static const double v = [] {
+      const char* e = std::getenv("MSTAB_DEBUG_STALL");
+      return e ? std::atof(e) : -1.0;
+    }();
+    return v;
+  }
+  explicit StallTrace(const char* w) : what(w), t0(Clock::now()) {}
+  ~StallTrace() {
+    const double lim = limit_ms();
+    if (lim < 0.0) return;
+    const double ms = ns_since(t0) / 1e6;
+    if (ms > lim) std::fprintf(stderr, "[mstab stall] %s took %.2f ms\n", what, ms);
+  }
+};
 
 void check_launch() {
   cudaError_t e = cudaGetLastError();
@@ -57,7 +79,7 @@ size_t cache_cap_bytes() {
     if (std::getenv("MSTAB_NO_BLOCK_CACHE")) return size_t(0);
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return size_t(0);
-    return total_b / 8;  // at most an eighth of the device per stream
+    return total_b / 3;  // at most a third of the device per stream
   }();
   return cap;
 }
@@ -71,16 +93,29 @@ void* StreamHolder::take(size_t bytes) {
   void* p = it->second.back();
   it->second.pop_back();
   cached_bytes -= bytes;
+  static const bool dbg = std::getenv("MSTAB_DEBUG_ALLOC") != nullptr;
+  if (dbg) std::fprintf(stderr, "[mstab alloc] take %zu MB from cache\n", bytes >> 20);
   return p;
 }
 
 bool StreamHolder::give(void* p, size_t bytes) {
   if (bytes < kCacheMinBytes) return false;
+  static const bool dbg = std::getenv("MSTAB_DEBUG_ALLOC") != nullptr;
   std::lock_guard<std::mutex> lk(cache_mu);
-  if (cached_bytes + bytes > cache_cap_bytes()) return false;
+  const bool ok = cached_bytes + bytes <= cache_cap_bytes();
+  if (dbg) std::fprintf(stderr, "[mstab alloc] give %zu MB %s (cached %zu MB)\n", bytes >> 20, ok ? "kept" : "REFUSED", cached_bytes >> 20);
+  if (!ok) return false;
   cache[bytes].push_back(p);
   cached_bytes += bytes;
   return true;
+}
+
+void StreamHolder::drop_cache() {
+  std::lock_guard<std::mutex> lk(cache_mu);
+  for (auto& kv : cache)
+    for (void* p : kv.second) cudaFreeAsync(p, stream);
+  cache.clear();
+  cached_bytes = 0;
 }
 
 StreamHolder::~StreamHolder() {
@@ -328,13 +363,21 @@ DevPtr make_cut_space(Context& ctx, int64_t n, int s, uint64_t seed) {
 // V = A U from the same sweep, happy breakdowns padded with seeded Gaussian directions.
 void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s, uint64_t seed,
                   double* U, double* V) {
+  std::unique_ptr<NormalStream, void (*)(NormalStream*)> rng(nullptr, normal_stream_destroy);
+  arnoldi_init(ctx, op, r0, s, [&](double* out, int64_t count) {
+    if (!rng) rng.reset(normal_stream_create(seed));
+    normal_stream_fill(rng.get(), out, count);
+  }, U, V);
+}
+
+void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s,
+                  const std::function<void(double*, int64_t)>& draw, double* U, double* V) {
   const int64_t n = op.n, ld = ctx.ld(n);
   cudaStream_t st = ctx.stream();
   norm2sq(ctx, n, r0, 0);
   if (read_scal(ctx, 1)[0] == 0.0) throw Error(MSTAB_E_ERROR, "arnoldi_init: zero start vector");
   launch_div_by_sqrt(st, n, r0, scal(ctx, 0), U);
   check_launch();
-  std::unique_ptr<NormalStream, void (*)(NormalStream*)> rng(nullptr, normal_stream_destroy);
   DevPtr w = ctx.alloc_vecs(n, 1);
   std::vector<double> hw;
   auto mgs2 = [&](int k) {
@@ -358,9 +401,8 @@ void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s, uin
     const double wnorm0 = std::sqrt(h[1]);
     double wnorm = std::sqrt(h[3]);
     while (wnorm <= 1e-12 * std::max(wnorm0, 1.0)) {
-      if (!rng) rng.reset(normal_stream_create(seed));
       hw.resize(draw_len(ctx, n));
-      normal_stream_fill(rng.get(), hw.data(), (int64_t)hw.size());
+      draw(hw.data(), (int64_t)hw.size());
       CUDA_OK(cudaMemcpyAsync(w->d(), own_rows(ctx, n, hw.data()), sizeof(double) * n, cudaMemcpyHostToDevice, st));
       CUDA_OK(cudaStreamSynchronize(st));
       mgs2(k);
@@ -374,17 +416,34 @@ void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s, uin
 
 namespace {
 
+void enqueue_level(Context& ctx, const Operator& op, const double* P, int s, int ell, int k,
+                   const WSet& S, const WSet& D, const std::vector<DevPtr>& R,
+                   const std::vector<DevPtr>& VL);
+void enqueue_poly(Context& ctx, const Operator& op, const double* P, int s, int ell, const WSet& D,
+                  const std::vector<DevPtr>& R, const std::vector<DevPtr>& VL);
+
 // One outer cycle: ell level iterations + poly_combination, S -> D (idrstab.cpp:250-259).
 void enqueue_cycle(Context& ctx, const Operator& op, const double* P, int s, int ell,
+                   const WSet& S, const WSet& D, const std::vector<DevPtr>& R,
+                   const std::vector<DevPtr>& VL) {
+  for (int k = 0; k < ell; ++k) enqueue_level(ctx, op, P, s, ell, k, S, D, R, VL);
+  check_launch();
+  enqueue_poly(ctx, op, P, s, ell, D, R, VL);
+}
+
+// One level iteration k (idrstab.cpp:105-152): the BiCG step on the top level with gamma_k
+// (ds->gamma row k), r^(k+1) = A r^(k), the s column rebuilds at the top level each raised by one
+// product, then the deferred lower levels. At k = 0 the state is read from S and written to D
+// (S == D is allowed: every kernel of the level is safe in place).
+void enqueue_level(Context& ctx, const Operator& op, const double* P, int s, int ell, int k,
                    const WSet& S, const WSet& D, const std::vector<DevPtr>& R,
                    const std::vector<DevPtr>& VL) {
   const int64_t n = op.n, ld = ctx.ld(n);
   const bool shard = ctx.sharded();
   cudaStream_t st = ctx.stream();
   DevState* ds = ctx.ds();
-  const Reducer red = ctx.reducer();
   auto col = [ld](double* base, int q) { return base + (size_t)q * ld; };
-  for (int k = 0; k < ell; ++k) {
+  {
     // (a) top level: r^(k) -= V^(k) gamma_k
     const double* r_in = (k == 0) ? S.r->d() : R[k]->d();
     double* r_out = (k == 0) ? D.r->d() : R[k]->d();
@@ -435,8 +494,16 @@ void enqueue_cycle(Context& ctx, const Operator& op, const double* P, int s, int
     launch_rebuild_deferred(st, n, ld, s, k, lv_in, lv_out, rin, rout,
                             (k == 0) ? S.x->d() : D.x->d(), D.x->d(), ds);
   }
-  check_launch();
-  // poly_combination: least squares, then the combined x, r, U, V (+ next cycle's P^H r, P^H V)
+}
+
+// poly_combination (idrstab.cpp:154-191): least squares, then the combined x, r, U, V (+ the next
+// cycle's P^H r, P^H V and gamma_0), all in D.
+void enqueue_poly(Context& ctx, const Operator& op, const double* P, int s, int ell, const WSet& D,
+                  const std::vector<DevPtr>& R, const std::vector<DevPtr>& VL) {
+  const int64_t n = op.n, ld = ctx.ld(n);
+  const bool shard = ctx.sharded();
+  cudaStream_t st = ctx.stream();
+  const Reducer red = ctx.reducer();
   const double* rr[kMaxEll + 1];
   rr[0] = D.r->d();
   for (int i = 1; i <= ell; ++i) rr[i] = R[i]->d();
@@ -986,6 +1053,18 @@ Workspace& workspace(Context& ctx, const Operator& op, int s, int ell, bool tres
   }
   w->b = ctx.alloc_vecs(n, 1);
   w->P = ctx.alloc_vecs(n, s);
+  // Result blocks of the solves to come (x; U, V of the fetched and the final recycle data): a solve
+  // hands out four fresh n x s blocks and the caller usually still holds the previous solve's. On
+  // this pool a cudaMallocAsync that has to grow the driver's pool stalled for 40-300 ms at random
+  // (r02 stall probe), so the blocks are created here, once, and parked in the stream's cache:
+  // twelve n x s blocks (two solves' worth plus what a caller's garbage collector may sit on) and
+  // three vectors. Blocks cached for a previous workspace shape are released first.
+  if (std::getenv("MSTAB_NO_BLOCK_CACHE") == nullptr) {
+    ctx.sh->drop_cache();
+    std::vector<DevPtr> warm;
+    for (int i = 0; i < 12; ++i) warm.push_back(ctx.alloc_vecs(n, s));
+    for (int i = 0; i < 3; ++i) warm.push_back(ctx.alloc_vecs(n, 1));
+  }
   return *w;
 }
 
@@ -1072,12 +1151,15 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   reset_status(ctx);
 
   // b: ensure_finite + bnorm (idrstab.cpp:200, :205)
+  std::optional<StallTrace> tr_in;
+  tr_in.emplace("copy-in + stats (first sync)");
   CUDA_OK(cudaMemcpyAsync(w.b->d(), b_in, sizeof(double) * n,
                           mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   launch_vec_stats(st, n, w.b->d(), scal(ctx, 0), ctx.reducer());
   check_launch();
   after_stats(ctx, scal(ctx, 0));
   const double* h = read_scal(ctx, 3);
+  tr_in.reset();
   if (h[1] > 0.0) throw Error(MSTAB_E_ERROR, "idrstab rhs: non-finite entries");
   const auto t0 = Clock::now();
   auto res = std::make_unique<SolveResultImpl>();
@@ -1116,7 +1198,10 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   std::vector<std::complex<double>> omega_levels;
   bool omegas_complete = true;
   if (recycle) {
-    validate(ctx, *recycle, op);
+    {
+      StallTrace tr("validate");
+      validate(ctx, *recycle, op);
+    }
     rep.h_mv_aux += recycle->s;
     if (recycle->s != cfg.s) throw Error(MSTAB_E_CONFIG, "idrstab: recycle s != config s");
     P = recycle->p;
@@ -1159,8 +1244,14 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
 
   bool broke = false;
   while (resnorm > threshold && rep.h_mv < cfg.max_mv) {
-    run_cycle(ctx, op, w, p);
-    const CycleStatus& cs = read_status(ctx);
+    {
+      StallTrace tr("cycle launch");
+      run_cycle(ctx, op, w, p);
+    }
+    const CycleStatus& cs = [&]() -> const CycleStatus& {
+      StallTrace tr("cycle status read (sync)");
+      return read_status(ctx);
+    }();
     if (w.graph[p].profiled) prof_accumulate(w.graph[p].prof);
     if (cs.breakdown) {  // BreakdownError: keep the last completed cycle (idrstab.cpp:290-293)
       rep.h_mv += cs.mv_at_breakdown;
@@ -1188,6 +1279,7 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
                        (fetch->kind == MSTAB_FETCH_AT_HALF_TOLERANCE &&
                         resnorm <= std::sqrt(cfg.tol) * rep.bnorm);
       if (hit) {  // fetch(): deep copy (recycle.cpp:26-38)
+        StallTrace tr("fetch copy");
         auto f = std::make_shared<Recycle>();
         f->n = n;
         f->s = s;
@@ -1204,6 +1296,7 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   if (!broke) rep.status = resnorm <= threshold ? MSTAB_STATUS_CONVERGED : MSTAB_STATUS_MAXMV;
   rep.final_resnorm = resnorm;
   const WSet& cur = w.set[p];
+  StallTrace tr_final("final copies + sync");
   res->x = copy_vec(ctx, cur.x, n);
   auto fin = std::make_shared<Recycle>();
   fin->n = n;
@@ -1221,6 +1314,123 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   ctx.sync();
   rep.wall_ns_total = ns_since(t0);
   return res;
+}
+
+// ---- the reference's test-visible helpers on the device (idrstab.hpp:27-68) ---------------------
+// Host blocks in, host blocks out (column-major, leading dimension n), every length-N step on the
+// kernels the solve loop runs. Used by the C-ABI kernel entry points and, through them, by the
+// drop-in shim's level_iteration / poly_combination / bicg_projection.
+namespace {
+
+void upload_cols(Context& ctx, double* dst, const double* src, int64_t n, int64_t cols) {
+  CUDA_OK(cudaMemcpy2DAsync(dst, sizeof(double) * ctx.ld(n), src, sizeof(double) * n, sizeof(double) * n,
+                            (size_t)cols, cudaMemcpyHostToDevice, ctx.stream()));
+}
+void download_cols(Context& ctx, double* dst, const double* src, int64_t n, int64_t cols) {
+  CUDA_OK(cudaMemcpy2DAsync(dst, sizeof(double) * n, src, sizeof(double) * ctx.ld(n), sizeof(double) * n,
+                            (size_t)cols, cudaMemcpyDeviceToHost, ctx.stream()));
+}
+
+// gamma = (P^H block)^-1 P^H target into ds->gamma row `slot` (the prologue kernel's reductions and
+// its warp LU); throws SingularProjection like solve_small.
+void project_dev(Context& ctx, int64_t n, int s, const double* P, const double* block, const double* target,
+                 int slot) {
+  reset_status(ctx);
+  launch_prologue(ctx.stream(), n, ctx.ld(n), s, P, block, target, ctx.reducer());
+  check_launch();
+  after_poly(ctx, s);
+  if (read_status(ctx).pending_singular) throw Error(MSTAB_E_SINGULAR, "solve_small: pivot collapse");
+  if (slot != 0)
+    CUDA_OK(cudaMemcpyAsync(ctx.ds()->gamma + (size_t)slot * kMaxS, ctx.ds()->gamma, sizeof(double) * s,
+                            cudaMemcpyDeviceToDevice, ctx.stream()));
+}
+
+}  // namespace
+
+void bicg_projection_host(Context& ctx, int64_t n, int s, const double* p, const double* block,
+                          const double* target, double* gamma) {
+  if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: 1 <= s <= 16");
+  DevPtr P = ctx.alloc_vecs(n, s), B = ctx.alloc_vecs(n, s), t = ctx.alloc_vecs(n, 1);
+  upload_cols(ctx, P->d(), p, n, s);
+  upload_cols(ctx, B->d(), block, n, s);
+  upload_cols(ctx, t->d(), target, n, 1);
+  project_dev(ctx, n, s, P->d(), B->d(), t->d(), 0);
+  CUDA_OK(cudaMemcpyAsync(gamma, ctx.ds()->gamma, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx.stream()));
+  ctx.sync();
+}
+
+void level_iteration_host(Context& ctx, const Operator& op, int s, int k, const double* p, double* x0,
+                          double* r_levels, double* v_levels) {
+  if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: 1 <= s <= 16");
+  if (k < 0 || k >= kMaxEll) throw Error(MSTAB_E_CONFIG, "b200: level 0 <= k < 8");
+  const int64_t n = op.n;
+  DevPtr P = ctx.alloc_vecs(n, s);
+  WSet D{ctx.alloc_vecs(n, 1), ctx.alloc_vecs(n, 1), ctx.alloc_vecs(n, s), ctx.alloc_vecs(n, s)};
+  std::vector<DevPtr> R(k + 2), VL(k + 2);
+  for (int i = 1; i <= k + 1; ++i) {
+    R[i] = ctx.alloc_vecs(n, 1);
+    VL[i] = ctx.alloc_vecs(n, s);
+  }
+  upload_cols(ctx, P->d(), p, n, s);
+  upload_cols(ctx, D.x->d(), x0, n, 1);
+  upload_cols(ctx, D.r->d(), r_levels, n, 1);
+  for (int i = 1; i <= k; ++i) upload_cols(ctx, R[i]->d(), r_levels + (size_t)i * n, n, 1);
+  upload_cols(ctx, D.U->d(), v_levels, n, s);                          // level -1
+  upload_cols(ctx, D.V->d(), v_levels + (size_t)n * s, n, s);          // level 0
+  for (int i = 1; i <= k; ++i) upload_cols(ctx, VL[i]->d(), v_levels + (size_t)(i + 1) * n * s, n, s);
+  // gamma_k = bicg_projection(P, V^(k), r^(k)) (idrstab.cpp:112); also leaves Ma = P^H V^(k)
+  project_dev(ctx, n, s, P->d(), k == 0 ? D.V->d() : VL[k]->d(), k == 0 ? D.r->d() : R[k]->d(), k);
+  reset_status(ctx);
+  enqueue_level(ctx, op, P->d(), s, k + 1, k, D, D, R, VL);
+  check_launch();
+  const CycleStatus& cs = read_status(ctx);
+  if (cs.breakdown) throw Error(MSTAB_E_SINGULAR, "solve_small: pivot collapse");
+  download_cols(ctx, x0, D.x->d(), n, 1);
+  download_cols(ctx, r_levels, D.r->d(), n, 1);
+  for (int i = 1; i <= k + 1; ++i) download_cols(ctx, r_levels + (size_t)i * n, R[i]->d(), n, 1);
+  download_cols(ctx, v_levels, D.U->d(), n, s);
+  download_cols(ctx, v_levels + (size_t)n * s, D.V->d(), n, s);
+  for (int i = 1; i <= k + 1; ++i) download_cols(ctx, v_levels + (size_t)(i + 1) * n * s, VL[i]->d(), n, s);
+  ctx.sync();
+}
+
+void poly_combination_host(Context& ctx, int64_t n, int s, int ell, const double* x0, const double* r_levels,
+                           const double* v_levels, double* x, double* r, double* u, double* v, double* tau,
+                           int32_t* tail_perturbed) {
+  if (s < 1 || s > kMaxS || ell < 1 || ell > kMaxEll) throw Error(MSTAB_E_CONFIG, "b200: s <= 16 and ell <= 8");
+  if (n < ell) throw Error(MSTAB_E_DIMENSION, "least_squares_tall: needs rows >= cols");
+  // the kernels take the length from an operator-free launch: a zero-entry operator of size n
+  // stands in for enqueue_poly's `op` (it only reads n and n_global)
+  Operator shape;
+  shape.n = n;
+  shape.n_global = n;
+  WSet D{ctx.alloc_vecs(n, 1), ctx.alloc_vecs(n, 1), ctx.alloc_vecs(n, s), ctx.alloc_vecs(n, s)};
+  std::vector<DevPtr> R(ell + 1), VL(ell + 1);
+  for (int i = 1; i <= ell; ++i) {
+    R[i] = ctx.alloc_vecs(n, 1);
+    VL[i] = ctx.alloc_vecs(n, s);
+  }
+  upload_cols(ctx, D.x->d(), x0, n, 1);
+  upload_cols(ctx, D.r->d(), r_levels, n, 1);
+  for (int i = 1; i <= ell; ++i) upload_cols(ctx, R[i]->d(), r_levels + (size_t)i * n, n, 1);
+  upload_cols(ctx, D.U->d(), v_levels, n, s);
+  upload_cols(ctx, D.V->d(), v_levels + (size_t)n * s, n, s);
+  for (int i = 1; i <= ell; ++i) upload_cols(ctx, VL[i]->d(), v_levels + (size_t)(i + 1) * n * s, n, s);
+  // P only feeds the next cycle's P^H r / P^H V reductions, which this helper discards
+  DevPtr P = ctx.alloc_vecs(n, s);
+  CUDA_OK(cudaMemsetAsync(P->ptr, 0, P->bytes, ctx.stream()));
+  reset_status(ctx);
+  enqueue_poly(ctx, shape, P->d(), s, ell, D, R, VL);
+  const CycleStatus& cs = read_status(ctx);
+  if (cs.breakdown == kBreakRank)
+    throw Error(MSTAB_E_RANK, "least_squares_tall: stabilization block lost rank");
+  for (int i = 0; i < ell; ++i) tau[i] = cs.tau[i];
+  if (tail_perturbed) *tail_perturbed = cs.tail_perturbed;
+  download_cols(ctx, x, D.x->d(), n, 1);
+  download_cols(ctx, r, D.r->d(), n, 1);
+  download_cols(ctx, u, D.U->d(), n, s);
+  download_cols(ctx, v, D.V->d(), n, s);
+  ctx.sync();
 }
 
 // sridr_solve (sridr.cpp:23-118): the recycled phase replays the donor's J relaxations with V

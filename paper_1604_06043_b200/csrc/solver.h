@@ -2,6 +2,7 @@
 #pragma once
 #include <complex>
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -46,6 +47,7 @@ struct StreamHolder {
   size_t cached_bytes = 0;
   void* take(size_t bytes);
   bool give(void* p, size_t bytes);
+  void drop_cache();  // releases every cached block (stream-ordered)
   ~StreamHolder();
 };
 
@@ -245,6 +247,21 @@ DevPtr make_cut_space(Context& ctx, int64_t n, int s, uint64_t seed);
 // arnoldi_init (idrstab.cpp:45-87) with rng seed `rng_seed` for the padding draws.
 void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s, uint64_t rng_seed,
                   double* U, double* V);
+// The same with the padding draws supplied by the caller (the reference draws them from the
+// caller's std::mt19937_64 through one std::normal_distribution per call, idrstab.cpp:60,77-78).
+void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s,
+                  const std::function<void(double*, int64_t)>& draw, double* U, double* V);
+// bicg_projection / level_iteration / poly_combination (idrstab.hpp:33-68) on the device, host
+// column-major blocks in and out. r_levels holds r^(0..k) on entry and r^(0..k+1) on return
+// (capacity n (k+2)); v_levels holds V^(-1..k) on entry and V^(-1..k+1) on return (capacity
+// n s (k+3)). Breakdowns throw with the reference's class codes (SINGULAR, RANK).
+void bicg_projection_host(Context& ctx, int64_t n, int s, const double* p, const double* block,
+                          const double* target, double* gamma);
+void level_iteration_host(Context& ctx, const Operator& op, int s, int k, const double* p, double* x0,
+                          double* r_levels, double* v_levels);
+void poly_combination_host(Context& ctx, int64_t n, int s, int ell, const double* x0, const double* r_levels,
+                           const double* v_levels, double* x, double* r, double* u, double* v, double* tau,
+                           int32_t* tail_perturbed);
 // Host-visible helpers for the kernel-level C entry points.
 const double* read_scal(Context& ctx, int count);
 const CycleStatus& read_status(Context& ctx);

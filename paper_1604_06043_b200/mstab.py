@@ -866,3 +866,102 @@ def arnoldi_init(a: CsrOperator, r0, s, rng_seed):
     mv = C.c_int64(0)
     _check(a.lib, a.lib.dll.mstab_kernel_arnoldi(a.ctx.h, a.h, dptr(r0), s, rng_seed, dptr(u), dptr(v), C.byref(mv)))
     return u.T, v.T, int(mv.value)
+
+
+NORMAL_FILL_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
+
+
+def arnoldi_init_draws(a: CsrOperator, r0, s, draw):
+    """arnoldi_init with the padding draws supplied by `draw(count) -> array of standard normals`
+    (the drop-in shim hands the caller's std::mt19937_64 through this entry point)."""
+    r0 = _f64(r0)
+    n = r0.size
+    u, v = np.empty((s, n)), np.empty((s, n))
+    mv = C.c_int64(0)
+
+    def fill(_user, out, count):
+        vals = np.ascontiguousarray(draw(int(count)), dtype=np.float64)
+        C.memmove(out, vals.ctypes.data, 8 * int(count))
+
+    cb = NORMAL_FILL_FN(fill)
+    _check(a.lib, a.lib.dll.mstab_kernel_arnoldi_cb(a.ctx.h, a.h, dptr(r0), s, C.cast(cb, C.c_void_p), None,
+                                                    dptr(u), dptr(v), C.byref(mv)))
+    return u.T, v.T, int(mv.value)
+
+
+def bicg_projection(p, block, target, ctx: Optional[Context] = None) -> np.ndarray:
+    """gamma with (P^H block) gamma = P^H target (idrstab.hpp:33-36); SingularProjection when singular."""
+    ctx = ctx if ctx is not None else default_context()
+    p, block = np.asfortranarray(_f64(p)), np.asfortranarray(_f64(block))
+    target = _f64(target)
+    n, s = p.shape
+    if block.shape != (n, s) or target.size != n:
+        raise DimensionMismatch("bicg_projection: shapes")
+    gamma = np.empty(s)
+    _check(ctx.lib, ctx.lib.dll.mstab_kernel_bicg_projection(ctx.h, n, s, p.ctypes.data_as(_capi._D),
+                                                             block.ctypes.data_as(_capi._D), dptr(target),
+                                                             dptr(gamma)))
+    return gamma
+
+
+class IterationState:
+    """Level vectors of one outer cycle (idrstab.hpp:38-46): r_levels[i] = r^(i), v_levels[i] = V^(i-1)."""
+
+    def __init__(self, x0, r_levels, v_levels):
+        self.x0, self.r_levels, self.v_levels = x0, r_levels, v_levels
+
+    @staticmethod
+    def start(x, r, u, v) -> "IterationState":
+        return IterationState(_f64(x).copy(), [_f64(r).copy()], [np.array(u, dtype=np.float64), np.array(v, dtype=np.float64)])
+
+    def v_level(self, level: int):
+        return self.v_levels[level + 1]
+
+
+def level_iteration(st: IterationState, a: CsrOperator, p, k: int, rep: Optional[SolveReport] = None) -> None:
+    """One IDR level iteration k on the device (idrstab.hpp:48-53): s + 1 operator applications."""
+    p = np.asfortranarray(_f64(p))
+    n, s = p.shape
+    if len(st.r_levels) < k + 1 or len(st.v_levels) < k + 2:
+        raise Error("level_iteration: missing levels")
+    x0 = _f64(st.x0).copy()
+    r = np.zeros((k + 2, n))
+    v = np.zeros((k + 3, s, n))
+    for i in range(k + 1):
+        r[i] = st.r_levels[i]
+    for i in range(k + 2):
+        v[i] = np.asarray(st.v_levels[i]).T
+    _check(a.lib, a.lib.dll.mstab_kernel_level_iteration(a.ctx.h, a.h, s, k, p.ctypes.data_as(_capi._D), dptr(x0),
+                                                         dptr(r), dptr(v)))
+    st.x0 = x0
+    st.r_levels = [r[i].copy() for i in range(k + 2)]
+    st.v_levels = [v[i].T.copy() for i in range(k + 3)]
+    if rep is not None:
+        rep.h_mv += s + 1
+
+
+@dataclass
+class PolyOut:
+    x: np.ndarray
+    r: np.ndarray
+    u: np.ndarray
+    v: np.ndarray
+    tau: np.ndarray
+    tail_perturbed: bool
+
+
+def poly_combination(st: IterationState, ell: int, ctx: Optional[Context] = None) -> PolyOut:
+    """Degree-ell residual minimisation on the device (idrstab.hpp:55-68); RankDeficient when Z lost rank."""
+    ctx = ctx if ctx is not None else default_context()
+    n = st.x0.size
+    s = np.asarray(st.v_levels[0]).shape[1]
+    if len(st.r_levels) < ell + 1 or len(st.v_levels) < ell + 2:
+        raise Error("poly_combination: missing levels")
+    r = np.ascontiguousarray(np.stack([_f64(st.r_levels[i]) for i in range(ell + 1)]))
+    v = np.ascontiguousarray(np.stack([np.asarray(st.v_levels[i], dtype=np.float64).T for i in range(ell + 2)]))
+    x0 = _f64(st.x0)
+    x, rr, u, vv, tau = np.empty(n), np.empty(n), np.empty((s, n)), np.empty((s, n)), np.empty(ell)
+    pert = C.c_int32(0)
+    _check(ctx.lib, ctx.lib.dll.mstab_kernel_poly_combination(ctx.h, n, s, ell, dptr(x0), dptr(r), dptr(v), dptr(x),
+                                                              dptr(rr), dptr(u), dptr(vv), dptr(tau), C.byref(pert)))
+    return PolyOut(x, rr, u.T.copy(), vv.T.copy(), tau, bool(pert.value))

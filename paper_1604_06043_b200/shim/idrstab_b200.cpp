@@ -6,9 +6,13 @@
 //
 // (proj/core/include/mstab/solvers/idrstab.hpp:88-96) defined on top of the B200 C-ABI
 // (include/mstab_b200.h), so a reference build that compiles this file instead of the two entry
-// points of src/idrstab.cpp runs every solve on the GPU. Everything else of
-// the reference library (CsrMatrix, CsrOperator, RecycleData, fetch/validate/save/load, the
-// harness, SRIDR and the level_iteration/poly_combination helpers) stays the reference's own.
+// points of src/idrstab.cpp runs every solve on the GPU. The test-visible
+// helpers of the same header (idrstab.hpp:27-68: arnoldi_init, bicg_projection,
+// IterationState::start, level_iteration, poly_combination) are defined here too, device-backed
+// through the kernel-level C-ABI (include/mstab_b200_kernels.h: host blocks copied in, the solve
+// loop's own kernels, results copied out), so this file replaces src/idrstab.cpp as a whole.
+// Everything else of the reference library (CsrMatrix, CsrOperator, RecycleData,
+// fetch/validate/save/load, the harness) stays the reference's own.
 //
 // Behaviour kept from idrstab.cpp:193-307:
 //   * check order: SolverConfig::validate (report.cpp:16-22) -> DimensionMismatch for b / x0
@@ -24,6 +28,7 @@
 #include <cstdint>
 #include <list>
 #include <memory>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -38,6 +43,7 @@
 #include "mstab/solvers/sridr.hpp"
 #include "mstab/types.hpp"
 #include "mstab_b200.h"
+#include "mstab_b200_kernels.h"
 
 namespace mstab {
 
@@ -397,6 +403,133 @@ std::pair<Vector, SolveReport> bicgstab_solve(const LinearOperator& a, const Vec
   std::pair<Vector, SolveReport> out;
   read_result(ss, res, n, 1, out.first, out.second);
   out.second.omega_history.clear();
+  return out;
+}
+
+// ---- the test-visible helpers (idrstab.hpp:27-68), device-backed --------------------------------
+namespace {
+
+std::vector<double> dense_real(const DenseMatrix& m, const char* what) { return real_parts(m.data(), what); }
+
+DenseMatrix dense_from(const double* a, size_t n, size_t s) {
+  DenseMatrix m(n, s);
+  for (size_t i = 0; i < n * s; ++i) m.data()[i] = Complex(a[i]);
+  return m;
+}
+
+struct DrawCtx {
+  std::mt19937_64* rng;
+  std::normal_distribution<double> normal{0.0, 1.0};  // one per arnoldi_init call (idrstab.cpp:60)
+};
+void draw_normals(void* user, double* out, int64_t count) {
+  auto* d = static_cast<DrawCtx*>(user);
+  for (int64_t i = 0; i < count; ++i) out[i] = d->normal(*d->rng);  // real problems: one draw per entry (:77-78)
+}
+
+}  // namespace
+
+ArnoldiResult arnoldi_init(const LinearOperator& a, std::span<const Complex> r0, std::size_t s,
+                           std::mt19937_64& rng) {
+  const std::size_t n = a.size();
+  if (s < 1) throw ConfigError("arnoldi_init: s >= 1 required");
+  if (r0.size() != n) throw DimensionMismatch("arnoldi_init: start vector length");
+  Session& ss = session();
+  mstab_operator* op = device_operator(ss, a);
+  const auto r = real_parts(r0, "start vector");
+  std::vector<double> u(n * s), v(n * s);
+  DrawCtx dc{&rng};
+  int64_t mv = 0;
+  check(mstab_kernel_arnoldi_cb(ss.ctx, op, r.data(), (int64_t)s, draw_normals, &dc, u.data(), v.data(), &mv));
+  ArnoldiResult res;
+  res.u = dense_from(u.data(), n, s);
+  res.v = dense_from(v.data(), n, s);
+  res.mv_cost = mv;
+  return res;
+}
+
+Vector bicg_projection(const DenseMatrix& p, const DenseMatrix& block, std::span<const Complex> target) {
+  const std::size_t n = p.rows(), s = p.cols();
+  if (block.rows() != n || block.cols() != s || target.size() != n)
+    throw DimensionMismatch("bicg_projection: shapes");
+  Session& ss = session();
+  const auto pp = dense_real(p, "P"), bb = dense_real(block, "block"), tt = real_parts(target, "target");
+  std::vector<double> g(s);
+  check(mstab_kernel_bicg_projection(ss.ctx, (int64_t)n, (int64_t)s, pp.data(), bb.data(), tt.data(), g.data()));
+  Vector out(s);
+  for (std::size_t i = 0; i < s; ++i) out[i] = Complex(g[i]);
+  return out;
+}
+
+IterationState IterationState::start(Vector x, Vector r, DenseMatrix u, DenseMatrix v) {
+  IterationState st;
+  st.x0 = std::move(x);
+  st.r_levels.push_back(std::move(r));
+  st.v_levels.push_back(std::move(u));  // level -1
+  st.v_levels.push_back(std::move(v));  // level 0
+  return st;
+}
+
+void level_iteration(IterationState& st, const LinearOperator& a, const DenseMatrix& p, std::size_t k,
+                     SolveReport& rep) {
+  const std::size_t n = a.size(), s = p.cols();
+  if (st.r_levels.size() < k + 1 || st.v_levels.size() < k + 2) throw Error("level_iteration: missing levels");
+  Session& ss = session();
+  mstab_operator* op = device_operator(ss, a);
+  const auto pp = dense_real(p, "P");
+  auto x0 = real_parts(st.x0, "x0");
+  std::vector<double> r((k + 2) * n), v((k + 3) * n * s);
+  for (std::size_t i = 0; i <= k; ++i) {
+    const auto ri = real_parts(st.r_levels[i], "residual level");
+    std::copy(ri.begin(), ri.end(), r.begin() + (std::ptrdiff_t)(i * n));
+  }
+  for (std::size_t i = 0; i <= k + 1; ++i) {
+    const auto vi = dense_real(st.v_levels[i], "auxiliary level");
+    std::copy(vi.begin(), vi.end(), v.begin() + (std::ptrdiff_t)(i * n * s));
+  }
+  check(mstab_kernel_level_iteration(ss.ctx, op, (int64_t)s, (int64_t)k, pp.data(), x0.data(), r.data(), v.data()));
+  for (std::size_t t = 0; t < n; ++t) st.x0[t] = Complex(x0[t]);
+  st.r_levels.resize(k + 1);
+  st.v_levels.resize(k + 2);
+  for (std::size_t i = 0; i <= k; ++i)
+    for (std::size_t t = 0; t < n; ++t) st.r_levels[i][t] = Complex(r[i * n + t]);
+  Vector rnew(n);
+  for (std::size_t t = 0; t < n; ++t) rnew[t] = Complex(r[(k + 1) * n + t]);
+  st.r_levels.push_back(std::move(rnew));
+  for (std::size_t i = 0; i <= k + 1; ++i) st.v_levels[i] = dense_from(v.data() + i * n * s, n, s);
+  st.v_levels.push_back(dense_from(v.data() + (k + 2) * n * s, n, s));
+  rep.h_mv += (std::int64_t)(s + 1);
+}
+
+PolyOut poly_combination(const IterationState& st, std::size_t ell) {
+  const std::size_t n = st.x0.size();
+  const std::size_t s = st.v_levels[0].cols();
+  if (st.r_levels.size() < ell + 1 || st.v_levels.size() < ell + 2) throw Error("poly_combination: missing levels");
+  Session& ss = session();
+  const auto x0 = real_parts(st.x0, "x0");
+  std::vector<double> r((ell + 1) * n), v((ell + 2) * n * s);
+  for (std::size_t i = 0; i <= ell; ++i) {
+    const auto ri = real_parts(st.r_levels[i], "residual level");
+    std::copy(ri.begin(), ri.end(), r.begin() + (std::ptrdiff_t)(i * n));
+  }
+  for (std::size_t i = 0; i <= ell + 1; ++i) {
+    const auto vi = dense_real(st.v_levels[i], "auxiliary level");
+    std::copy(vi.begin(), vi.end(), v.begin() + (std::ptrdiff_t)(i * n * s));
+  }
+  std::vector<double> x(n), rr(n), u(n * s), vv(n * s), tau(ell);
+  int32_t pert = 0;
+  check(mstab_kernel_poly_combination(ss.ctx, (int64_t)n, (int64_t)s, (int64_t)ell, x0.data(), r.data(), v.data(),
+                                      x.data(), rr.data(), u.data(), vv.data(), tau.data(), &pert));
+  PolyOut out;
+  out.x.resize(n);
+  out.r.resize(n);
+  for (std::size_t t = 0; t < n; ++t) {
+    out.x[t] = Complex(x[t]);
+    out.r[t] = Complex(rr[t]);
+  }
+  out.u = dense_from(u.data(), n, s);
+  out.v = dense_from(vv.data(), n, s);
+  for (std::size_t i = 0; i < ell; ++i) out.tau.emplace_back(tau[i]);
+  out.tail_perturbed = pert != 0;
   return out;
 }
 

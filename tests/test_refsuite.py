@@ -41,3 +41,21 @@ def test_reference_suite_on_reference(suite):
 def test_reference_suite_on_b200_shim(suite):
     """The reference's assertions hold with every solve routed through the B200 shim."""
     assert run_suite(SUITE_DIR / f"b200_{suite}") > 0
+
+
+@pytest.mark.gpu
+def test_helper_cases_launch_kernels_through_the_shim():
+    """The Arnoldi / BicgProjection / LevelIteration / PolyCombination cases of test_solvers.cpp run
+    the shim's device-backed helpers: the library reports the kernels it launched at exit."""
+    import os
+    path = SUITE_DIR / "b200_test_solvers"
+    if not path.exists():
+        pytest.fail(f"{path.relative_to(ROOT)} missing: run `make ref` where /root/reference exists")
+    env = dict(os.environ, MSTAB_REPORT_LAUNCHES="1")
+    p = subprocess.run([str(path), "--gtest_filter=Arnoldi.*:BicgProjection.*:LevelIteration.*:PolyCombination.*"],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert p.returncode == 0, (p.stdout[-3000:], p.stderr[-3000:])
+    ran = [ln for ln in p.stdout.splitlines() if ln.startswith("[ RUN")]
+    assert len(ran) >= 10, p.stdout[-2000:]
+    line = [ln for ln in p.stderr.splitlines() if ln.startswith("[mstab] kernel launches:")]
+    assert line and int(line[-1].split(":")[1]) > 100, p.stderr[-1000:]
