@@ -43,6 +43,12 @@ int mstab_kernel_arnoldi_cb(mstab_context* ctx, const mstab_operator* op, const 
 int mstab_kernel_bicg_projection(mstab_context* ctx, int64_t n, int64_t s, const double* p,
                                  const double* block, const double* target, double* gamma);
 
+/* The two reductions of bicg_projection without the solve: m = P^T block (s x s, column-major) and
+ * g = P^T target (s). The shim assembles the complex P^H block / P^H target of a complex call from
+ * four of these (real and imaginary parts) and solves the s x s system with solve_small. */
+int mstab_kernel_projection_gram(mstab_context* ctx, int64_t n, int64_t s, const double* p,
+                                 const double* block, const double* target, double* m, double* g);
+
 /* level_iteration (idrstab.cpp:105-152), level k of IterationState (idrstab.hpp:38-46):
  *   x0        n               in/out
  *   r_levels  n x (k + 2)     r^(0..k) on entry, r^(0..k+1) on return

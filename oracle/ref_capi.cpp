@@ -567,6 +567,16 @@ int mstab_kernel_bicg_projection(mstab_context*, int64_t n, int64_t s, const dou
   });
 }
 
+int mstab_kernel_projection_gram(mstab_context*, int64_t n, int64_t s, const double* p, const double* block,
+                                 const double* target, double* m, double* g) {
+  return guarded([&] {
+    const mstab::DenseMatrix pm = to_dense(p, n, s);
+    from_dense(mstab::gemm(mstab::adjoint(pm), to_dense(block, n, s)), m);
+    const mstab::Vector gv = mstab::gemv_adjoint(pm, to_vec(target, n));
+    for (int64_t i = 0; i < s; ++i) g[i] = gv[(size_t)i].real();
+  });
+}
+
 int mstab_kernel_level_iteration(mstab_context*, const mstab_operator* op, int64_t s, int64_t k, const double* p,
                                  double* x0, double* r_levels, double* v_levels) {
   return guarded([&] {

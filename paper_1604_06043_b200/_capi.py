@@ -160,6 +160,7 @@ KERNEL_ABI = [
     ("mstab_kernel_arnoldi", C.c_int, [_P, _P, _D, C.c_int64, C.c_uint64, _D, _D, _I64]),
     ("mstab_kernel_arnoldi_cb", C.c_int, [_P, _P, _D, C.c_int64, C.c_void_p, C.c_void_p, _D, _D, _I64]),
     ("mstab_kernel_bicg_projection", C.c_int, [_P, C.c_int64, C.c_int64, _D, _D, _D, _D]),
+    ("mstab_kernel_projection_gram", C.c_int, [_P, C.c_int64, C.c_int64, _D, _D, _D, _D, _D]),
     ("mstab_kernel_level_iteration", C.c_int, [_P, _P, C.c_int64, C.c_int64, _D, _D, _D, _D]),
     ("mstab_kernel_poly_combination", C.c_int,
      [_P, C.c_int64, C.c_int64, C.c_int64, _D, _D, _D, _D, _D, _D, _D, _D, C.POINTER(C.c_int32)]),

@@ -594,6 +594,15 @@ int mstab_kernel_bicg_projection(mstab_context* ctx, int64_t n, int64_t s, const
   });
 }
 
+int mstab_kernel_projection_gram(mstab_context* ctx, int64_t n, int64_t s, const double* p,
+                                 const double* block, const double* target, double* m, double* g) {
+  return guarded([&] {
+    bind(ctx);
+    if (n < 1) throw Error(MSTAB_E_DIMENSION, "projection_gram: empty vectors");
+    projection_gram_host(*ctx->impl, n, (int)s, p, block, target, m, g);
+  });
+}
+
 int mstab_kernel_level_iteration(mstab_context* ctx, const mstab_operator* op, int64_t s, int64_t k,
                                  const double* p, double* x0, double* r_levels, double* v_levels) {
   return guarded([&] {

@@ -1359,6 +1359,22 @@ void bicg_projection_host(Context& ctx, int64_t n, int s, const double* p, const
   ctx.sync();
 }
 
+void projection_gram_host(Context& ctx, int64_t n, int s, const double* p, const double* block,
+                          const double* target, double* m, double* g) {
+  if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: 1 <= s <= 16");
+  DevPtr P = ctx.alloc_vecs(n, s), B = ctx.alloc_vecs(n, s), t = ctx.alloc_vecs(n, 1);
+  upload_cols(ctx, P->d(), p, n, s);
+  upload_cols(ctx, B->d(), block, n, s);
+  upload_cols(ctx, t->d(), target, n, 1);
+  reset_status(ctx);
+  launch_prologue(ctx.stream(), n, ctx.ld(n), s, P->d(), B->d(), t->d(), ctx.reducer());
+  check_launch();
+  after_poly(ctx, s);
+  CUDA_OK(cudaMemcpyAsync(m, ctx.ds()->Ma, sizeof(double) * s * s, cudaMemcpyDeviceToHost, ctx.stream()));
+  CUDA_OK(cudaMemcpyAsync(g, ctx.ds()->g, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx.stream()));
+  ctx.sync();
+}
+
 void level_iteration_host(Context& ctx, const Operator& op, int s, int k, const double* p, double* x0,
                           double* r_levels, double* v_levels) {
   if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: 1 <= s <= 16");

@@ -257,6 +257,8 @@ void arnoldi_init(Context& ctx, const Operator& op, const double* r0, int s,
 // n s (k+3)). Breakdowns throw with the reference's class codes (SINGULAR, RANK).
 void bicg_projection_host(Context& ctx, int64_t n, int s, const double* p, const double* block,
                           const double* target, double* gamma);
+void projection_gram_host(Context& ctx, int64_t n, int s, const double* p, const double* block,
+                          const double* target, double* m, double* g);
 void level_iteration_host(Context& ctx, const Operator& op, int s, int k, const double* p, double* x0,
                           double* r_levels, double* v_levels);
 void poly_combination_host(Context& ctx, int64_t n, int s, int ell, const double* x0, const double* r_levels,

@@ -34,6 +34,7 @@
 
 #include "mstab/csr.hpp"
 #include "mstab/errors.hpp"
+#include "mstab/kernels.hpp"
 #include "mstab/operator.hpp"
 #include "mstab/precond.hpp"
 #include "mstab/recycle.hpp"
@@ -447,11 +448,52 @@ ArnoldiResult arnoldi_init(const LinearOperator& a, std::span<const Complex> r0,
   return res;
 }
 
+namespace {
+bool all_real(std::span<const Complex> v) {
+  for (const Complex& z : v)
+    if (z.imag() != 0.0) return false;
+  return true;
+}
+void split(std::span<const Complex> v, std::vector<double>& re, std::vector<double>& im) {
+  re.resize(v.size());
+  im.resize(v.size());
+  for (size_t i = 0; i < v.size(); ++i) {
+    re[i] = v[i].real();
+    im[i] = v[i].imag();
+  }
+}
+}  // namespace
+
 Vector bicg_projection(const DenseMatrix& p, const DenseMatrix& block, std::span<const Complex> target) {
   const std::size_t n = p.rows(), s = p.cols();
   if (block.rows() != n || block.cols() != s || target.size() != n)
     throw DimensionMismatch("bicg_projection: shapes");
   Session& ss = session();
+  if (!all_real(p.data()) || !all_real(block.data()) || !all_real(target)) {
+    // Complex data (the reference's BicgProjection tests): the length-n reductions still run on
+    // the device, on real and imaginary parts,
+    //   P^H B = (Pr^T Br + Pi^T Bi) + i (Pr^T Bi - Pi^T Br),  P^H t likewise,
+    // and the s x s complex system goes to the reference's own solve_small (kernels.cpp:150-154).
+    std::vector<double> pr, pi, br, bi, tr, ti;
+    split(p.data(), pr, pi);
+    split(block.data(), br, bi);
+    split(target, tr, ti);
+    std::vector<double> m[4], g[4];
+    const double* lhs[4] = {pr.data(), pi.data(), pr.data(), pi.data()};
+    const double* rb[4] = {br.data(), bi.data(), bi.data(), br.data()};
+    const double* rt[4] = {tr.data(), ti.data(), ti.data(), tr.data()};
+    for (int k = 0; k < 4; ++k) {
+      m[k].resize(s * s);
+      g[k].resize(s);
+      check(mstab_kernel_projection_gram(ss.ctx, (int64_t)n, (int64_t)s, lhs[k], rb[k], rt[k], m[k].data(),
+                                         g[k].data()));
+    }
+    DenseMatrix msys(s, s);
+    Vector rhs(s);
+    for (std::size_t i = 0; i < s * s; ++i) msys.data()[i] = Complex(m[0][i] + m[1][i], m[2][i] - m[3][i]);
+    for (std::size_t i = 0; i < s; ++i) rhs[i] = Complex(g[0][i] + g[1][i], g[2][i] - g[3][i]);
+    return solve_small(msys, rhs);
+  }
   const auto pp = dense_real(p, "P"), bb = dense_real(block, "block"), tt = real_parts(target, "target");
   std::vector<double> g(s);
   check(mstab_kernel_bicg_projection(ss.ctx, (int64_t)n, (int64_t)s, pp.data(), bb.data(), tt.data(), g.data()));
