@@ -307,6 +307,27 @@ int mstab_context_comm_info(mstab_context* ctx, int32_t* rank, int32_t* world);
 int mstab_operator_create_csr_slab(mstab_context* ctx, int64_t n, const int64_t* row_ptr,
                                    const int64_t* col_idx, const double* values,
                                    const int64_t* slab_starts, mstab_operator** out);
+/* The same slab from the rank's OWN rows, for systems no rank can hold whole (c4: 1.5e9 entries):
+ * row_ptr (local, from 0, n_local + 1 entries), col_idx (GLOBAL column indices) and values of rows
+ * [slab_starts[rank], slab_starts[rank+1]). What the global form derives from the whole matrix is
+ * passed in instead:
+ *   col_spans    2 x world: [lo_r, hi_r) = the column range rank r's rows reference (each rank
+ *                computes its own pair and the caller allgathers them); the halo plans of all ranks
+ *                follow from these and match by construction;
+ *   fingerprint  the reference checksum of the GLOBAL matrix (csr.cpp:28-43), folded over the ranks
+ *                with mstab_fnv_* below (three relays: row_ptr, col_idx, values), or any value
+ *                agreed by all ranks when .mrd interchange with the reference is not needed. */
+int mstab_operator_create_csr_slab_local(mstab_context* ctx, int64_t n_global, const int64_t* slab_starts,
+                                         const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                                         const int64_t* col_spans, uint64_t fingerprint, mstab_operator** out);
+/* The reference's CSR checksum as a resumable fold (FNV-1a over dims, every row_ptr entry, every
+ * col_idx entry, every value as complex<double>): h = mstab_fnv_begin(n, n, nnz); then in rank
+ * order h = mstab_fnv_fold_index(h, row_ptr_local + (rank ? 1 : 0), count, first_entry_of_slab)
+ * (local offsets rebased by `add`), again in rank order over col_idx (add = 0), and again over the
+ * values. The state is 8 bytes: pass it to the next rank between folds. */
+uint64_t mstab_fnv_begin(int64_t n_rows, int64_t n_cols, int64_t nnz);
+uint64_t mstab_fnv_fold_index(uint64_t h, const int64_t* v, int64_t count, int64_t add);
+uint64_t mstab_fnv_fold_values(uint64_t h, const double* values, int64_t count);
 /* First global row of the operator's slab (0 for a whole-matrix operator); size() is the
  * number of local rows. */
 int64_t mstab_operator_row_begin(const mstab_operator* op);

@@ -25,6 +25,13 @@ int64_t mstab_gen_convdiff_nnz(int32_t dim, int64_t n, int32_t stencil);
 /* Fills row_ptr (N+1), col_idx (nnz), values (nnz); N = n^dim. beta has 3 entries. */
 int mstab_gen_convdiff(int32_t dim, int64_t n, int32_t stencil, const double* beta, double dt,
                        int64_t* row_ptr, int64_t* col_idx, double* values);
+/* Rows [row0, row1) of the same matrix: row_ptr local (from 0, row1 - row0 + 1 entries), col_idx
+ * GLOBAL column indices. Returns the entry count of the range; with row_ptr = col_idx = values =
+ * NULL it only counts (a rank of a row-sharded run generates its own slab: no process holds the
+ * global matrix). */
+int64_t mstab_gen_convdiff_rows(int32_t dim, int64_t n, int32_t stencil, const double* beta, double dt,
+                                int64_t row0, int64_t row1, int64_t* row_ptr, int64_t* col_idx,
+                                double* values);
 /* std::mt19937_64(seed) + std::uniform_real_distribution<double>(0,1): `count` draws. For the
  * conv-diff sequences the first N draws are x0 and the next N are f. */
 int mstab_gen_uniform(uint64_t seed, int64_t count, double* out);

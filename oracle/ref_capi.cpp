@@ -262,6 +262,39 @@ int mstab_operator_create_csr_slab(mstab_context*, int64_t, const int64_t*, cons
                                    const int64_t*, mstab_operator**) {
   return mstab_nccl_unique_id(nullptr);
 }
+int mstab_operator_create_csr_slab_local(mstab_context*, int64_t, const int64_t*, const int64_t*, const int64_t*,
+                                         const double*, const int64_t*, uint64_t, mstab_operator**) {
+  return mstab_nccl_unique_id(nullptr);
+}
+// The resumable checksum fold: the reference's own mixing (csr.cpp:28-43), byte for byte.
+namespace {
+uint64_t fnv_mix(uint64_t h, const void* p, size_t len) {
+  const unsigned char* b = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < len; ++i) {
+    h ^= b[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+}  // namespace
+uint64_t mstab_fnv_begin(int64_t n_rows, int64_t n_cols, int64_t nnz) {
+  const uint64_t dims[3] = {(uint64_t)n_rows, (uint64_t)n_cols, (uint64_t)nnz};
+  return fnv_mix(1469598103934665603ull, dims, sizeof(dims));
+}
+uint64_t mstab_fnv_fold_index(uint64_t h, const int64_t* v, int64_t count, int64_t add) {
+  for (int64_t i = 0; i < count; ++i) {
+    const uint64_t w = (uint64_t)(v[i] + add);
+    h = fnv_mix(h, &w, sizeof(w));
+  }
+  return h;
+}
+uint64_t mstab_fnv_fold_values(uint64_t h, const double* values, int64_t count) {
+  for (int64_t k = 0; k < count; ++k) {
+    const Complex z(values[k], 0.0);
+    h = fnv_mix(h, &z, sizeof(z));
+  }
+  return h;
+}
 int64_t mstab_operator_row_begin(const mstab_operator*) { return 0; }
 int64_t mstab_operator_global_size(const mstab_operator* op) { return (int64_t)op->m.n_rows; }
 

@@ -8,5 +8,5 @@ from .mstab import (  # noqa: F401
     make_cut_space, mstab_solve, save, solve_small, validate, PrecondKind, SplitPreconditioner,
     PreconditionedOperator, ZeroPivot, build_ilu0, build_jacobi, build_none, preconditioned_rhs,
     unpreconditioned_solution, MissingOmegas, sridr_solve, bicg_solve, bicgstab_solve, gmres_solve,
-    IterationState, PolyOut, arnoldi_init_draws, bicg_projection, level_iteration, poly_combination)
+    IterationState, PolyOut, arnoldi_init_draws, distributed_fingerprint, local_col_span, bicg_projection, level_iteration, poly_combination)
 from ._capi import Lib, PRODUCT_LIB  # noqa: F401

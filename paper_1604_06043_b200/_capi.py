@@ -133,6 +133,11 @@ ABI += [
     ("mstab_context_set_comm_host", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(HostCommC)]),
     ("mstab_context_comm_info", C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     ("mstab_operator_create_csr_slab", C.c_int, [_P, C.c_int64, _I64, _I64, _D, _I64, C.POINTER(_P)]),
+    ("mstab_operator_create_csr_slab_local", C.c_int,
+     [_P, C.c_int64, _I64, _I64, _I64, _D, _I64, C.c_uint64, C.POINTER(_P)]),
+    ("mstab_fnv_begin", C.c_uint64, [C.c_int64, C.c_int64, C.c_int64]),
+    ("mstab_fnv_fold_index", C.c_uint64, [C.c_uint64, _I64, C.c_int64, C.c_int64]),
+    ("mstab_fnv_fold_values", C.c_uint64, [C.c_uint64, _D, C.c_int64]),
     ("mstab_operator_row_begin", C.c_int64, [_P]),
     ("mstab_operator_global_size", C.c_int64, [_P]),
 ]
@@ -170,6 +175,8 @@ KERNEL_ABI = [
 GEN_ABI = [
     ("mstab_gen_convdiff_nnz", C.c_int64, [C.c_int32, C.c_int64, C.c_int32]),
     ("mstab_gen_convdiff", C.c_int, [C.c_int32, C.c_int64, C.c_int32, _D, C.c_double, _I64, _I64, _D]),
+    ("mstab_gen_convdiff_rows", C.c_int64,
+     [C.c_int32, C.c_int64, C.c_int32, _D, C.c_double, C.c_int64, C.c_int64, _I64, _I64, _D]),
     ("mstab_gen_uniform", C.c_int, [C.c_uint64, C.c_int64, _D]),
     ("mstab_gen_euler_rhs", None, [C.c_int64, _D, _D, C.c_double, C.c_double, _D]),
     ("mstab_gen_banded", C.c_int, [C.c_int64, C.c_int32, C.c_int64, C.c_uint64, _I64, _I64, _D]),

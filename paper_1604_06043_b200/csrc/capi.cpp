@@ -148,6 +148,26 @@ int mstab_operator_create_csr_slab(mstab_context* ctx, int64_t n, const int64_t*
   });
 }
 
+int mstab_operator_create_csr_slab_local(mstab_context* ctx, int64_t n_global, const int64_t* slab_starts,
+                                         const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                                         const int64_t* col_spans, uint64_t fingerprint, mstab_operator** out) {
+  return guarded([&] {
+    bind(ctx);
+    auto o = std::make_unique<mstab_operator>();
+    o->impl = make_operator_slab_local(*ctx->impl, n_global, slab_starts, row_ptr, col_idx, values, col_spans,
+                                       fingerprint);
+    *out = o.release();
+  });
+}
+
+uint64_t mstab_fnv_begin(int64_t n_rows, int64_t n_cols, int64_t nnz) { return fnv_begin(n_rows, n_cols, nnz); }
+uint64_t mstab_fnv_fold_index(uint64_t h, const int64_t* v, int64_t count, int64_t add) {
+  return fnv_fold_u64(h, v, count, add);
+}
+uint64_t mstab_fnv_fold_values(uint64_t h, const double* values, int64_t count) {
+  return fnv_fold_values(h, values, count);
+}
+
 int64_t mstab_operator_row_begin(const mstab_operator* op) { return op->impl->row0; }
 int64_t mstab_operator_global_size(const mstab_operator* op) { return op->impl->n_global; }
 
@@ -727,7 +747,7 @@ void mstab_profiling_reset(void) {
 
 const char* mstab_kernel_class_name(int32_t cls) {
   static const char* names[kKNumClasses] = {"spmv_ph", "level_update", "rebuild_top", "rebuild_deferred",
-                                            "ls_tsqr", "poly", "prologue", "validate", "other"};
+                                            "ls_tsqr", "poly", "prologue", "validate", "other", "persist_cycle"};
   return (cls >= 0 && cls < kKNumClasses) ? names[cls] : "?";
 }
 

@@ -17,7 +17,10 @@ constexpr int kMaxGrid = 148 * 8;
 constexpr int kMaxXred = 2 + 2 * kMaxS * kMaxS + 6;  // largest split payload (validate)
 
 // Breakdown codes written by the device finalizers (idrstab.cpp:290-293 reasons).
-enum : int32_t { kBreakNone = 0, kBreakSingular = 1, kBreakRank = 2 };
+// kBreakFallback is not a breakdown of the method: the persistent cycle kernel (kpersist.cu) asks
+// the host to rerun the cycle on the stream-of-kernels path (its least squares left the
+// CholeskyQR2 regime); the host never reports it.
+enum : int32_t { kBreakNone = 0, kBreakSingular = 1, kBreakRank = 2, kBreakFallback = 3 };
 
 // Small, per-solve scalar state living in device memory. The "status" head is copied back to
 // the host once per cycle (one small D2H); the rest stays on the device.

@@ -42,6 +42,13 @@ int64_t mstab_gen_convdiff_nnz(int32_t dim, int64_t n, int32_t stencil) {
 
 int mstab_gen_convdiff(int32_t dim, int64_t n, int32_t stencil, const double* beta, double dt,
                        int64_t* row_ptr, int64_t* col_idx, double* values) {
+  const int64_t N = dim == 3 ? n * n * n : n * n;
+  return mstab_gen_convdiff_rows(dim, n, stencil, beta, dt, 0, N, row_ptr, col_idx, values) < 0 ? -3 : 0;
+}
+
+int64_t mstab_gen_convdiff_rows(int32_t dim, int64_t n, int32_t stencil, const double* beta, double dt,
+                                int64_t row0, int64_t row1, int64_t* row_ptr, int64_t* col_idx,
+                                double* values) {
   const std::vector<Nb> offs = stencil_offsets(dim, stencil);
   if (offs.empty() || n < 1) return -3;
   const double h = 1.0 / (double)(n + 1);
@@ -62,10 +69,10 @@ int mstab_gen_convdiff(int32_t dim, int64_t n, int32_t stencil, const double* be
     off_upwind[d] = off_plain - h * beta[d];
   }
   int64_t k_nz = 0;
-  row_ptr[0] = 0;
-  for (int64_t z = 0; z < nz; ++z)
-    for (int64_t y = 0; y < n; ++y)
-      for (int64_t x = 0; x < n; ++x) {
+  if (row_ptr) row_ptr[0] = 0;
+  for (int64_t row = row0; row < row1; ++row) {
+      const int64_t x = row % n, y = (row / n) % n, z = row / (n * n);
+      {
         for (const Nb& o : offs) {
           const int64_t xx = x + o.dx, yy = y + o.dy, zz = z + o.dz;
           if (xx < 0 || xx >= n || yy < 0 || yy >= n || zz < 0 || zz >= nz) continue;
@@ -79,13 +86,16 @@ int mstab_gen_convdiff(int32_t dim, int64_t n, int32_t stencil, const double* be
           } else {
             v = off_plain;
           }
-          col_idx[k_nz] = (zz * n + yy) * n + xx;
-          values[k_nz] = v;
+          if (col_idx) {
+            col_idx[k_nz] = (zz * n + yy) * n + xx;
+            values[k_nz] = v;
+          }
           ++k_nz;
         }
-        row_ptr[(z * n + y) * n + x + 1] = k_nz;
+        if (row_ptr) row_ptr[row - row0 + 1] = k_nz;
       }
-  return 0;
+  }
+  return k_nz;
 }
 
 int mstab_gen_uniform(uint64_t seed, int64_t count, double* out) {

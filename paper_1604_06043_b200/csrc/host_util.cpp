@@ -67,6 +67,30 @@ uint64_t fnv_csr_fingerprint(int64_t n, const int64_t* row_ptr, const int64_t* c
   return h;
 }
 
+// The same fold, resumable: a rank that holds only a slice of the matrix continues the hash a
+// peer started (csr.cpp:28-43 folds dims, then every row_ptr entry, then every col_idx entry, then
+// every value, so a distributed matrix is hashed in three relays over the ranks).
+uint64_t fnv_begin(int64_t n_rows, int64_t n_cols, int64_t nnz) {
+  static const U64Mixer mx;
+  uint64_t h = kFnvOffset;
+  h = mx.mix(h, (uint64_t)n_rows);
+  h = mx.mix(h, (uint64_t)n_cols);
+  return mx.mix(h, (uint64_t)nnz);
+}
+uint64_t fnv_fold_u64(uint64_t h, const int64_t* v, int64_t count, int64_t add) {
+  static const U64Mixer mx;
+  for (int64_t i = 0; i < count; ++i) h = mx.mix(h, (uint64_t)(v[i] + add));
+  return h;
+}
+uint64_t fnv_fold_values(uint64_t h, const double* values, int64_t count) {
+  static const U64Mixer mx;
+  for (int64_t k = 0; k < count; ++k) {
+    h = fnv_bytes(h, reinterpret_cast<const unsigned char*>(values + k), sizeof(double));
+    h *= mx.pow[8];  // imaginary part +0.0: eight zero bytes
+  }
+  return h;
+}
+
 std::vector<double> symmetric_eigenvalues(const double* h, int n) {
   std::vector<double> a(h, h + (size_t)n * n);
   auto A = [&](int i, int j) -> double& { return a[(size_t)j * n + i]; };

@@ -22,6 +22,11 @@ struct Error : std::runtime_error {
 // +0.0 imaginary part. Zero bytes are folded in as multiplications by powers of the prime.
 uint64_t fnv_csr_fingerprint(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
                              const double* values, int64_t nnz);
+// Resumable form of the same fold (a row-distributed matrix is hashed in three relays): the
+// dims, then row_ptr entries (each + add: a slab's local offsets rebased to global), col_idx, values.
+uint64_t fnv_begin(int64_t n_rows, int64_t n_cols, int64_t nnz);
+uint64_t fnv_fold_u64(uint64_t h, const int64_t* v, int64_t count, int64_t add);
+uint64_t fnv_fold_values(uint64_t h, const double* values, int64_t count);
 
 // Cyclic Jacobi eigenvalues (ascending) of a real symmetric s x s matrix (column-major);
 // the real specialisation of hermitian_eigenvalues (kernels.cpp:156-208).

@@ -98,6 +98,7 @@ enum KernelClass : int32_t {
   kKPrologue,
   kKValidate,
   kKOther,
+  kKPersistCycle,
   kKNumClasses
 };
 struct KernelClassStats {
@@ -189,6 +190,18 @@ void launch_poly(cudaStream_t st, int64_t n, int64_t ld, int s, int ell, const d
 // Start of a solve: Ma := P^H V, g := P^H r, pending gamma_0 := solve(Ma, g).
 void launch_prologue(cudaStream_t st, int64_t n, int64_t ld, int s, const double* p,
                      const double* v, const double* r, const Reducer& red);
+
+// ---- persistent cycle (kpersist.cu): one cooperative kernel runs a whole cycle out of registers ----
+// set p = (x_in, r_in, u_in, v_in) -> set 1-p; b != nullptr adds the true-residual refresh. xbuf: n
+// doubles of scratch; partials: persist_partials_doubles(n) doubles; bar: 4 bytes (grid barrier
+// counter, zeroed by the launcher). Returns false when (s, ell) is
+// not instantiated or the grid cannot be co-resident (probe_only: answer without launching).
+int64_t persist_partials_doubles(int64_t n);
+bool launch_persist_cycle(cudaStream_t st, const DevCsr& a, int64_t n, int64_t ld, int s, int ell,
+                          const double* x_in, const double* r_in, const double* u_in, const double* v_in,
+                          double* x_out, double* r_out, double* u_out, double* v_out, const double* p,
+                          const double* b, double* xbuf, double* partials, DevState* ds, unsigned* bar,
+                          bool probe_only);
 
 // ---- validate (recycle.cpp:40-83): ||V - A U||^2, ||V||^2 per column, P^H P, V^H V ----------
 // Results land in ds->scal[0..1] (dev_num, dev_den) and ds->gram (P^H P then V^H V).

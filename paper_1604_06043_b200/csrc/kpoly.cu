@@ -12,6 +12,7 @@
 // CTA (ticket counter) reduces the partials in a fixed order and runs the dense step that
 // consumes them (s x s LU, Givens-TSQR least squares) without another launch.
 #include "kcommon.cuh"
+#include "kdense.cuh"
 
 namespace mstab_b200 {
 
@@ -61,34 +62,6 @@ struct PolyArgs {
   double* x_out;
   const double* p;
 };
-
-// The dense tail of poly / prologue (run by every thread of one CTA): ||r||, g = P^H r,
-// Ma = P^H V and the next cycle's gamma_0 = (P^H V)^-1 P^H r, staged in parallel and solved by
-// one warp in shared memory.
-template <int S>
-__device__ void poly_tail(const double* redv, DevState* ds) {
-  __shared__ double lu[kMaxS * kMaxS];
-  __shared__ double vin[kMaxS], vout[kMaxS];
-  __shared__ int ok;
-  const int t = threadIdx.x;
-  if (t == 0) ds->st.resnorm = sqrt(redv[0]);
-  if (t < S) {
-    ds->g[t] = redv[1 + t];
-    vin[t] = redv[1 + t];
-  }
-  for (int i = t; i < S * S; i += blockDim.x) {
-    ds->Ma[i] = redv[1 + S + i];
-    lu[i] = redv[1 + S + i];
-  }
-  __syncthreads();
-  if (t < 32) {
-    const bool r2 = warp_lu_solve<S>(S, lu, vin, vout);
-    if (t == 0) ok = r2 ? 1 : 0;
-  }
-  __syncthreads();
-  if (t < S) ds->gamma[t] = vout[t];
-  if (t == 0) ds->st.pending_singular = ok ? 0 : 1;
-}
 
 // POLY = true: poly_combination (idrstab.cpp:154-191) + fused reductions.
 // POLY = false: prologue (reductions of the given V and r only).

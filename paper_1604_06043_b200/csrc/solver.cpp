@@ -7,6 +7,7 @@
 #include "solver.h"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <complex>
@@ -37,7 +38,11 @@ int64_t ns_since(Clock::time_point t0) {
   return std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count();
 }
 
-// MSTAB_DEBUG_STALL=ms: report any traced host-side step of a solve that took longer (stderr).
+// Phase tracing (the reference only has steady_clock stamps per history point). Every
+// traced host-side step of a solve is an NVTX range ("mstab: validate", "mstab: cycle", ...), so
+// an Nsight Systems / Compute timeline shows the solve's phases over the kernels they launch
+// (header-only NVTX 3: a no-op costing a relaxed load when no tool is attached), and with
+// MSTAB_DEBUG_STALL=ms any step that took longer than that is reported on stderr.
 struct StallTrace {
   const char* what;
   Clock::time_point t0;
@@ -48,8 +53,9 @@ struct StallTrace {
     }();
     return v;
   }
-  explicit StallTrace(const char* w) : what(w), t0(Clock::now()) {}
+  explicit StallTrace(const char* w) : what(w), t0(Clock::now()) { nvtxRangePushA(w); }
   ~StallTrace() {
+    nvtxRangePop();
     const double lim = limit_ms();
     if (lim < 0.0) return;
     const double ms = ns_since(t0) / 1e6;
@@ -736,6 +742,78 @@ std::shared_ptr<Operator> make_operator_slab(Context& ctx, int64_t n, const int6
   return op;
 }
 
+// The same slab from the rank's OWN rows (column indices global): no rank needs the global CSR.
+// What make_operator_slab derives from the global matrix arrives as arguments instead: the column
+// span [lo_r, hi_r) of every rank's rows (spans: 2 x world, allgathered by the caller) and the
+// reference fingerprint of the global matrix (fnv_begin / fnv_fold_*: a relay over the ranks).
+std::shared_ptr<Operator> make_operator_slab_local(Context& ctx, int64_t n_global, const int64_t* slabs,
+                                                   const int64_t* row_ptr, const int64_t* col_idx,
+                                                   const double* values, const int64_t* spans,
+                                                   uint64_t fingerprint) {
+  if (!ctx.comm) throw Error(MSTAB_E_CONFIG, "slab operator: the context has no communicator");
+  const int world = ctx.comm->world(), rank = ctx.comm->rank();
+  if (slabs[0] != 0 || slabs[world] != n_global)
+    throw Error(MSTAB_E_DIMENSION, "slab operator: boundaries must span 0..n");
+  for (int r = 0; r < world; ++r)
+    if (slabs[r] > slabs[r + 1]) throw Error(MSTAB_E_DIMENSION, "slab operator: boundaries not ascending");
+  const int64_t start = slabs[rank], end = slabs[rank + 1], nl = end - start;
+  if (nl < 1) throw Error(MSTAB_E_DIMENSION, "slab operator: empty slab");
+  // CsrMatrix::validate (csr.cpp:11-24) on the local rows, columns against the global size
+  if (row_ptr[0] != 0) throw Error(MSTAB_E_ERROR, "csr: row_ptr bounds");
+  int64_t lo_own = start, hi_own = end;
+  for (int64_t i = 0; i < nl; ++i) {
+    if (row_ptr[i] > row_ptr[i + 1]) throw Error(MSTAB_E_ERROR, "csr: row_ptr not nondecreasing");
+    for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+      if (col_idx[k] < 0 || col_idx[k] >= n_global) throw Error(MSTAB_E_ERROR, "csr: column index out of range");
+      if (k > row_ptr[i] && col_idx[k - 1] >= col_idx[k])
+        throw Error(MSTAB_E_ERROR, "csr: columns not strictly increasing within a row");
+      lo_own = std::min(lo_own, col_idx[k]);
+      hi_own = std::max(hi_own, col_idx[k] + 1);
+    }
+  }
+  std::vector<int64_t> lo(world), hi(world);
+  for (int r = 0; r < world; ++r) {
+    lo[r] = std::min(spans[2 * r], slabs[r]);
+    hi[r] = std::max(spans[2 * r + 1], slabs[r + 1]);
+  }
+  if (lo[rank] > lo_own || hi[rank] < hi_own)
+    throw Error(MSTAB_E_DIMENSION, "slab operator: this rank's column span does not cover its rows");
+  auto op = std::make_shared<Operator>();
+  op->uid = next_operator_uid();
+  op->fingerprint = fingerprint;
+  op->n_global = n_global;
+  op->row0 = start;
+  op->xlo = lo[rank] - start;
+  op->xhi = hi[rank] - start;
+  auto overlap = [](int64_t a0, int64_t a1, int64_t b0, int64_t b1, int64_t& o0, int64_t& o1) {
+    o0 = std::max(a0, b0);
+    o1 = std::min(a1, b1);
+    return o0 < o1;
+  };
+  for (int p = 0; p < world; ++p) {
+    if (p == rank) continue;
+    int64_t o0, o1;
+    if (overlap(lo[rank], start, slabs[p], slabs[p + 1], o0, o1)) op->halo.recvs.push_back({p, o0 - start, o1 - o0});
+    if (overlap(end, hi[rank], slabs[p], slabs[p + 1], o0, o1)) op->halo.recvs.push_back({p, o0 - start, o1 - o0});
+    if (overlap(lo[p], slabs[p], start, end, o0, o1)) op->halo.sends.push_back({p, o0 - start, o1 - o0});
+    if (overlap(slabs[p + 1], hi[p], start, end, o0, o1)) op->halo.sends.push_back({p, o0 - start, o1 - o0});
+  }
+  ctx.lay_n = nl;
+  ctx.lay_lo = (start - lo[rank] + 63) / 64 * 64;
+  ctx.lay_ld = padded_ld(ctx.lay_lo + nl + (hi[rank] - end));
+  ctx.lay_row0 = start;
+  ctx.lay_nglobal = n_global;
+  ctx.ws.reset();
+  ctx.pcache.reset();
+  ctx.val_au.reset();
+  ctx.val_au_n = -1;
+  std::vector<int64_t> ci((size_t)row_ptr[nl]);
+  for (size_t k = 0; k < ci.size(); ++k) ci[k] = col_idx[k] - start;
+  upload_rows(ctx, op.get(), nl, row_ptr, ci.data(), values);
+  if (!ctx.xgath) ctx.xgath = ctx.alloc(sizeof(double) * (size_t)world * kMaxXred);
+  return op;
+}
+
 // ---- split preconditioning (precond.cpp) --------------------------------------------------------
 namespace {
 
@@ -1053,6 +1131,18 @@ Workspace& workspace(Context& ctx, const Operator& op, int s, int ell, bool tres
   }
   w->b = ctx.alloc_vecs(n, 1);
   w->P = ctx.alloc_vecs(n, s);
+  // Small, L2-resident problems run each cycle as one cooperative kernel out of registers
+  // (kpersist.cu) when (s, ell) is instantiated and one row per thread fits the device. Tiny
+  // systems (the reference's dense-step tests, n < 4096) keep the stream-of-kernels path, whose
+  // Givens least squares their 1e-12 trajectory tolerances were calibrated against.
+  if (!ctx.sharded() && !op.pc && n >= 4096 && std::getenv("MSTAB_NO_PERSIST") == nullptr &&
+      (size_t)persist_partials_doubles(n) * sizeof(double) <= ctx.partials->bytes &&
+      launch_persist_cycle(ctx.stream(), op.csr(), n, ctx.ld(n), s, ell, nullptr, nullptr, nullptr, nullptr, nullptr,
+                           nullptr, nullptr, nullptr, nullptr, tres ? w->b->d() : nullptr, nullptr, nullptr, nullptr,
+                           nullptr, true)) {
+    w->xbuf = ctx.alloc_vecs(n + 64, 1);  // the last 4 bytes' worth past n: the grid barrier counter
+    w->persist = true;
+  }
   // Result blocks of the solves to come (x; U, V of the fetched and the final recycle data): a solve
   // hands out four fresh n x s blocks and the caller usually still holds the previous solve's. On
   // this pool a cudaMallocAsync that has to grow the driver's pool stalled for 40-300 ms at random
@@ -1089,6 +1179,15 @@ void enqueue_full_cycle(Context& ctx, const Operator& op, Workspace& w, int p) {
 // launches the kernels directly when graphs are off.
 void run_cycle(Context& ctx, const Operator& op, Workspace& w, int p) {
   cudaStream_t st = ctx.stream();
+  if (w.persist) {
+    const WSet& S = w.set[p];
+    const WSet& D = w.set[1 - p];
+    launch_persist_cycle(st, op.csr(), op.n, ctx.ld(op.n), w.s, w.ell, S.x->d(), S.r->d(), S.U->d(), S.V->d(),
+                         D.x->d(), D.r->d(), D.U->d(), D.V->d(), w.P->d(), w.tres ? w.b->d() : nullptr, w.xbuf->d(),
+                         ctx.partials->d(), ctx.ds(), reinterpret_cast<unsigned*>(w.xbuf->d() + ctx.ld(op.n)), false);
+    check_launch();
+    return;
+  }
   if (!ctx.use_graphs || (ctx.comm && !ctx.comm->capturable())) {
     enqueue_full_cycle(ctx, op, w, p);
     return;
@@ -1123,6 +1222,21 @@ void run_cycle(Context& ctx, const Operator& op, Workspace& w, int p) {
   count_launches(g.kernels);
 }
 
+// Runs one cycle and reads its status. A persistent-kernel cycle that asks for the other path
+// (kBreakFallback: its least squares left the CholeskyQR2 regime) is rerun on the stream of kernels
+// from the same, untouched source set, and the workspace stays on that path.
+const CycleStatus& run_cycle_sync(Context& ctx, const Operator& op, Workspace& w, int p) {
+  run_cycle(ctx, op, w, p);
+  const CycleStatus* cs = &read_status(ctx);
+  if (w.persist && cs->breakdown == kBreakFallback) {
+    w.persist = false;
+    reset_status(ctx);
+    run_cycle(ctx, op, w, p);
+    cs = &read_status(ctx);
+  }
+  return *cs;
+}
+
 DevPtr copy_vec(Context& ctx, const DevPtr& src, int64_t n) {
   DevPtr d = ctx.alloc_vecs(n, 1);
   CUDA_OK(cudaMemcpyAsync(d->d(), src->d(), sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx.stream()));
@@ -1152,7 +1266,7 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
 
   // b: ensure_finite + bnorm (idrstab.cpp:200, :205)
   std::optional<StallTrace> tr_in;
-  tr_in.emplace("copy-in + stats (first sync)");
+  tr_in.emplace("mstab: copy-in");
   CUDA_OK(cudaMemcpyAsync(w.b->d(), b_in, sizeof(double) * n,
                           mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   launch_vec_stats(st, n, w.b->d(), scal(ctx, 0), ctx.reducer());
@@ -1199,7 +1313,7 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   bool omegas_complete = true;
   if (recycle) {
     {
-      StallTrace tr("validate");
+      StallTrace tr("mstab: validate");
       validate(ctx, *recycle, op);
     }
     rep.h_mv_aux += recycle->s;
@@ -1218,13 +1332,17 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
     if (ctx.pcache && ctx.pcache_n == n && ctx.pcache_s == s && ctx.pcache_seed == cfg.seed) {
       P = ctx.pcache;
     } else {
+      StallTrace tr("mstab: make_cut_space");
       P = make_cut_space(ctx, n, s, cfg.seed);
       ctx.pcache = P;
       ctx.pcache_n = n;
       ctx.pcache_s = s;
       ctx.pcache_seed = cfg.seed;
     }
-    arnoldi_init(ctx, op, c0.r->d(), s, cfg.seed ^ 0x9e3779b97f4a7c15ull, c0.U->d(), c0.V->d());
+    {
+      StallTrace tr("mstab: arnoldi_init");
+      arnoldi_init(ctx, op, c0.r->d(), s, cfg.seed ^ 0x9e3779b97f4a7c15ull, c0.U->d(), c0.V->d());
+    }
     rep.h_mv += s;
   }
   if (w.p_src != P) {  // the graphs read P from the workspace copy
@@ -1244,13 +1362,9 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
 
   bool broke = false;
   while (resnorm > threshold && rep.h_mv < cfg.max_mv) {
-    {
-      StallTrace tr("cycle launch");
-      run_cycle(ctx, op, w, p);
-    }
     const CycleStatus& cs = [&]() -> const CycleStatus& {
-      StallTrace tr("cycle status read (sync)");
-      return read_status(ctx);
+      StallTrace tr("mstab: cycle");
+      return run_cycle_sync(ctx, op, w, p);
     }();
     if (w.graph[p].profiled) prof_accumulate(w.graph[p].prof);
     if (cs.breakdown) {  // BreakdownError: keep the last completed cycle (idrstab.cpp:290-293)
@@ -1279,7 +1393,7 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
                        (fetch->kind == MSTAB_FETCH_AT_HALF_TOLERANCE &&
                         resnorm <= std::sqrt(cfg.tol) * rep.bnorm);
       if (hit) {  // fetch(): deep copy (recycle.cpp:26-38)
-        StallTrace tr("fetch copy");
+        StallTrace tr("mstab: fetch");
         auto f = std::make_shared<Recycle>();
         f->n = n;
         f->s = s;
@@ -1296,7 +1410,7 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   if (!broke) rep.status = resnorm <= threshold ? MSTAB_STATUS_CONVERGED : MSTAB_STATUS_MAXMV;
   rep.final_resnorm = resnorm;
   const WSet& cur = w.set[p];
-  StallTrace tr_final("final copies + sync");
+  StallTrace tr_final("mstab: hand-off copies");
   res->x = copy_vec(ctx, cur.x, n);
   auto fin = std::make_shared<Recycle>();
   fin->n = n;
@@ -1557,8 +1671,7 @@ std::unique_ptr<SolveResultImpl> sridr(Context& ctx, const Operator& op, const d
     check_launch();
     read_status(ctx);
     while (resnorm > threshold && rep.h_mv < cfg.max_mv) {
-      run_cycle(ctx, op, w, p);
-      const CycleStatus& ccs = read_status(ctx);
+      const CycleStatus& ccs = run_cycle_sync(ctx, op, w, p);
       if (w.graph[p].profiled) prof_accumulate(w.graph[p].prof);
       if (ccs.breakdown) {
         rep.h_mv += ccs.mv_at_breakdown;

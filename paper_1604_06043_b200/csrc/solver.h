@@ -83,6 +83,10 @@ struct Workspace {
   // the copy is trusted (a freed-and-reallocated P at the same address must be copied again)
   DevPtr p_src;
   CycleGraph graph[2];          // graph[p]: set[p] -> set[1-p]
+  // persistent cycle kernel (kpersist.cu): chosen once per workspace, dropped for the rest of a
+  // solve after a fallback request
+  DevPtr xbuf;
+  bool persist = false;
 };
 
 struct Context {
@@ -227,6 +231,13 @@ std::shared_ptr<Operator> make_operator(Context& ctx, int64_t n, const int64_t* 
 std::shared_ptr<Operator> make_operator_slab(Context& ctx, int64_t n, const int64_t* row_ptr,
                                              const int64_t* col_idx, const double* values,
                                              const int64_t* slab_starts);
+
+// The same from the rank's own rows only (global column indices), the peers' column spans and the
+// global fingerprint supplied by the caller (large systems: no rank holds the global CSR).
+std::shared_ptr<Operator> make_operator_slab_local(Context& ctx, int64_t n_global, const int64_t* slab_starts,
+                                                   const int64_t* row_ptr, const int64_t* col_idx,
+                                                   const double* values, const int64_t* spans,
+                                                   uint64_t fingerprint);
 
 void spmv(Context& ctx, const Operator& op, const double* x_dev, double* y_dev);
 

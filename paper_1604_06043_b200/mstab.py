@@ -409,6 +409,27 @@ class CsrOperator:
                 i64ptr(self._slabs), C.byref(h)))
         self.h = h
 
+    @classmethod
+    def from_local_rows(cls, n_global: int, slabs, row_ptr, col_idx, values, col_spans, fingerprint: int,
+                        ctx: Context) -> "CsrOperator":
+        """Row slab of the context's rank from the rank's OWN rows (row_ptr from 0, GLOBAL column
+        indices): no rank holds the global matrix. `col_spans` (world x 2) are the column ranges every
+        rank's rows reference (`local_col_span` on each rank, allgathered); `fingerprint` is the
+        global reference checksum (`distributed_fingerprint`)."""
+        self = cls.__new__(cls)
+        self.ctx, self.lib, self.matrix = ctx, ctx.lib, None
+        self._slabs = np.ascontiguousarray(slabs, dtype=np.int64)
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int64)
+        va = np.ascontiguousarray(values, dtype=np.float64)
+        sp = np.ascontiguousarray(col_spans, dtype=np.int64).reshape(-1)
+        h = C.c_void_p()
+        _check(self.lib, self.lib.dll.mstab_operator_create_csr_slab_local(
+            ctx.h, n_global, i64ptr(self._slabs), i64ptr(rp), i64ptr(ci), dptr(va), i64ptr(sp),
+            C.c_uint64(fingerprint), C.byref(h)))
+        self.h = h
+        return self
+
     @property
     def row_begin(self) -> int:
         return int(self.lib.dll.mstab_operator_row_begin(self.h))
@@ -965,3 +986,63 @@ def poly_combination(st: IterationState, ell: int, ctx: Optional[Context] = None
     _check(ctx.lib, ctx.lib.dll.mstab_kernel_poly_combination(ctx.h, n, s, ell, dptr(x0), dptr(r), dptr(v), dptr(x),
                                                               dptr(rr), dptr(u), dptr(vv), dptr(tau), C.byref(pert)))
     return PolyOut(x, rr, u.T.copy(), vv.T.copy(), tau, bool(pert.value))
+
+
+def local_col_span(row0: int, row1: int, col_idx) -> tuple:
+    """[lo, hi) of the columns a slab's rows reference (at least its own rows)."""
+    ci = np.asarray(col_idx)
+    if ci.size == 0:
+        return int(row0), int(row1)
+    return int(min(row0, ci.min())), int(max(row1, ci.max() + 1))
+
+
+def distributed_fingerprint(lib: Lib, n_global: int, nnz_global: int, row_ptr, col_idx, values, first_entry: int,
+                            group=None) -> int:
+    """The reference's checksum of a row-distributed CSR matrix (csr.cpp:28-43) without gathering it.
+
+    The checksum folds dims, then all row_ptr entries, all col_idx entries and all values, so the
+    8-byte state makes three passes over the ranks of torch.distributed's `group` (send / recv to
+    the next rank; the last rank broadcasts the result). `row_ptr` is the slab's local row_ptr (from
+    0), `first_entry` the global index of its first stored entry (the nnz of the lower ranks).
+    Without an initialised process group (one rank) it is the plain fold."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int64)
+    va = np.ascontiguousarray(values, dtype=np.float64)
+    dll = lib.dll
+    rank, world, dist, torch, dev = 0, 1, None, None, None
+    try:
+        import torch
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+            dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+    except ImportError:
+        pass
+
+    def to_t(h):
+        return torch.from_numpy(np.array([h], dtype=np.uint64).view(np.int64).copy()).to(dev)
+
+    def from_t(t):
+        return int(t.cpu().numpy().view(np.uint64)[0])
+
+    h = int(dll.mstab_fnv_begin(n_global, n_global, nnz_global)) if rank == 0 else 0
+    for phase in range(3):
+        if world > 1 and not (phase == 0 and rank == 0):
+            t = to_t(0)
+            dist.recv(t, src=(rank - 1) % world, group=group)
+            h = from_t(t)
+        if phase == 0:  # rank 0 contributes the leading 0, every rank its n_local end offsets
+            off = 0 if rank == 0 else 1
+            part = np.ascontiguousarray(rp[off:])
+            h = int(dll.mstab_fnv_fold_index(C.c_uint64(h), i64ptr(part), part.size, first_entry))
+        elif phase == 1:
+            h = int(dll.mstab_fnv_fold_index(C.c_uint64(h), i64ptr(ci), ci.size, 0))
+        else:
+            h = int(dll.mstab_fnv_fold_values(C.c_uint64(h), dptr(va), va.size))
+        if world > 1 and not (phase == 2 and rank == world - 1):
+            dist.send(to_t(h), dst=(rank + 1) % world, group=group)
+    if world > 1:
+        t = to_t(h)
+        dist.broadcast(t, src=world - 1, group=group)
+        h = from_t(t)
+    return h

@@ -35,6 +35,22 @@ def convdiff(dim: int, n: int, stencil: int, beta, dt: float) -> CsrMatrix:
     return CsrMatrix(N, N, rp, ci, va)
 
 
+def convdiff_rows(dim: int, n: int, stencil: int, beta, dt: float, row0: int, row1: int):
+    """Rows [row0, row1) of the conv-diff matrix: (local row_ptr, GLOBAL col_idx, values). A rank of
+    a row-sharded run generates its own slab; the global matrix is never materialised."""
+    g = gen_lib()
+    b = np.zeros(3)
+    b[:len(beta)] = beta
+    nnz = int(g.mstab_gen_convdiff_rows(dim, n, stencil, dptr(b), dt, row0, row1, None, None, None))
+    if nnz < 0:
+        raise ValueError("unsupported stencil")
+    rp = np.empty(row1 - row0 + 1, dtype=np.int64)
+    ci = np.empty(nnz, dtype=np.int64)
+    va = np.empty(nnz, dtype=np.float64)
+    g.mstab_gen_convdiff_rows(dim, n, stencil, dptr(b), dt, row0, row1, i64ptr(rp), i64ptr(ci), dptr(va))
+    return rp, ci, va
+
+
 def banded(n: int, nnz_per_row: int, half_width: int, seed: int) -> CsrMatrix:
     g = gen_lib()
     nnz = 0

@@ -1,4 +1,8 @@
-"""Row-slab partition of the Mstab path across the GPUs of one node.
+"""TEST MODEL (not product code): a NumPy statement of the row-slab partition of the Mstab path
+ that the CPU tests check the slab logic against; the product's planner is the
+C++ one (csrc/solver.cpp make_operator_slab / make_operator_slab_local).
+
+Row-slab partition of the Mstab path across the GPUs of one node.
 
 Every operation of the solve loop except the SpMV is row-local (idrstab.cpp:105-191: the BiCG
 updates, column rebuilds and the poly combination touch one row at a time); the SpMV needs the

@@ -37,6 +37,10 @@ def _matrix(name):
         A.values = A.values.copy()
         A.values[5] *= 1.0 + 2.0 ** -30
         return cfg, A
+    if name == "c4_24":  # 27-point stencil (BASELINE c4's shape): one halo plane per side
+        cfg = pb.config("c4", grid=24)
+        cfg.s, cfg.ell = 2, 2  # M(8,4) converges in 3 cycles at 24^3 and hands off a degenerate space
+        return cfg, cfg.matrix()
     if name == "c3_20000":  # banded random: CSR form, halo of up to 512 rows
         cfg = pb.config("c3", grid=20000)
         cfg.half_width = 512
@@ -45,10 +49,10 @@ def _matrix(name):
 
 
 def _slabs(n, world):
-    return np.array([(n * r) // world for r in range(world + 1)], dtype=np.int64)
+    return np.array([(n * r) // world for r in range(world + 1)], dtype=np.int64)  # not plane-aligned on purpose
 
 
-def _worker(rank, world, port, name, b, b2, q):
+def _worker(rank, world, port, name, b, b2, q, local=False):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -60,7 +64,22 @@ def _worker(rank, world, port, name, b, b2, q):
         lo, hi = int(slabs[rank]), int(slabs[rank + 1])
         ctx = m.Context(m.Lib(), 0)
         ctx.set_comm_host(rank, world, m.TorchHostComm())
-        op = m.CsrOperator(A, ctx, slabs=slabs)
+        if local:
+            # the rank's OWN rows only: spans allgathered, the global fingerprint folded over the ranks
+            import torch
+            rp = np.asarray(A.row_ptr, dtype=np.int64)
+            loc_rp = rp[lo:hi + 1] - rp[lo]
+            ci = np.asarray(A.col_idx, dtype=np.int64)[rp[lo]:rp[hi]]
+            va = np.asarray(A.values)[rp[lo]:rp[hi]]
+            span = torch.tensor(m.local_col_span(lo, hi, ci), dtype=torch.int64)
+            spans = [torch.zeros_like(span) for _ in range(world)]
+            dist.all_gather(spans, span)
+            spans = np.array([t.numpy() for t in spans], dtype=np.int64)
+            fp = m.distributed_fingerprint(ctx.lib, n, int(rp[-1]), loc_rp, ci, va, int(rp[lo]))
+            op = m.CsrOperator.from_local_rows(n, slabs, loc_rp, ci, va, spans, fp, ctx)
+            assert op.fingerprint() == m.CsrOperator(A, m.Context(m.Lib(), 0)).fingerprint()
+        else:
+            op = m.CsrOperator(A, ctx, slabs=slabs)
         assert op.row_begin == lo and op.size() == hi - lo and op.global_size == n
         rng = np.random.default_rng(7)
         xg = rng.standard_normal(n)
@@ -76,8 +95,10 @@ def _worker(rank, world, port, name, b, b2, q):
         q.put((rank, None, None, None, None, None, None, None, None, traceback.format_exc() + repr(e)))
 
 
-@pytest.mark.parametrize("name,world", [("c1_64", 2), ("c2_48", 3), ("c2_48_dia", 2), ("c3_20000", 2)])
-def test_sharded_matches_single_gpu(gpu_ctx, name, world):
+@pytest.mark.parametrize("name,world,local", [("c1_64", 2, False), ("c2_48", 3, False), ("c2_48_dia", 2, False),
+                                              ("c3_20000", 2, False), ("c4_24", 2, True), ("c4_24", 3, True),
+                                              ("c3_20000", 3, True)])
+def test_sharded_matches_single_gpu(gpu_ctx, name, world, local):
     cfg, A = _matrix(name)
     n = A.n_rows
     # single-GPU runs first: they also define the teacher-forced second right-hand side
@@ -94,7 +115,7 @@ def test_sharded_matches_single_gpu(gpu_ctx, name, world):
     ctxm = mp.get_context("spawn")
     q = ctxm.Queue()
     port = _free_port()
-    procs = [ctxm.Process(target=_worker, args=(r, world, port, name, b, b2, q)) for r in range(world)]
+    procs = [ctxm.Process(target=_worker, args=(r, world, port, name, b, b2, q, local)) for r in range(world)]
     for p in procs:
         p.start()
     out = {}

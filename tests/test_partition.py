@@ -5,7 +5,7 @@ import socket
 import numpy as np
 import pytest
 
-from paper_1604_06043_b200 import partition as pt
+import partition_model as pt
 from paper_1604_06043_b200 import problems as pb
 
 
@@ -98,3 +98,51 @@ def test_gloo_world2_halo_spmv_and_allreduce():
     assert np.array_equal(y, ref)                    # halo SpMV is bit-exact
     assert len(totals) == 1                          # every rank holds the same reduced bits
     assert abs(totals.pop() - float(np.dot(ref, x))) <= 1e-12 * abs(float(np.dot(ref, x)))
+
+
+def _fp_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import paper_1604_06043_b200 as m
+    from conftest import REF_LIB
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # every rank keeps ONLY its rows (a slab of whole grid planes) and folds the reference
+        # checksum of the global matrix in three relays over the ranks
+        A = pb.config("c4", grid=10).matrix()
+        slabs = pt.plan_rows(A.row_ptr, world, align=100)
+        a, b = slabs[rank]
+        rp = np.asarray(A.row_ptr, dtype=np.int64)
+        loc_rp = rp[a:b + 1] - rp[a]
+        ci = np.asarray(A.col_idx, dtype=np.int64)[rp[a]:rp[b]]
+        va = np.asarray(A.values)[rp[a]:rp[b]]
+        lib = m.Lib(str(REF_LIB))  # the fold is host code in both libraries; this one needs no GPU
+        h = m.distributed_fingerprint(lib, A.n_rows, int(rp[-1]), loc_rp, ci, va, int(rp[a]))
+        q.put((rank, h, m.local_col_span(a, b, ci)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_distributed_fingerprint_matches_the_global_checksum():
+    """Rank-local rows only: the relayed FNV fold equals the reference's checksum of the whole
+    matrix on every rank (csr.cpp:28-43), and the column spans describe one halo plane per side."""
+    import multiprocessing as mp
+
+    import oracle_c as oc
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_fp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A = pb.config("c4", grid=10).matrix()
+    want = oc.Csr(A).fingerprint()
+    assert [h for _, h, _ in res] == [want, want]
+    (lo0, hi0), (lo1, hi1) = res[0][2], res[1][2]
+    assert (lo0, hi0) == (0, 600) and (lo1, hi1) == (400, 1000)  # 27-point: exactly one halo plane per side
