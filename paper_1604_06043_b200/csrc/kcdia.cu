@@ -29,9 +29,9 @@ struct MaskOf {
                                       typename std::conditional<(ND <= 16), uint16_t, uint32_t>::type>::type;
 };
 
-// 512-thread CTAs, two per SM: the same 32 warps per SM as 4 x 256, but half the per-CTA partials,
-// so the last CTA sums each reduced value with one batch of loads per lane (the tail of every
-// SpMV sits on the critical path of the column loop).
+// 512-thread CTAs, two per SM: the same 32 warps per SM as 4 x 256, but half the per-CTA partials.
+// CTA 0 is the finisher (kcommon.cuh, finisher protocol): it streams no rows; CTAs 1..G-1 split the
+// rows grid-stride and publish their partial sums through the sentinel slots.
 constexpr int kCdiaBlock = 512;
 
 template <int S, bool TRUE_RES, int ND>
@@ -41,6 +41,37 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
                 FinParams fin, Reducer red) {
   DevState* ds = red.ds;
   constexpr int NS = S + (TRUE_RES ? 1 : 0);
+  __shared__ double scratch[NS * 32];  // block_totals: up to 32 warps
+  __shared__ double blk[NS];
+  if (blockIdx.x == 0) {
+    // ---- finisher CTA ----
+    __shared__ PreLU pl;
+    __shared__ double xs[S];
+    __shared__ int oks;
+    if (threadIdx.x == 0) {
+      TL_MIN(0);
+      TL_MAX(1);
+    }
+    pdl_wait();
+    pdl_trigger();
+    if (!red.xred) finisher_prepare<S>(fin, ds, pl);
+    slots_collect(NS, red.slots, blk);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      TL_SET(7);
+      TL_CLK(11);
+    }
+    if (red.xred) {  // row-sharded: the rank-local totals go to the cross-rank reduction
+      if (threadIdx.x < NS) red.xred[threadIdx.x] = blk[threadIdx.x];
+      return;
+    }
+    finisher_finish<S>(fin, blk, ds, pl, xs, &oks);
+    if (threadIdx.x == 0) {
+      TL_SET(9);
+      TL_CLK(13);
+    }
+    return;
+  }
   const int64_t n = a.n;
   const int nd = ND > 0 ? ND : a.ndiag;
   const int mb = a.mask_bytes;
@@ -56,8 +87,8 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
                    : (mb == 2 ? (uint32_t)__ldg(static_cast<const uint16_t*>(a.dia_mask) + r)
                               : __ldg(static_cast<const uint32_t*>(a.dia_mask) + r));
   };
-  const int32_t rstride = gridDim.x * blockDim.x;
-  const int32_t row0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t rstride = (gridDim.x - 1) * blockDim.x;
+  const int32_t row0 = (blockIdx.x - 1) * blockDim.x + threadIdx.x;
   // The masks never change and, inside a cycle, neither do P and b: the first row's mask, P row
   // and b are loaded before waiting on the producer of x (programmatic dependent launch), so that
   // DRAM round trip overlaps the predecessor's tail. A plain product (kFinStore) may pass a
@@ -117,26 +148,11 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
     if (TRUE_RES) part[S] = part[S] + acc * acc;
   }
   pdl_trigger();
-  __shared__ double scratch[NS * 32];  // block_totals: up to 32 warps
-  __shared__ double blk[NS];
-  __shared__ double redv[NS];
-  __shared__ FinStage fs;
-  if (!red.xred) fin_prestage(fin, ds, fs);
   block_totals<NS>(part, blk, scratch);
+  slots_publish(blk, NS, red.slots);
   if (threadIdx.x == 0) {
     TL_MIN(4);
     TL_MAX(5);
-  }
-  if (!cta_commit(blk, NS, red.partials, &ds->ticket, redv, red.xred)) return;
-  if (threadIdx.x == 0) {
-    TL_SET(7);
-    TL_CLK(11);
-  }
-  finalize_spmv<S>(fin, redv, ds, fs);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    TL_SET(9);
-    TL_CLK(13);
   }
 }
 
@@ -148,7 +164,10 @@ template <int S, bool TRUE_RES, int ND>
 void launch_cdia_nd(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
                     int64_t ld, const double* b, const FinParams& fin, const Reducer& red) {
   auto kfn = k_spmv_cdia<S, TRUE_RES, ND>;
-  launch_pdl(kfn, occupancy_grid(kfn, a.n, 0, kCdiaBlock), kCdiaBlock, 0, st, a, x, y, p, ld, b, fin, red);
+  // the resident capacity minus the finisher streams; one more CTA (index 0) finishes
+  int grid = occupancy_grid(kfn, a.n + kCdiaBlock, 0, kCdiaBlock);
+  if (grid < 2) grid = 2;
+  launch_pdl(kfn, grid, kCdiaBlock, 0, st, a, x, y, p, ld, b, fin, red);
 }
 
 // Specialised stencil widths: 5 (2-D 5-point: c1), 7 (3-D 7-point: c2, c5), 27 (27-point: c4).

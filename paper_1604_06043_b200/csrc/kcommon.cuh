@@ -589,6 +589,347 @@ __device__ void finalize_spmv(const FinParams& f, const double* red, DevState* d
   }
 }
 
+// ---- finisher protocol (kcdia.cu) ---------------------------------------------------------------
+// The dense step after an SpMV reduction sits on the critical path of the column loop (37 SpMVs per
+// cycle at c2). With the last-CTA scheme above that tail was ~8 us of a 34 us launch (r02 timeline:
+// store fence + ticket 2.2 us, partial sums 1.3 us, s x s LU 4.3 us). Here CTA 0 of the grid streams
+// no rows. While the others stream it factors everything of the small system that is already known
+// (fin_prefactor), then polls the partial slots (an empty slot holds an all-ones NaN, so a partial is
+// published by ONE relaxed store: no fence, no ticket), sums them in index order, and only forward-
+// eliminates the ONE new column (or right-hand side) and back-substitutes (fin_finish).
+//
+// Which part is known early: after the SpMV of column q the system is msys_{q+1} = [P^H V^(k+1)_{0..q},
+// P^H V^(k)_{q+1..s-1}] (idrstab.cpp:133-137) and only column q is new; the right-hand side P^H r^(k+1)
+// is known since step (b). The finisher factors the s-1 known columns with partial pivoting, taking
+// the new column LAST: for q = s-1 this is exactly the reference's LuFactor (kernels.cpp:95-127), for
+// q < s-1 it is the same Gaussian elimination on a column-permuted system (the solution's entries are
+// permuted back), equally stable but rounded differently at the 1e-16 level, like the tree reductions.
+// After step (b) and after the true-residual product the matrix is fully known and only the right-
+// hand side is new: the factorisation and both substitutions are the reference's, bit for bit.
+constexpr unsigned long long kSlotEmpty = 0xffffffffffffffffull;
+
+__device__ __forceinline__ double slot_load(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void slot_store(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+// a streaming CTA's totals -> its slots (never the empty pattern: a NaN total is canonicalised)
+__device__ __forceinline__ void slots_publish(const double* blk, int nslots, double* slots) {
+  if ((int)threadIdx.x < nslots) {
+    double v = blk[threadIdx.x];
+    if (v != v) v = __longlong_as_double(0x7ff8000000000000ll);
+    slot_store(slots + (size_t)threadIdx.x * gridDim.x + blockIdx.x, v);
+  }
+}
+// finisher CTA: waits for the slots of CTAs 1..G-1, sums each value over the CTAs in a fixed order
+// (per lane ascending, then the warp butterfly: the order cta_commit uses) and empties the slots.
+__device__ void slots_collect(int nslots, double* slots, double* red) {
+  const int G = gridDim.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = w; i < nslots; i += nw) {
+    double* p = slots + (size_t)i * G;
+    double acc = 0.0;
+    for (int c0 = 1 + lane; c0 < G; c0 += 32 * 16) {
+      double v[16];
+      bool all;
+      do {
+        all = true;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = (c0 + 32 * u < G) ? slot_load(p + c0 + 32 * u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) all = all && ((unsigned long long)__double_as_longlong(v[u]) != kSlotEmpty);
+      } while (!all);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc += v[u];
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (c0 + 32 * u < G) slot_store(p + c0 + 32 * u, __longlong_as_double((long long)kSlotEmpty));
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) red[i] = acc;
+  }
+}
+
+struct PreLU {
+  double lu[kMaxS * kMaxS];  // in: the columns to factor (column-major, ld = s); out: L \ U by position
+  double y[kMaxS];           // column mode: in the right-hand side, out L^-1 (perm rhs)
+  double rinv[kMaxS];        // reciprocals of the pivots
+  double mx, minpiv;         // max |entry| of the factored columns; smallest pivot magnitude
+  int perm[kMaxS];           // perm[position] = original row
+  int nc;                    // factored columns: s (right-hand-side mode) or s - 1 (column mode)
+  int solve;                 // 0: this step has no solve
+};
+
+// One warp: partially pivoted LU of the first nc columns of the s x s system in f.lu (lane i holds
+// row i, replicated in every PW-wide segment; the structure of warp_lu_fixed: pivot = largest
+// magnitude, ties to the lowest position = the reference's first strictly larger scan; multipliers
+// a_ik * (1 / a_kk); elimination skipped for a zero multiplier). With with_rhs the right-hand side
+// in f.y is eliminated along. Rows never move: each lane tracks its row's position and the factors
+// are scattered by position at the end (multipliers travel with their row, like the reference's
+// full-row swaps).
+template <int S>
+__device__ void fin_prefactor(PreLU& f, int nc, bool with_rhs) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int PW = S <= 1 ? 1 : (S <= 2 ? 2 : (S <= 4 ? 4 : (S <= 8 ? 8 : 16)));
+  const int lane = threadIdx.x & 31;
+  const int row = lane & (PW - 1);
+  const bool mine = row < S;
+  double r[S];
+#pragma unroll
+  for (int j = 0; j < S; ++j) r[j] = (mine && j < nc) ? f.lu[row + j * S] : 0.0;
+  double bi = (mine && with_rhs) ? f.y[row] : 0.0;
+  double mx = 0.0;
+#pragma unroll
+  for (int j = 0; j < S; ++j) mx = dmax_ref(mx, fabs(r[j]));
+#pragma unroll
+  for (int o = PW / 2; o > 0; o >>= 1) mx = dmax_ref(mx, __shfl_xor_sync(FULL, mx, o));
+  double minpiv = __longlong_as_double(0x7ff0000000000000ll);
+  double myrinv = 0.0;
+  int pos = row;
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    if (k >= nc) break;
+    const bool cand = mine && pos >= k;
+    double mag = cand ? fabs(r[k]) : -1.0;
+    int key = ((cand ? pos : 255) << 8) | row;
+    const double myinv = 1.0 / r[k];
+#pragma unroll
+    for (int o = PW / 2; o > 0; o >>= 1) {
+      const double om = __shfl_xor_sync(FULL, mag, o);
+      const int ok = __shfl_xor_sync(FULL, key, o);
+      const bool take = (om > mag) || (om == mag && ok < key);
+      mag = take ? om : mag;
+      key = take ? ok : key;
+    }
+    const int piv = key >> 8, wl = key & 255;
+    minpiv = (mag < minpiv) ? mag : minpiv;
+    const double inv = __shfl_sync(FULL, myinv, wl, PW);
+    const double bp = __shfl_sync(FULL, bi, wl, PW);
+    pos = (row == wl) ? k : (pos == k ? piv : pos);
+    if (row == wl) myrinv = inv;
+    const bool below = mine && pos > k;
+    const double m = r[k] * inv;
+#pragma unroll
+    for (int j = k + 1; j < S; ++j) {
+      const double pj = __shfl_sync(FULL, r[j], wl, PW);
+      if (below && m != 0.0 && j < nc) r[j] = r[j] - m * pj;
+    }
+    if (below) {
+      bi = bi - m * bp;
+      r[k] = m;
+    }
+  }
+  __syncwarp();
+  if (lane < PW && mine) {
+#pragma unroll
+    for (int j = 0; j < S; ++j) f.lu[pos + j * S] = r[j];
+    f.y[pos] = bi;
+    f.perm[pos] = row;
+    f.rinv[pos] = myrinv;
+  }
+  if (lane == 0) {
+    f.mx = mx;
+    f.minpiv = minpiv;
+    f.nc = nc;
+  }
+  __syncwarp();
+}
+
+// quotient t / u on the dependent chain as RN(q + (t - u q) rc), q = RN(t rc), rc = RN(1 / u) (3
+// dependent operations instead of a 112-cycle division); the IEEE quotient is formed beside it, off
+// the chain, and `same` records whether every quotient agreed (it does in practice; else the caller
+// reruns with plain divisions), so the result is always the division's.
+__device__ __forceinline__ double quot_chain(double t, double u, double rc, bool& same) {
+  const double q = t * rc;
+  const double rem = __fma_rn(-u, q, t);
+  const double xi = __fma_rn(rem, rc, q);
+  same = same && (__double_as_longlong(xi) == __double_as_longlong(t / u));
+  return xi;
+}
+
+// One thread: finishes the solve with the new vector v (original row order). Column mode
+// (f.nc == S - 1): v is the last column; x comes back in the factored column order (new column
+// last). Right-hand-side mode (f.nc == S): v is the right-hand side; forward substitution with
+// ascending j, backward substitution with ascending j and a final division (LuFactor::solve,
+// kernels.cpp:129-141). Returns false when the reference's pivot test fails.
+template <int S>
+__device__ bool fin_finish(const PreLU& f, const double* v, double* x) {
+  double w[S], xv[S];
+  double vmax = 0.0;
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    w[i] = v[f.perm[i]];
+    vmax = dmax_ref(vmax, fabs(v[i]));
+  }
+  const bool colmode = f.nc == S - 1;
+  if (colmode) {
+    // the new column through the S - 1 elimination steps, then it holds u_{.,S-1}
+#pragma unroll
+    for (int k = 0; k < S - 1; ++k) {
+#pragma unroll
+      for (int i = k + 1; i < S; ++i) {
+        const double m = f.lu[i + k * S];
+        if (m != 0.0) w[i] = w[i] - m * w[k];
+      }
+    }
+    const double scale = dmax_ref(f.mx, vmax);
+    const double upiv = w[S - 1];
+    const double lastmag = fabs(upiv);
+    const double minpiv = (lastmag < f.minpiv) ? lastmag : f.minpiv;
+    if (minpiv < 1e-14 * scale || scale == 0.0) return false;
+    const double rlast = 1.0 / upiv;
+    bool same = true;
+    double t[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) t[i] = f.y[i];
+    xv[S - 1] = quot_chain(t[S - 1], upiv, rlast, same);
+#pragma unroll
+    for (int i = 0; i < S - 1; ++i) t[i] = t[i] - w[i] * xv[S - 1];
+#pragma unroll
+    for (int j = S - 2; j >= 0; --j) {
+      xv[j] = quot_chain(t[j], f.lu[j + j * S], f.rinv[j], same);
+#pragma unroll
+      for (int i = 0; i < j; ++i) t[i] = t[i] - f.lu[i + j * S] * xv[j];
+    }
+    if (!same) {  // the same substitution with plain divisions
+#pragma unroll
+      for (int i = 0; i < S; ++i) t[i] = f.y[i];
+      xv[S - 1] = t[S - 1] / upiv;
+#pragma unroll
+      for (int i = 0; i < S - 1; ++i) t[i] = t[i] - w[i] * xv[S - 1];
+#pragma unroll
+      for (int j = S - 2; j >= 0; --j) {
+        xv[j] = t[j] / f.lu[j + j * S];
+#pragma unroll
+        for (int i = 0; i < j; ++i) t[i] = t[i] - f.lu[i + j * S] * xv[j];
+      }
+    }
+  } else {
+    if (f.minpiv < 1e-14 * f.mx || f.mx == 0.0) return false;
+#pragma unroll
+    for (int i = 1; i < S; ++i) {
+#pragma unroll
+      for (int j = 0; j < i; ++j) w[i] = w[i] - f.lu[i + j * S] * w[j];
+    }
+    bool same = true;
+#pragma unroll
+    for (int i = S - 1; i >= 0; --i) {
+      double t = w[i];
+#pragma unroll
+      for (int j = i + 1; j < S; ++j) t = t - f.lu[i + j * S] * xv[j];
+      xv[i] = quot_chain(t, f.lu[i + i * S], f.rinv[i], same);
+    }
+    if (!same) {
+#pragma unroll
+      for (int i = S - 1; i >= 0; --i) {
+        double t = w[i];
+#pragma unroll
+        for (int j = i + 1; j < S; ++j) t = t - f.lu[i + j * S] * xv[j];
+        xv[i] = t / f.lu[i + i * S];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < S; ++i) x[i] = xv[i];
+  return true;
+}
+
+// Finisher CTA, before the partials arrive: stages what the step's small system already has and
+// factors it (warp 0). Everything read here was written by kernels that completed before this
+// launch's pdl_wait returned.
+template <int S>
+__device__ void finisher_prepare(const FinParams& f, DevState* ds, PreLU& pl) {
+  const int t = threadIdx.x, nt = blockDim.x;
+  int nc = 0;
+  bool with_rhs = false, solve = false;
+  if (f.op == kFinRhsEta0 || f.op == kFinTrueRes) {
+    for (int i = t; i < S * S; i += nt) pl.lu[i] = ds->Ma[i];
+    nc = S;
+    solve = true;
+  } else if (f.op == kFinColEta) {
+    const int q = f.q;
+    // factored column j < S - 1 is column j (j < q: P^H V^(k+1)_j) or j + 1 (P^H V^(k)_{j+1})
+    for (int i = t; i < S * (S - 1); i += nt) {
+      const int j = i / S, rw = i - j * S;
+      pl.lu[i] = j < q ? ds->Mn[rw + j * S] : ds->Ma[rw + (j + 1) * S];
+    }
+    if (t < S) pl.y[t] = ds->rhs[t];
+    nc = S - 1;
+    with_rhs = true;
+    solve = (q + 1 < S) || (f.k + 1 < f.ell);
+  }
+  __syncthreads();
+  if (f.op == kFinColEta && f.q + 1 == S) {
+    // level done: Ma := P^H V^(k+1) (its last column arrives with the reduction), g := P^H r^(k+1)
+    for (int i = t; i < S * (S - 1); i += nt) ds->Ma[i] = ds->Mn[i];
+    if (t < S) ds->g[t] = ds->rhs[t];
+  }
+  if (t == 0) pl.solve = solve ? 1 : 0;
+  if (t < 32 && solve) fin_prefactor<S>(pl, nc, with_rhs);
+}
+
+// Finisher CTA, after slots_collect: the bookkeeping of finalize_spmv plus the short solve.
+template <int S>
+__device__ void finisher_finish(const FinParams& f, const double* red, DevState* ds, PreLU& pl, double* xs /*smem S*/,
+                                int* oks) {
+  const int t = threadIdx.x;
+  if (f.op == kFinStore) {
+    if (t < S) f.dst[t] = red[t];
+    return;
+  }
+  double* dst = nullptr;
+  int mv = 0;
+  bool pending = false;
+  const int q = f.q, k = f.k;
+  if (f.op == kFinRhsEta0) {
+    if (t < S) ds->rhs[t] = red[t];
+    dst = ds->eta;
+    mv = k * (S + 1) + 1;
+  } else if (f.op == kFinColEta) {
+    if (t < S) {
+      ds->Mn[t + q * S] = red[t];
+      if (q + 1 == S) ds->Ma[t + q * S] = red[t];
+    }
+    if (q + 1 < S) {
+      dst = ds->eta + (q + 1) * S;
+      mv = k * (S + 1) + 1 + (q + 1);
+    } else {
+      dst = ds->gamma + (k + 1) * kMaxS;
+      mv = (k + 1) * (S + 1);
+    }
+  } else if (f.op == kFinTrueRes) {
+    if (t == 0) ds->st.resnorm = sqrt(red[S]);
+    if (t < S) ds->g[t] = red[t];
+    dst = ds->gamma;
+    pending = true;
+  } else {
+    return;
+  }
+  if (!pl.solve) return;
+  if (t == 0) {
+    *oks = fin_finish<S>(pl, red, xs) ? 1 : 0;
+    TL_SET(8);
+    TL_CLK(12);
+  }
+  __syncthreads();
+  if (t < S) {
+    // column mode: entry j of the solve belongs to column j (j < q), j + 1 (q <= j < S - 1) or q (last)
+    int c = t;
+    if (f.op == kFinColEta) c = t < q ? t : (t == S - 1 ? q : t + 1);
+    dst[c] = xs[t];
+  }
+  if (t == 0) {
+    if (pending)
+      ds->st.pending_singular = *oks ? 0 : 1;
+    else if (!*oks)
+      set_breakdown(ds, kBreakSingular, mv);
+  }
+}
+
 // Resident CTAs per SM of each kernel, queried once (the occupancy API costs tens of us per
 // call, which would starve the GPU between launches).
 

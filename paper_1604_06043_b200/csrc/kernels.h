@@ -60,6 +60,10 @@ struct Reducer {
   // Non-null in row-sharded solves: the last CTA writes its rank-local totals here (ds->xred)
   // and skips the fused dense step (cta_commit), which then runs after the cross-rank reduction.
   double* xred = nullptr;
+  // Finisher protocol of the constant-diagonal SpMV (kcdia.cu): (kMaxS + 1) x kMaxGrid partial
+  // slots that hold an all-ones NaN pattern while empty. A streaming CTA publishes a partial with
+  // one relaxed store; the finisher CTA polls the slots, sums them in index order and re-arms them.
+  double* slots = nullptr;
 };
 
 // What the last CTA does with the reduced vector of an SpMV (see kernels.cu, finalize_spmv).

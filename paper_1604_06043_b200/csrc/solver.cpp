@@ -166,6 +166,8 @@ Context::Context(int dev) {
   ds_mem = alloc(sizeof(DevState));
   CUDA_OK(cudaMemsetAsync(ds_mem->ptr, 0, sizeof(DevState), stream()));
   partials = alloc(sizeof(double) * (size_t)kMaxGrid * 640);
+  slots = alloc(sizeof(double) * (size_t)kMaxGrid * (kMaxS + 1));
+  CUDA_OK(cudaMemsetAsync(slots->ptr, 0xff, slots->bytes, stream()));  // every slot empty
   CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host_status), sizeof(CycleStatus)));
   CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host_scal), sizeof(double) * 64));
   sync();

@@ -94,6 +94,7 @@ struct Context {
   int device = 0;
   DevPtr ds_mem;        // DevState
   DevPtr partials;      // reduction partials
+  DevPtr slots;         // sentinel-armed partial slots of the finisher protocol (Reducer::slots)
   CycleStatus* host_status = nullptr;  // pinned
   double* host_scal = nullptr;         // pinned, 64 doubles
   std::unique_ptr<Workspace> ws;       // cycle buffers + captured cycle graphs
@@ -114,7 +115,7 @@ struct Context {
   int64_t ld(int64_t n) const { return n == lay_n ? lay_ld : padded_ld(n); }
   cudaStream_t stream() const { return sh->stream; }
   DevState* ds() const { return static_cast<DevState*>(ds_mem->ptr); }
-  Reducer reducer() const { return Reducer{partials->d(), ds(), sharded() ? ds()->xred : nullptr}; }
+  Reducer reducer() const { return Reducer{partials->d(), ds(), sharded() ? ds()->xred : nullptr, slots->d()}; }
   DevPtr alloc(size_t bytes) { return std::make_shared<DevMem>(sh, bytes); }
   DevPtr alloc_vecs(int64_t n, int64_t cols);
   void sync();
