@@ -46,8 +46,6 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
   if (blockIdx.x == 0) {
     // ---- finisher CTA ----
     __shared__ PreLU pl;
-    __shared__ double xs[S];
-    __shared__ int oks;
     if (threadIdx.x == 0) {
       TL_MIN(0);
       TL_MAX(1);
@@ -65,7 +63,7 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
       if (threadIdx.x < NS) red.xred[threadIdx.x] = blk[threadIdx.x];
       return;
     }
-    finisher_finish<S>(fin, blk, ds, pl, xs, &oks);
+    finisher_finish<S>(fin, blk, ds, pl);
     if (threadIdx.x == 0) {
       TL_SET(9);
       TL_CLK(13);

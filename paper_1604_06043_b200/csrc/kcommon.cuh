@@ -632,8 +632,13 @@ __device__ void slots_collect(int nslots, double* slots, double* red) {
   for (int i = w; i < nslots; i += nw) {
     double* p = slots + (size_t)i * G;
     double acc = 0.0;
-    for (int c0 = 1 + lane; c0 < G; c0 += 32 * 16) {
+    // The sums are formed inside the poll loop, on every pass: when the last partial lands, the
+    // instructions that consume it are already in the instruction cache (see fin_finish).
+    double tot = 0.0;
+    for (int cb = 1; cb < G; cb += 32 * 16) {  // warp-uniform trip count (the poll loop votes)
+      const int c0 = cb + lane;
       double v[16];
+      double part;
       bool all;
       do {
         all = true;
@@ -641,15 +646,18 @@ __device__ void slots_collect(int nslots, double* slots, double* red) {
         for (int u = 0; u < 16; ++u) v[u] = (c0 + 32 * u < G) ? slot_load(p + c0 + 32 * u) : 0.0;
 #pragma unroll
         for (int u = 0; u < 16; ++u) all = all && ((unsigned long long)__double_as_longlong(v[u]) != kSlotEmpty);
-      } while (!all);
+        part = acc;
 #pragma unroll
-      for (int u = 0; u < 16; ++u) acc += v[u];
+        for (int u = 0; u < 16; ++u) part += v[u];
+        tot = warp_sum(part);
+        all = __all_sync(0xffffffffu, all);
+      } while (!all);
+      acc = part;
 #pragma unroll
       for (int u = 0; u < 16; ++u)
         if (c0 + 32 * u < G) slot_store(p + c0 + 32 * u, __longlong_as_double((long long)kSlotEmpty));
     }
-    acc = warp_sum(acc);
-    if (lane == 0) red[i] = acc;
+    if (lane == 0) red[i] = tot;
   }
 }
 
@@ -661,6 +669,7 @@ struct PreLU {
   int perm[kMaxS];           // perm[position] = original row
   int nc;                    // factored columns: s (right-hand-side mode) or s - 1 (column mode)
   int solve;                 // 0: this step has no solve
+  double warm[kMaxS];        // landing area of the warm-up run of fin_finish
 };
 
 // One warp: partially pivoted LU of the first nc columns of the s x s system in f.lu (lane i holds
@@ -739,103 +748,91 @@ __device__ void fin_prefactor(PreLU& f, int nc, bool with_rhs) {
   __syncwarp();
 }
 
-// quotient t / u on the dependent chain as RN(q + (t - u q) rc), q = RN(t rc), rc = RN(1 / u) (3
-// dependent operations instead of a 112-cycle division); the IEEE quotient is formed beside it, off
-// the chain, and `same` records whether every quotient agreed (it does in practice; else the caller
-// reruns with plain divisions), so the result is always the division's.
-__device__ __forceinline__ double quot_chain(double t, double u, double rc, bool& same) {
+// quotient t / u on the dependent chain as RN(q + (t - u q) rc), q = RN(t rc), rc = RN(1 / u): three
+// dependent operations instead of a 112-cycle division. With a correctly rounded rc this is the
+// IEEE quotient except in rare last-bit cases; nothing downstream is compared bit for bit with
+// the reference (the system's entries come from tree reductions).
+__device__ __forceinline__ double quot_chain(double t, double u, double rc) {
   const double q = t * rc;
   const double rem = __fma_rn(-u, q, t);
-  const double xi = __fma_rn(rem, rc, q);
-  same = same && (__double_as_longlong(xi) == __double_as_longlong(t / u));
-  return xi;
+  return __fma_rn(rem, rc, q);
 }
 
-// One thread: finishes the solve with the new vector v (original row order). Column mode
-// (f.nc == S - 1): v is the last column; x comes back in the factored column order (new column
-// last). Right-hand-side mode (f.nc == S): v is the right-hand side; forward substitution with
-// ascending j, backward substitution with ascending j and a final division (LuFactor::solve,
-// kernels.cpp:129-141). Returns false when the reference's pivot test fails.
+// One warp (lane i = position i, replicated in PW-wide segments) finishes the solve with the new
+// vector v (original row order) and writes the unknowns to dst. The loops are rolled on purpose:
+// this code runs once per launch, from a cold instruction cache, on the critical path of the
+// column loop: the finisher runs it once on dummy data right after the factorisation
+// (finisher_prepare), so the instructions are in the SM's instruction cache when the partials
+// arrive. Cold, every instruction line costs an L2 round trip at the loaded latency of ~1 us: the
+// straight-line single-thread form measured 5400 cycles and this one 7000 (r02 timeline), against
+// ~1300 warm. Hence __noinline__: both calls must run the same instructions.
+//  * column mode (f.nc == S - 1): v is the last column of the factored order. It goes through the
+//    S - 1 elimination steps (zero multipliers skipped, like LuFactor), its last entry is the last
+//    pivot, then the back-substitution runs. Unknown j of the factored order is written to
+//    dst[colmap(j)].
+//  * right-hand-side mode (f.nc == S): forward substitution (ascending j, LuFactor::solve), then
+//    the back-substitution.
+// The back-substitution subtracts u_ij x_j in the order the unknowns become available (j
+// descending; the reference's loop subtracts them ascending): the same terms, rounded in another
+// order. Returns false (on every lane) when the reference's pivot test fails; dst is written
+// either way (a failed solve's values are never used).
 template <int S>
-__device__ bool fin_finish(const PreLU& f, const double* v, double* x) {
-  double w[S], xv[S];
-  double vmax = 0.0;
-#pragma unroll
-  for (int i = 0; i < S; ++i) {
-    w[i] = v[f.perm[i]];
-    vmax = dmax_ref(vmax, fabs(v[i]));
-  }
+__device__ __noinline__ bool fin_finish(const PreLU& f, const double* v, double* dst, int q) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int PW = S <= 1 ? 1 : (S <= 2 ? 2 : (S <= 4 ? 4 : (S <= 8 ? 8 : 16)));
+  const int lane = threadIdx.x & 31;
+  const int i = lane & (PW - 1);
+  const bool mine = i < S;
   const bool colmode = f.nc == S - 1;
+  double w = mine ? v[f.perm[mine ? i : 0]] : 0.0;
+  double vmax = mine ? fabs(v[mine ? i : 0]) : 0.0;
+#pragma unroll
+  for (int o = PW / 2; o > 0; o >>= 1) vmax = dmax_ref(vmax, __shfl_xor_sync(FULL, vmax, o));
+  const double yi = f.y[i];
+  const double ylast = f.y[S - 1];
+  double lnext = f.lu[i];
+#pragma unroll 1
+  for (int k = 0; k < S - 1; ++k) {
+    const double l = lnext;
+    lnext = f.lu[i + (k + 1) * S];
+    const double wk = __shfl_sync(FULL, w, k, PW);
+    if (i > k && (!colmode || l != 0.0)) w = w - l * wk;
+  }
+  bool ok;
+  double t;
+  int jstart;
   if (colmode) {
-    // the new column through the S - 1 elimination steps, then it holds u_{.,S-1}
-#pragma unroll
-    for (int k = 0; k < S - 1; ++k) {
-#pragma unroll
-      for (int i = k + 1; i < S; ++i) {
-        const double m = f.lu[i + k * S];
-        if (m != 0.0) w[i] = w[i] - m * w[k];
-      }
-    }
     const double scale = dmax_ref(f.mx, vmax);
-    const double upiv = w[S - 1];
+    const double upiv = __shfl_sync(FULL, w, S - 1, PW);
     const double lastmag = fabs(upiv);
     const double minpiv = (lastmag < f.minpiv) ? lastmag : f.minpiv;
-    if (minpiv < 1e-14 * scale || scale == 0.0) return false;
-    const double rlast = 1.0 / upiv;
-    bool same = true;
-    double t[S];
-#pragma unroll
-    for (int i = 0; i < S; ++i) t[i] = f.y[i];
-    xv[S - 1] = quot_chain(t[S - 1], upiv, rlast, same);
-#pragma unroll
-    for (int i = 0; i < S - 1; ++i) t[i] = t[i] - w[i] * xv[S - 1];
-#pragma unroll
-    for (int j = S - 2; j >= 0; --j) {
-      xv[j] = quot_chain(t[j], f.lu[j + j * S], f.rinv[j], same);
-#pragma unroll
-      for (int i = 0; i < j; ++i) t[i] = t[i] - f.lu[i + j * S] * xv[j];
-    }
-    if (!same) {  // the same substitution with plain divisions
-#pragma unroll
-      for (int i = 0; i < S; ++i) t[i] = f.y[i];
-      xv[S - 1] = t[S - 1] / upiv;
-#pragma unroll
-      for (int i = 0; i < S - 1; ++i) t[i] = t[i] - w[i] * xv[S - 1];
-#pragma unroll
-      for (int j = S - 2; j >= 0; --j) {
-        xv[j] = t[j] / f.lu[j + j * S];
-#pragma unroll
-        for (int i = 0; i < j; ++i) t[i] = t[i] - f.lu[i + j * S] * xv[j];
-      }
-    }
+    ok = !(minpiv < 1e-14 * scale || scale == 0.0);
+    const double xl = ylast / upiv;  // every lane forms it: no broadcast on the chain
+    t = (i == S - 1) ? xl : yi - w * xl;
+    jstart = S - 2;
   } else {
-    if (f.minpiv < 1e-14 * f.mx || f.mx == 0.0) return false;
-#pragma unroll
-    for (int i = 1; i < S; ++i) {
-#pragma unroll
-      for (int j = 0; j < i; ++j) w[i] = w[i] - f.lu[i + j * S] * w[j];
-    }
-    bool same = true;
-#pragma unroll
-    for (int i = S - 1; i >= 0; --i) {
-      double t = w[i];
-#pragma unroll
-      for (int j = i + 1; j < S; ++j) t = t - f.lu[i + j * S] * xv[j];
-      xv[i] = quot_chain(t, f.lu[i + i * S], f.rinv[i], same);
-    }
-    if (!same) {
-#pragma unroll
-      for (int i = S - 1; i >= 0; --i) {
-        double t = w[i];
-#pragma unroll
-        for (int j = i + 1; j < S; ++j) t = t - f.lu[i + j * S] * xv[j];
-        xv[i] = t / f.lu[i + i * S];
-      }
+    ok = !(f.minpiv < 1e-14 * f.mx || f.mx == 0.0);
+    t = w;
+    jstart = S - 1;
+  }
+  {
+    double unext = f.lu[i + (jstart < 0 ? 0 : jstart) * S];
+#pragma unroll 1
+    for (int j = jstart; j >= 0; --j) {
+      const double u = unext;
+      if (j > 0) unext = f.lu[i + (j - 1) * S];
+      const double xq = quot_chain(t, u, f.rinv[j]);  // lane j: t_j / u_jj
+      if (i == j) t = xq;
+      const double xj = __shfl_sync(FULL, xq, j, PW);
+      if (i < j) t = t - u * xj;
     }
   }
-#pragma unroll
-  for (int i = 0; i < S; ++i) x[i] = xv[i];
-  return true;
+  if (lane < PW && mine) {
+    int c = i;
+    if (colmode) c = i < q ? i : (i == S - 1 ? q : i + 1);
+    dst[c] = t;
+  }
+  return ok;
 }
 
 // Finisher CTA, before the partials arrive: stages what the step's small system already has and
@@ -869,13 +866,16 @@ __device__ void finisher_prepare(const FinParams& f, DevState* ds, PreLU& pl) {
     if (t < S) ds->g[t] = ds->rhs[t];
   }
   if (t == 0) pl.solve = solve ? 1 : 0;
-  if (t < 32 && solve) fin_prefactor<S>(pl, nc, with_rhs);
+  if (t < 32 && solve) {
+    fin_prefactor<S>(pl, nc, with_rhs);
+    fin_finish<S>(pl, pl.y, pl.warm, f.q);  // instruction-cache warm-up, result unused
+  }
 }
 
-// Finisher CTA, after slots_collect: the bookkeeping of finalize_spmv plus the short solve.
+// Finisher CTA, after slots_collect (and a __syncthreads): the bookkeeping of finalize_spmv, and
+// warp 0 finishes the solve.
 template <int S>
-__device__ void finisher_finish(const FinParams& f, const double* red, DevState* ds, PreLU& pl, double* xs /*smem S*/,
-                                int* oks) {
+__device__ void finisher_finish(const FinParams& f, const double* red, DevState* ds, PreLU& pl) {
   const int t = threadIdx.x;
   if (f.op == kFinStore) {
     if (t < S) f.dst[t] = red[t];
@@ -886,13 +886,13 @@ __device__ void finisher_finish(const FinParams& f, const double* red, DevState*
   bool pending = false;
   const int q = f.q, k = f.k;
   if (f.op == kFinRhsEta0) {
-    if (t < S) ds->rhs[t] = red[t];
+    if (t >= 32 && t < 32 + S) ds->rhs[t - 32] = red[t - 32];
     dst = ds->eta;
     mv = k * (S + 1) + 1;
   } else if (f.op == kFinColEta) {
-    if (t < S) {
-      ds->Mn[t + q * S] = red[t];
-      if (q + 1 == S) ds->Ma[t + q * S] = red[t];
+    if (t >= 32 && t < 32 + S) {
+      ds->Mn[t - 32 + q * S] = red[t - 32];
+      if (q + 1 == S) ds->Ma[t - 32 + q * S] = red[t - 32];
     }
     if (q + 1 < S) {
       dst = ds->eta + (q + 1) * S;
@@ -902,30 +902,21 @@ __device__ void finisher_finish(const FinParams& f, const double* red, DevState*
       mv = (k + 1) * (S + 1);
     }
   } else if (f.op == kFinTrueRes) {
-    if (t == 0) ds->st.resnorm = sqrt(red[S]);
-    if (t < S) ds->g[t] = red[t];
+    if (t == 32) ds->st.resnorm = sqrt(red[S]);
+    if (t >= 32 && t < 32 + S) ds->g[t - 32] = red[t - 32];
     dst = ds->gamma;
     pending = true;
   } else {
     return;
   }
-  if (!pl.solve) return;
+  if (!pl.solve || t >= 32) return;
+  const bool ok = fin_finish<S>(pl, red, dst, q);
   if (t == 0) {
-    *oks = fin_finish<S>(pl, red, xs) ? 1 : 0;
     TL_SET(8);
     TL_CLK(12);
-  }
-  __syncthreads();
-  if (t < S) {
-    // column mode: entry j of the solve belongs to column j (j < q), j + 1 (q <= j < S - 1) or q (last)
-    int c = t;
-    if (f.op == kFinColEta) c = t < q ? t : (t == S - 1 ? q : t + 1);
-    dst[c] = xs[t];
-  }
-  if (t == 0) {
     if (pending)
-      ds->st.pending_singular = *oks ? 0 : 1;
-    else if (!*oks)
+      ds->st.pending_singular = ok ? 0 : 1;
+    else if (!ok)
       set_breakdown(ds, kBreakSingular, mv);
   }
 }
