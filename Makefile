@@ -14,9 +14,9 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVCCFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC -Xptxas -O3
 CXXFLAGS := -O3 -std=c++20 -fPIC -ffp-contract=off -Wall -Wextra -I$(CUDA_HOME)/include
 
-HOST_SRCS := $(CSRC)/solver.cpp $(CSRC)/capi.cpp $(CSRC)/host_util.cpp $(CSRC)/comm.cpp
+HOST_SRCS := $(CSRC)/solver.cpp $(CSRC)/capi.cpp $(CSRC)/host_util.cpp $(CSRC)/comm.cpp $(CSRC)/zsolver.cpp
 HOST_OBJS := $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.o,$(HOST_SRCS))
-CU_SRCS := $(CSRC)/kspmv.cu $(CSRC)/kcdia.cu $(CSRC)/klevel.cu $(CSRC)/kls.cu $(CSRC)/kpoly.cu $(CSRC)/kmisc.cu $(CSRC)/ktri.cu $(CSRC)/ksridr.cu $(CSRC)/kbase.cu $(CSRC)/kpersist.cu
+CU_SRCS := $(CSRC)/kspmv.cu $(CSRC)/kcdia.cu $(CSRC)/klevel.cu $(CSRC)/kls.cu $(CSRC)/kpoly.cu $(CSRC)/kmisc.cu $(CSRC)/ktri.cu $(CSRC)/ksridr.cu $(CSRC)/kbase.cu $(CSRC)/kpersist.cu $(CSRC)/kcomplex.cu
 CU_OBJS := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
 HEADERS := $(wildcard $(CSRC)/*.h) $(CSRC)/kcommon.cuh $(CSRC)/kdense.cuh $(CSRC)/ktimeline.cuh include/mstab_b200.h include/mstab_b200_kernels.h
 

@@ -47,7 +47,7 @@ extern "C" {
 #define MSTAB_E_ZEROPIVOT (-10)    /* mstab::ZeroPivot (build_jacobi / build_ilu0, precond.cpp:33,56-82) */
 #define MSTAB_E_MISSING_OMEGAS (-11) /* mstab::MissingOmegas (sridr_solve, sridr.cpp:33-34) */
 #define MSTAB_E_CUDA (-20)         /* device/runtime failure (no reference counterpart) */
-#define MSTAB_E_NOTREAL (-21)      /* complex data rejected: this build is the real fp64 path */
+#define MSTAB_E_NOTREAL (-21)      /* complex data passed to a real fp64 entry point (use the *_z ones) */
 
 /* ---- memory spaces for pointer arguments --------------------------------------------------- */
 #define MSTAB_MEM_HOST 0
@@ -258,6 +258,35 @@ int64_t mstab_result_taus(const mstab_result* res, double* re_im, int64_t cap);
 int mstab_result_final_data(const mstab_result* res, mstab_recycle** out);
 int mstab_result_fetched(const mstab_result* res, mstab_recycle** out);
 int mstab_result_handoff(const mstab_result* res, mstab_recycle** out);
+
+/* ---- complex128 data (types.hpp:11-15) --------------------------
+ * The reference computes in std::complex<double> throughout; the entry points above are its real
+ * embedding (imaginary parts +0.0). These take complex arrays as interleaved (re, im) pairs:
+ * a complex CsrMatrix (csr.hpp:17-52; fingerprint over the same byte layout, csr.cpp:28-43),
+ * idrstab_solve / mstab_solve with complex b, x0 and recycle data (idrstab.cpp:193-307; a real
+ * A, b, x0 triple draws the real cut-space, baselines.cpp:36-47), RecycleData with complex P, U,
+ * V (recycle.hpp:18-64). The handles are the same types: mstab_recycle_info_get,
+ * mstab_recycle_validate, mstab_result_report / _history / _taus / _final_data / _fetched /
+ * _handoff and the destroy calls accept both kinds; every other real entry point returns
+ * MSTAB_E_NOTREAL for a complex handle. Single-GPU, unpreconditioned operators. */
+int mstab_operator_create_csr_z(mstab_context* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                const double* values_re_im, mstab_operator** out);
+int32_t mstab_operator_is_complex(const mstab_operator* op);
+int32_t mstab_recycle_is_complex(const mstab_recycle* rd);
+int32_t mstab_result_is_complex(const mstab_result* res);
+/* y = A x (CsrOperator::apply), N complex values each in `mem`. */
+int mstab_operator_apply_z(mstab_context* ctx, const mstab_operator* op, const double* x_re_im, double* y_re_im,
+                           int32_t mem);
+int mstab_recycle_create_z(mstab_context* ctx, int64_t n, int64_t s, const double* p_re_im, const double* u_re_im,
+                           const double* v_re_im, int32_t mem, const double* omega_re_im, int64_t omega_count,
+                           int64_t level_j, uint64_t fingerprint, mstab_recycle** out);
+/* P, U, V as N x s column-major complex blocks on the host (any may be NULL), omega as (re, im) pairs. */
+int mstab_recycle_download_z(mstab_context* ctx, const mstab_recycle* rd, double* p_re_im, double* u_re_im,
+                             double* v_re_im, double* omega_re_im);
+int mstab_solve_z(mstab_context* ctx, const mstab_operator* op, const double* b_re_im, const double* x0_re_im,
+                  int32_t mem, const mstab_solver_config* cfg, const mstab_recycle* recycle,
+                  const mstab_fetch_policy* fetch, mstab_result** out);
+int mstab_result_x_z(mstab_context* ctx, const mstab_result* res, double* x_re_im, int32_t mem);
 
 /* ---- sequence-driver helpers (the caller side of the path: run_sequence's RHS rules) ------- */
 /* b = h2 * (x / dt + f) (implicit-Euler chain of the BASELINE conv-diff configs) and

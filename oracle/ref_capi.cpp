@@ -759,3 +759,126 @@ extern "C" int mstab_timeline(mstab_context*, int32_t, uint64_t*) {
   g_err = "reference implementation: no kernel timeline";
   return MSTAB_E_CONFIG;
 }
+
+// ---- complex128 data (include/mstab_b200.h, *_z entry points): the reference's native types ----
+extern "C" {
+int mstab_operator_create_csr_z(mstab_context*, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                const double* values_re_im, mstab_operator** out) {
+  return guarded([&] {
+    auto o = std::make_unique<mstab_operator>();
+    o->m.n_rows = o->m.n_cols = (size_t)n;
+    const int64_t nnz = row_ptr[n];
+    o->m.row_ptr.assign(row_ptr, row_ptr + n + 1);
+    o->m.col_idx.assign(col_idx, col_idx + nnz);
+    o->m.values.resize((size_t)nnz);
+    for (int64_t k = 0; k < nnz; ++k) o->m.values[(size_t)k] = Complex(values_re_im[2 * k], values_re_im[2 * k + 1]);
+    o->m.validate();
+    o->op = std::make_unique<mstab::CsrOperator>(o->m);
+    o->fp = o->op->fingerprint();
+    *out = o.release();
+  });
+}
+// the reference has one (complex) type: every handle can serve both kinds of entry points; "complex"
+// means some imaginary part is nonzero (is_real, types.cpp:25-29)
+int32_t mstab_operator_is_complex(const mstab_operator* op) { return op && !op->m.is_real() ? 1 : 0; }
+int32_t mstab_recycle_is_complex(const mstab_recycle* rd) {
+  if (!rd || !rd->d) return 0;
+  auto cplx = [](const mstab::DenseMatrix& m) { return !mstab::is_real(std::span<const Complex>(m.data())); };
+  return cplx(rd->d->p) || cplx(rd->d->u) || cplx(rd->d->v) ? 1 : 0;
+}
+int32_t mstab_result_is_complex(const mstab_result* res) {
+  return res && !mstab::is_real(std::span<const Complex>(res->r.x)) ? 1 : 0;
+}
+
+static mstab::Vector to_vec_z(const double* x, int64_t n) {
+  mstab::Vector v((size_t)n);
+  for (int64_t i = 0; i < n; ++i) v[(size_t)i] = Complex(x[2 * i], x[2 * i + 1]);
+  return v;
+}
+static mstab::DenseMatrix to_dense_z(const double* a, int64_t n, int64_t s) {
+  mstab::DenseMatrix m((size_t)n, (size_t)s);
+  for (int64_t j = 0; j < s; ++j)
+    for (int64_t i = 0; i < n; ++i) m((size_t)i, (size_t)j) = Complex(a[2 * (i + j * n)], a[2 * (i + j * n) + 1]);
+  return m;
+}
+static void from_dense_z(const mstab::DenseMatrix& m, double* out) {
+  if (!out) return;
+  for (size_t j = 0; j < m.cols(); ++j)
+    for (size_t i = 0; i < m.rows(); ++i) {
+      out[2 * (i + j * m.rows())] = m(i, j).real();
+      out[2 * (i + j * m.rows()) + 1] = m(i, j).imag();
+    }
+}
+
+int mstab_operator_apply_z(mstab_context*, const mstab_operator* op, const double* x, double* y, int32_t mem) {
+  return guarded([&] {
+    host_only(mem);
+    const int64_t n = (int64_t)op->m.n_rows;
+    mstab::Vector r = op->op->apply(to_vec_z(x, n));
+    for (int64_t i = 0; i < n; ++i) {
+      y[2 * i] = r[(size_t)i].real();
+      y[2 * i + 1] = r[(size_t)i].imag();
+    }
+  });
+}
+
+int mstab_recycle_create_z(mstab_context*, int64_t n, int64_t s, const double* p, const double* u, const double* v,
+                           int32_t mem, const double* omega_re_im, int64_t omega_count, int64_t level_j,
+                           uint64_t fingerprint, mstab_recycle** out) {
+  return guarded([&] {
+    host_only(mem);
+    std::vector<Complex> om;
+    for (int64_t i = 0; i < omega_count; ++i) om.emplace_back(omega_re_im[2 * i], omega_re_im[2 * i + 1]);
+    auto d = std::make_shared<mstab::RecycleData>(mstab::fetch(to_dense_z(p, n, s), to_dense_z(u, n, s),
+                                                               to_dense_z(v, n, s), std::move(om), (size_t)level_j,
+                                                               fingerprint));
+    *out = new mstab_recycle{d};
+  });
+}
+
+int mstab_recycle_download_z(mstab_context*, const mstab_recycle* rd, double* p, double* u, double* v,
+                             double* omega_re_im) {
+  return guarded([&] {
+    from_dense_z(rd->d->p, p);
+    from_dense_z(rd->d->u, u);
+    from_dense_z(rd->d->v, v);
+    if (omega_re_im)
+      for (size_t i = 0; i < rd->d->omega_history.size(); ++i) {
+        omega_re_im[2 * i] = rd->d->omega_history[i].real();
+        omega_re_im[2 * i + 1] = rd->d->omega_history[i].imag();
+      }
+  });
+}
+
+int mstab_solve_z(mstab_context*, const mstab_operator* op, const double* b, const double* x0, int32_t mem,
+                  const mstab_solver_config* cfg, const mstab_recycle* recycle, const mstab_fetch_policy* fetch,
+                  mstab_result** out) {
+  return guarded([&] {
+    host_only(mem);
+    const int64_t n = (int64_t)op->m.n_rows;
+    mstab::SolverConfig sc{(size_t)cfg->s, (size_t)cfg->ell, cfg->tol, cfg->max_mv,
+                           cfg->true_residual_each_cycle != 0, cfg->seed};
+    std::optional<mstab::FetchPolicy> fp;
+    if (fetch) {
+      if (fetch->kind == MSTAB_FETCH_AT_CYCLE) fp = mstab::FetchPolicy::at_cycle((size_t)fetch->cycle);
+      else if (fetch->kind == MSTAB_FETCH_AT_HALF_TOLERANCE) fp = mstab::FetchPolicy::at_half_tolerance();
+      else fp = mstab::FetchPolicy::manual();
+    }
+    mstab::Vector bv = to_vec_z(b, n);
+    mstab::Vector xv = x0 ? to_vec_z(x0, n) : mstab::Vector{};
+    auto r = std::make_unique<mstab_result>();
+    r->r = mstab::idrstab_solve(*op->op, bv, xv, sc, recycle ? recycle->d.get() : nullptr, fp ? &*fp : nullptr);
+    *out = r.release();
+  });
+}
+
+int mstab_result_x_z(mstab_context*, const mstab_result* res, double* x, int32_t mem) {
+  return guarded([&] {
+    host_only(mem);
+    for (size_t i = 0; i < res->r.x.size(); ++i) {
+      x[2 * i] = res->r.x[i].real();
+      x[2 * i + 1] = res->r.x[i].imag();
+    }
+  });
+}
+}  // extern "C"

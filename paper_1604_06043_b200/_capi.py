@@ -98,6 +98,18 @@ ABI = [
     ("mstab_recycle_destroy", None, [_P]),
     ("mstab_recycle_info_get", C.c_int, [_P, C.POINTER(RecycleInfoC)]),
     ("mstab_recycle_download", C.c_int, [_P, _P, _D, _D, _D, _D]),
+    # complex128 data: interleaved (re, im) arrays
+    ("mstab_operator_create_csr_z", C.c_int, [_P, C.c_int64, _I64, _I64, _P, C.POINTER(_P)]),
+    ("mstab_operator_is_complex", C.c_int32, [_P]),
+    ("mstab_recycle_is_complex", C.c_int32, [_P]),
+    ("mstab_result_is_complex", C.c_int32, [_P]),
+    ("mstab_operator_apply_z", C.c_int, [_P, _P, _P, _P, C.c_int32]),
+    ("mstab_recycle_create_z", C.c_int, [_P, C.c_int64, C.c_int64, _P, _P, _P, C.c_int32, _D, C.c_int64,
+                                         C.c_int64, C.c_uint64, C.POINTER(_P)]),
+    ("mstab_recycle_download_z", C.c_int, [_P, _P, _P, _P, _P, _D]),
+    ("mstab_solve_z", C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(SolverConfigC), _P,
+                                C.POINTER(FetchPolicyC), C.POINTER(_P)]),
+    ("mstab_result_x_z", C.c_int, [_P, _P, _P, C.c_int32]),
     ("mstab_recycle_validate", C.c_int, [_P, _P, _P, C.POINTER(ValidationReportC)]),
     ("mstab_recycle_save", C.c_int, [_P, _P, C.c_char_p]),
     ("mstab_recycle_load", C.c_int, [_P, C.c_char_p, C.POINTER(_P)]),

@@ -19,14 +19,19 @@ using namespace mstab_b200;
 struct mstab_context {
   std::unique_ptr<Context> impl;
 };
+// A handle holds either the real object (impl) or, for complex128 data, the
+// complex one (z); the *_z entry points create and consume the latter.
 struct mstab_operator {
   std::shared_ptr<Operator> impl;
+  std::shared_ptr<ZOperator> z;
 };
 struct mstab_recycle {
   RecyclePtr impl;
+  std::shared_ptr<const ZRecycle> z;
 };
 struct mstab_result {
   std::unique_ptr<SolveResultImpl> impl;
+  std::unique_ptr<ZResult> z;
 };
 
 namespace {
@@ -65,6 +70,21 @@ int guarded(F&& f) {
 void bind(mstab_context* ctx) {
   if (!ctx || !ctx->impl) throw Error(MSTAB_E_CONFIG, "null context");
   cudaSetDevice(ctx->impl->device);
+}
+
+// the real fp64 entry points reject complex handles (use the *_z entry points)
+const Operator& real_of(const mstab_operator* op) {
+  if (!op || !op->impl) throw Error(MSTAB_E_NOTREAL, "complex operator: use the *_z entry points");
+  return *op->impl;
+}
+const Recycle* real_of(const mstab_recycle* rd) {
+  if (!rd) return nullptr;
+  if (!rd->impl) throw Error(MSTAB_E_NOTREAL, "complex recycle data: use the *_z entry points");
+  return rd->impl.get();
+}
+const ZOperator& complex_of(const mstab_operator* op) {
+  if (!op || !op->z) throw Error(MSTAB_E_CONFIG, "real operator: create it with mstab_operator_create_csr_z");
+  return *op->z;
 }
 
 }  // namespace
@@ -172,9 +192,11 @@ int64_t mstab_operator_row_begin(const mstab_operator* op) { return op->impl->ro
 int64_t mstab_operator_global_size(const mstab_operator* op) { return op->impl->n_global; }
 
 void mstab_operator_destroy(mstab_operator* op) { delete op; }
-int64_t mstab_operator_size(const mstab_operator* op) { return op->impl->n; }
-int64_t mstab_operator_nnz(const mstab_operator* op) { return op->impl->nnz; }
-uint64_t mstab_operator_fingerprint(const mstab_operator* op) { return op->impl->fingerprint; }
+int64_t mstab_operator_size(const mstab_operator* op) { return op->z ? op->z->n : op->impl->n; }
+int64_t mstab_operator_nnz(const mstab_operator* op) { return op->z ? op->z->nnz : op->impl->nnz; }
+uint64_t mstab_operator_fingerprint(const mstab_operator* op) {
+  return op->z ? op->z->fingerprint : op->impl->fingerprint;
+}
 
 namespace {
 
@@ -182,7 +204,7 @@ namespace {
 void apply_mem(mstab_context* ctx, const mstab_operator* op, const double* x, double* y, int32_t mem, bool adjoint) {
     bind(ctx);
     Context& c = *ctx->impl;
-    const Operator& a = adjoint ? adjoint_of(c, *op->impl) : *op->impl;
+    const Operator& a = adjoint ? adjoint_of(c, real_of(op)) : real_of(op);
     const int64_t n = a.n;
     // The SpMV kernels move row pairs with 16-byte accesses: caller buffers are used in place
     // only when 16-byte aligned and of even length, otherwise staged through padded buffers.
@@ -251,7 +273,7 @@ int mstab_precond_solve(mstab_context* ctx, const mstab_operator* op, int32_t wh
   return guarded([&] {
     bind(ctx);
     Context& c = *ctx->impl;
-    const int64_t n = op->impl->n;
+    const int64_t n = real_of(op).n;
     if (which != 0 && which != 1) throw Error(MSTAB_E_CONFIG, "precond_solve: which must be 0 (L) or 1 (R)");
     const cudaMemcpyKind in = mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     const cudaMemcpyKind out = mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
@@ -303,6 +325,14 @@ void mstab_recycle_destroy(mstab_recycle* rd) { delete rd; }
 
 int mstab_recycle_info_get(const mstab_recycle* rd, mstab_recycle_info* out) {
   return guarded([&] {
+    if (rd->z) {
+      out->n = rd->z->n;
+      out->s = rd->z->s;
+      out->level_j = rd->z->level_j;
+      out->omega_count = (int64_t)rd->z->omega.size();
+      out->fingerprint = rd->z->fingerprint;
+      return;
+    }
     out->n = rd->impl->n;
     out->s = rd->impl->s;
     out->level_j = rd->impl->level_j;
@@ -316,7 +346,7 @@ int mstab_recycle_download(mstab_context* ctx, const mstab_recycle* rd, double* 
   return guarded([&] {
     bind(ctx);
     Context& c = *ctx->impl;
-    const Recycle& r = *rd->impl;
+    const Recycle& r = *real_of(rd);
     const int64_t ld = c.ld(r.n);
     auto down = [&](const DevPtr& src, double* dst) {
       if (!dst) return;
@@ -340,6 +370,12 @@ int mstab_recycle_validate(mstab_context* ctx, const mstab_recycle* rd, const ms
                            mstab_validation_report* out) {
   return guarded([&] {
     bind(ctx);
+    if (rd->z || op->z) {  // complex data: both sides must be complex (a real side has another fingerprint space)
+      if (!rd->z || !op->z) throw Error(MSTAB_E_FINGERPRINT, "recycle data belongs to a different operator");
+      mstab_validation_report rz = validate_z(*ctx->impl, *rd->z, *op->z);
+      if (out) *out = rz;
+      return;
+    }
     mstab_validation_report r = validate(*ctx->impl, *rd->impl, *op->impl);
     if (out) *out = r;
   });
@@ -350,7 +386,7 @@ int mstab_recycle_save(mstab_context* ctx, const mstab_recycle* rd, const char* 
     bind(ctx);
     if (ctx->impl->sharded())
       throw Error(MSTAB_E_CONFIG, "recycle save: a row-sharded context holds a slab; gather P/U/V on the host");
-    const Recycle& r = *rd->impl;
+    const Recycle& r = *real_of(rd);
     MrdData d;
     d.n = r.n;
     d.s = r.s;
@@ -389,8 +425,7 @@ int mstab_solve(mstab_context* ctx, const mstab_operator* op, const double* b, c
   return guarded([&] {
     bind(ctx);
     auto r = std::make_unique<mstab_result>();
-    r->impl = solve(*ctx->impl, *op->impl, b, x0, mem, *cfg, recycle ? recycle->impl.get() : nullptr,
-                    fetch);
+    r->impl = solve(*ctx->impl, real_of(op), b, x0, mem, *cfg, real_of(recycle), fetch);
     *out = r.release();
   });
 }
@@ -402,7 +437,7 @@ int mstab_sridr_solve(mstab_context* ctx, const mstab_operator* op, const double
     bind(ctx);
     if (!recycle) throw Error(MSTAB_E_CONFIG, "sridr: recycle data required");
     auto r = std::make_unique<mstab_result>();
-    r->impl = sridr(*ctx->impl, *op->impl, b, x0, mem, *cfg, *recycle->impl);
+    r->impl = sridr(*ctx->impl, real_of(op), b, x0, mem, *cfg, *real_of(recycle));
     *out = r.release();
   });
 }
@@ -412,7 +447,7 @@ int mstab_bicgstab_solve(mstab_context* ctx, const mstab_operator* op, const dou
   return guarded([&] {
     bind(ctx);
     auto r = std::make_unique<mstab_result>();
-    r->impl = bicgstab(*ctx->impl, *op->impl, b, x0, mem, tol, max_mv, shadow);
+    r->impl = bicgstab(*ctx->impl, real_of(op), b, x0, mem, tol, max_mv, shadow);
     *out = r.release();
   });
 }
@@ -422,7 +457,7 @@ int mstab_bicg_solve(mstab_context* ctx, const mstab_operator* op, const double*
   return guarded([&] {
     bind(ctx);
     auto r = std::make_unique<mstab_result>();
-    r->impl = bicg(*ctx->impl, *op->impl, b, x0, mem, tol, max_mv, shadow);
+    r->impl = bicg(*ctx->impl, real_of(op), b, x0, mem, tol, max_mv, shadow);
     *out = r.release();
   });
 }
@@ -432,7 +467,7 @@ int mstab_gmres_solve(mstab_context* ctx, const mstab_operator* op, const double
   return guarded([&] {
     bind(ctx);
     auto r = std::make_unique<mstab_result>();
-    r->impl = gmres(*ctx->impl, *op->impl, b, x0, mem, tol, max_it);
+    r->impl = gmres(*ctx->impl, real_of(op), b, x0, mem, tol, max_it);
     *out = r.release();
   });
 }
@@ -440,13 +475,14 @@ int mstab_gmres_solve(mstab_context* ctx, const mstab_operator* op, const double
 void mstab_result_destroy(mstab_result* res) { delete res; }
 
 int mstab_result_report(const mstab_result* res, mstab_report* out) {
-  return guarded([&] { *out = res->impl->report; });
+  return guarded([&] { *out = res->z ? res->z->report : res->impl->report; });
 }
 
 int mstab_result_x(mstab_context* ctx, const mstab_result* res, double* x, int32_t mem) {
   return guarded([&] {
     bind(ctx);
     Context& c = *ctx->impl;
+    if (!res->impl) throw Error(MSTAB_E_NOTREAL, "complex result: use mstab_result_x_z");
     if (cudaMemcpyAsync(x, res->impl->x->d(), sizeof(double) * res->impl->n,
                         mem == MSTAB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                         c.stream()) != cudaSuccess)
@@ -456,13 +492,22 @@ int mstab_result_x(mstab_context* ctx, const mstab_result* res, double* x, int32
 }
 
 int64_t mstab_result_history(const mstab_result* res, mstab_history_point* out, int64_t cap) {
-  const auto& h = res->impl->history;
+  const auto& h = res->z ? res->z->history : res->impl->history;
   const int64_t cnt = std::min<int64_t>(cap, (int64_t)h.size());
   if (cnt > 0) std::memcpy(out, h.data(), sizeof(mstab_history_point) * cnt);
   return cnt;
 }
 
 int64_t mstab_result_taus(const mstab_result* res, double* re_im, int64_t cap) {
+  if (res->z) {
+    const auto& tz = res->z->taus;
+    const int64_t cz = std::min<int64_t>(cap, (int64_t)tz.size());
+    for (int64_t i = 0; i < cz; ++i) {
+      re_im[2 * i] = tz[i].real();
+      re_im[2 * i + 1] = tz[i].imag();
+    }
+    return cz;
+  }
   const auto& t = res->impl->taus;
   const int64_t cnt = std::min<int64_t>(cap, (int64_t)t.size());
   for (int64_t i = 0; i < cnt; ++i) {
@@ -474,8 +519,13 @@ int64_t mstab_result_taus(const mstab_result* res, double* re_im, int64_t cap) {
 
 int mstab_result_final_data(const mstab_result* res, mstab_recycle** out) {
   return guarded([&] {
-    if (!res->impl->final_data) throw Error(MSTAB_E_ERROR, "no final recycle data (sridr result)");
     auto h = std::make_unique<mstab_recycle>();
+    if (res->z) {
+      h->z = res->z->final_data;
+      *out = h.release();
+      return;
+    }
+    if (!res->impl->final_data) throw Error(MSTAB_E_ERROR, "no final recycle data (sridr result)");
     h->impl = res->impl->final_data;
     *out = h.release();
   });
@@ -483,8 +533,14 @@ int mstab_result_final_data(const mstab_result* res, mstab_recycle** out) {
 
 int mstab_result_fetched(const mstab_result* res, mstab_recycle** out) {
   return guarded([&] {
-    if (!res->impl->fetched) throw Error(MSTAB_E_ERROR, "no fetched recycle data");
     auto h = std::make_unique<mstab_recycle>();
+    if (res->z) {
+      if (!res->z->fetched) throw Error(MSTAB_E_ERROR, "no fetched recycle data");
+      h->z = res->z->fetched;
+      *out = h.release();
+      return;
+    }
+    if (!res->impl->fetched) throw Error(MSTAB_E_ERROR, "no fetched recycle data");
     h->impl = res->impl->fetched;
     *out = h.release();
   });
@@ -492,10 +548,77 @@ int mstab_result_fetched(const mstab_result* res, mstab_recycle** out) {
 
 int mstab_result_handoff(const mstab_result* res, mstab_recycle** out) {
   return guarded([&] {
-    if (!res->impl->fetched && !res->impl->final_data) throw Error(MSTAB_E_ERROR, "no recycle data (sridr result)");
     auto h = std::make_unique<mstab_recycle>();
+    if (res->z) {
+      h->z = res->z->fetched ? res->z->fetched : res->z->final_data;
+      *out = h.release();
+      return;
+    }
+    if (!res->impl->fetched && !res->impl->final_data) throw Error(MSTAB_E_ERROR, "no recycle data (sridr result)");
     h->impl = res->impl->fetched ? res->impl->fetched : res->impl->final_data;
     *out = h.release();
+  });
+}
+
+// ---- complex128 data -------------------------------------------------------
+int mstab_operator_create_csr_z(mstab_context* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                const double* values_re_im, mstab_operator** out) {
+  return guarded([&] {
+    bind(ctx);
+    auto o = std::make_unique<mstab_operator>();
+    o->z = make_operator_z(*ctx->impl, n, row_ptr, col_idx, values_re_im);
+    *out = o.release();
+  });
+}
+int32_t mstab_operator_is_complex(const mstab_operator* op) { return op && op->z ? 1 : 0; }
+int32_t mstab_recycle_is_complex(const mstab_recycle* rd) { return rd && rd->z ? 1 : 0; }
+int32_t mstab_result_is_complex(const mstab_result* res) { return res && res->z ? 1 : 0; }
+
+int mstab_operator_apply_z(mstab_context* ctx, const mstab_operator* op, const double* x_re_im, double* y_re_im,
+                           int32_t mem) {
+  return guarded([&] {
+    bind(ctx);
+    apply_z(*ctx->impl, complex_of(op), x_re_im, y_re_im, mem);
+  });
+}
+
+int mstab_recycle_create_z(mstab_context* ctx, int64_t n, int64_t s, const double* p, const double* u, const double* v,
+                           int32_t mem, const double* omega_re_im, int64_t omega_count, int64_t level_j,
+                           uint64_t fingerprint, mstab_recycle** out) {
+  return guarded([&] {
+    bind(ctx);
+    auto h = std::make_unique<mstab_recycle>();
+    h->z = make_recycle_z(*ctx->impl, n, s, p, u, v, mem, omega_re_im, omega_count, level_j, fingerprint);
+    *out = h.release();
+  });
+}
+
+int mstab_recycle_download_z(mstab_context* ctx, const mstab_recycle* rd, double* p, double* u, double* v,
+                             double* omega_re_im) {
+  return guarded([&] {
+    bind(ctx);
+    if (!rd || !rd->z) throw Error(MSTAB_E_CONFIG, "real recycle data: use mstab_recycle_download");
+    download_recycle_z(*ctx->impl, *rd->z, p, u, v, omega_re_im);
+  });
+}
+
+int mstab_solve_z(mstab_context* ctx, const mstab_operator* op, const double* b_re_im, const double* x0_re_im,
+                  int32_t mem, const mstab_solver_config* cfg, const mstab_recycle* recycle,
+                  const mstab_fetch_policy* fetch, mstab_result** out) {
+  return guarded([&] {
+    bind(ctx);
+    if (recycle && !recycle->z) throw Error(MSTAB_E_CONFIG, "real recycle data in a complex solve");
+    auto r = std::make_unique<mstab_result>();
+    r->z = solve_z(*ctx->impl, complex_of(op), b_re_im, x0_re_im, mem, *cfg, recycle ? recycle->z.get() : nullptr, fetch);
+    *out = r.release();
+  });
+}
+
+int mstab_result_x_z(mstab_context* ctx, const mstab_result* res, double* x_re_im, int32_t mem) {
+  return guarded([&] {
+    bind(ctx);
+    if (!res || !res->z) throw Error(MSTAB_E_CONFIG, "real result: use mstab_result_x");
+    result_x_z(*ctx->impl, *res->z, x_re_im, mem);
   });
 }
 
@@ -569,7 +692,7 @@ int mstab_kernel_arnoldi(mstab_context* ctx, const mstab_operator* op, const dou
     bind(ctx);
     Context& c = *ctx->impl;
     if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: 1 <= s <= 16");
-    const int64_t n = op->impl->n, ld = c.ld(n);
+    const int64_t n = real_of(op).n, ld = c.ld(n);
     DevPtr r = c.alloc_vecs(n, 1), U = c.alloc_vecs(n, s), V = c.alloc_vecs(n, s);
     cudaMemcpyAsync(r->d(), r0, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream());
     reset_status(c);
@@ -590,7 +713,7 @@ int mstab_kernel_arnoldi_cb(mstab_context* ctx, const mstab_operator* op, const 
     Context& c = *ctx->impl;
     if (s < 1 || s > kMaxS) throw Error(MSTAB_E_CONFIG, "b200: 1 <= s <= 16");
     if (!fill) throw Error(MSTAB_E_CONFIG, "arnoldi: no draw callback");
-    const int64_t n = op->impl->n, ld = c.ld(n);
+    const int64_t n = real_of(op).n, ld = c.ld(n);
     DevPtr r = c.alloc_vecs(n, 1), U = c.alloc_vecs(n, s), V = c.alloc_vecs(n, s);
     cudaMemcpyAsync(r->d(), r0, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream());
     reset_status(c);
@@ -627,7 +750,7 @@ int mstab_kernel_level_iteration(mstab_context* ctx, const mstab_operator* op, i
                                  const double* p, double* x0, double* r_levels, double* v_levels) {
   return guarded([&] {
     bind(ctx);
-    level_iteration_host(*ctx->impl, *op->impl, (int)s, (int)k, p, x0, r_levels, v_levels);
+    level_iteration_host(*ctx->impl, real_of(op), (int)s, (int)k, p, x0, r_levels, v_levels);
   });
 }
 
@@ -756,7 +879,7 @@ int mstab_kernel_bench(mstab_context* ctx, const mstab_operator* op, int32_t kin
   return guarded([&] {
     bind(ctx);
     Context& c = *ctx->impl;
-    const Operator& o = *op->impl;
+    const Operator& o = real_of(op);
     const int s = (int)s64, ell = (int)ell64;
     if (s < 1 || s > kMaxS || ell < 1 || ell > kMaxEll) throw Error(MSTAB_E_CONFIG, "bench: bad s/ell");
     const int64_t n = o.n, ld = c.ld(n);

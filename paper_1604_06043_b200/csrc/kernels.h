@@ -283,4 +283,27 @@ void launch_fill_hash(cudaStream_t st, double* p, int64_t count, uint64_t seed);
 void launch_small_solve(cudaStream_t st, int s, const double* m, const double* rhs, double* x,
                         int32_t* ok);
 
+// ---- complex128 primitives (kcomplex.cu) ---------------------------------------
+// Complex vectors are interleaved (re, im) pairs; every pointer below addresses such pairs.
+constexpr int kZMaxTerms = kMaxS + 1;
+struct ZTerms {
+  int32_t m = 0;
+  const double* col[kZMaxTerms] = {};  // m vectors
+  double re[kZMaxTerms] = {}, im[kZMaxTerms] = {};  // their complex coefficients (unused by the dots)
+};
+// y = A x, rows in CSR order (csr.cpp:103-113)
+void launch_zspmv(cudaStream_t st, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* val,
+                  const double* x, double* y);
+// mode 0: y_out = y_in then += coef_c col_c in order (axpy chain); mode 1 / 2: y_out = y_in +/- gemv
+void launch_zaxpys(cudaStream_t st, int64_t n, int mode, double* y_out, const double* y_in, const ZTerms& t);
+// mode 0: y = x * (a + 0i); mode 1: y = x / a
+void launch_zscale(cudaStream_t st, int64_t n, int mode, double* y, const double* x, double a);
+void launch_zsub(cudaStream_t st, int64_t n, double* r, const double* b, const double* ax);
+// out[2c], out[2c+1] = conj(col_c) . y; y == nullptr: out[2c] = sum |col_c|^2
+void launch_zdots(cudaStream_t st, int64_t n, const ZTerms& cols, const double* y, double* out, const Reducer& red);
+// out: sum |x|^2, #non-finite, #nonzero, #entries with a nonzero imaginary part
+void launch_zstats(cudaStream_t st, int64_t n, const double* x, double* out, const Reducer& red);
+// out: sum |v - au|^2, sum |v|^2
+void launch_zdiff(cudaStream_t st, int64_t n, const double* v, const double* au, double* out, const Reducer& red);
+
 }  // namespace mstab_b200

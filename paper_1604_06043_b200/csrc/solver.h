@@ -203,6 +203,41 @@ struct SolveResultImpl {
   RecyclePtr fetched;
 };
 
+// ---- complex128 path (zsolver.cpp) ---------------------------------------------
+// Complex vectors and blocks are interleaved (re, im) pairs with column stride padded_ld(n).
+struct ZOperator {
+  int64_t n = 0, nnz = 0;
+  uint64_t fingerprint = 0;
+  bool real = false;  // CsrMatrix::is_real (csr.cpp:26)
+  DevPtr rp, ci, val;
+};
+struct ZRecycle {
+  int64_t n = 0, s = 0, level_j = 0;
+  uint64_t fingerprint = 0;
+  DevPtr p, u, v;
+  std::vector<std::complex<double>> omega;
+};
+struct ZResult {
+  DevPtr x;
+  int64_t n = 0;
+  mstab_report report{};
+  std::vector<mstab_history_point> history;
+  std::vector<std::complex<double>> taus;
+  std::shared_ptr<const ZRecycle> final_data, fetched;
+};
+std::shared_ptr<ZOperator> make_operator_z(Context& ctx, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                           const double* values_re_im);
+void apply_z(Context& ctx, const ZOperator& op, const double* x, double* y, int mem);
+std::shared_ptr<ZRecycle> make_recycle_z(Context& ctx, int64_t n, int64_t s, const double* p, const double* u,
+                                         const double* v, int mem, const double* omega_re_im, int64_t omega_count,
+                                         int64_t level_j, uint64_t fingerprint);
+void download_recycle_z(Context& ctx, const ZRecycle& rd, double* p, double* u, double* v, double* omega_re_im);
+mstab_validation_report validate_z(Context& ctx, const ZRecycle& rd, const ZOperator& a);
+std::unique_ptr<ZResult> solve_z(Context& ctx, const ZOperator& a, const double* b, const double* x0, int mem,
+                                 const mstab_solver_config& cfg, const ZRecycle* recycle,
+                                 const mstab_fetch_policy* fetch);
+void result_x_z(Context& ctx, const ZResult& res, double* x, int mem);
+
 // idrstab_solve / mstab_solve (idrstab.cpp:193-307) on the device.
 std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const double* b,
                                        const double* x0, int mem, const mstab_solver_config& cfg,

@@ -290,9 +290,22 @@ def _f64(a) -> np.ndarray:
     a = np.asarray(a)
     if np.iscomplexobj(a):
         if np.any(a.imag != 0):
-            raise NotReal("complex data: this build is the real fp64 path")
+            raise NotReal("complex data passed to a real fp64 entry point")
         a = a.real
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _is_complex(a) -> bool:
+    """Host data with a nonzero imaginary part (the reference's !is_real, types.cpp:25-29)."""
+    if a is None or hasattr(a, "is_cuda") or hasattr(a, "__cuda_array_interface__"):
+        return False
+    a = np.asarray(a)
+    return bool(np.iscomplexobj(a) and np.any(a.imag != 0))
+
+
+def _c128(a) -> np.ndarray:
+    """Contiguous complex128 copy: its memory is the interleaved (re, im) layout of the *_z ABI."""
+    return np.ascontiguousarray(np.asarray(a), dtype=np.complex128)
 
 
 def _dev_ptr(a, n=None, ctx=None, what="vector"):
@@ -336,7 +349,11 @@ class CsrMatrix:
         self.n_rows, self.n_cols = int(n_rows), int(n_cols)
         self.row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
         self.col_idx = np.ascontiguousarray(col_idx, dtype=np.int64)
-        self.values = _f64(values)
+        # complex values (types.hpp:11-15) are kept as complex128 and routed to the *_z entry points
+        self.values = _c128(values) if _is_complex(values) else _f64(values)
+
+    def is_real(self) -> bool:
+        return not np.iscomplexobj(self.values)
 
     def nnz(self) -> int:
         return int(self.values.size)
@@ -374,13 +391,14 @@ class CsrMatrix:
 
     @staticmethod
     def from_dense(m):
-        m = np.asarray(m, dtype=np.float64)
+        m = np.asarray(m)
+        m = m.astype(np.complex128) if _is_complex(m) else np.asarray(m.real if np.iscomplexobj(m) else m, dtype=np.float64)
         n = m.shape[0]
         t = [(i, j, m[i, j]) for i in range(n) for j in range(m.shape[1])]
         return CsrMatrix.from_triplets(n, m.shape[1], t)
 
     def to_dense(self):
-        d = np.zeros((self.n_rows, self.n_cols))
+        d = np.zeros((self.n_rows, self.n_cols), dtype=self.values.dtype)
         for i in range(self.n_rows):
             for k in range(self.row_ptr[i], self.row_ptr[i + 1]):
                 d[i, self.col_idx[k]] = self.values[k]
@@ -398,8 +416,15 @@ class CsrOperator:
         self.ctx = ctx if ctx is not None else default_context()
         self.lib = self.ctx.lib
         self.matrix = a
+        self._ztwin = None
+        self._z = not a.is_real()  # the handle is a complex operator (*_z entry points)
         h = C.c_void_p()
-        if slabs is None:
+        if not a.is_real():
+            if slabs is not None:
+                raise ConfigError("b200: the complex path is single-GPU")
+            _check(self.lib, self.lib.dll.mstab_operator_create_csr_z(
+                self.ctx.h, a.n_rows, i64ptr(a.row_ptr), i64ptr(a.col_idx), a.values.ctypes.data, C.byref(h)))
+        elif slabs is None:
             _check(self.lib, self.lib.dll.mstab_operator_create_csr(
                 self.ctx.h, a.n_rows, i64ptr(a.row_ptr), i64ptr(a.col_idx), dptr(a.values), C.byref(h)))
         else:
@@ -418,6 +443,7 @@ class CsrOperator:
         global reference checksum (`distributed_fingerprint`)."""
         self = cls.__new__(cls)
         self.ctx, self.lib, self.matrix = ctx, ctx.lib, None
+        self._ztwin, self._z = None, False
         self._slabs = np.ascontiguousarray(slabs, dtype=np.int64)
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(col_idx, dtype=np.int64)
@@ -445,9 +471,39 @@ class CsrOperator:
         return int(self.lib.dll.mstab_operator_fingerprint(self.h))
 
     def is_real(self) -> bool:
-        return True
+        return self.matrix is None or self.matrix.is_real()
+
+    def _complex_twin(self) -> "CsrOperator":
+        """This operator with complex128 values: a real operator meeting a complex vector computes in
+        complex arithmetic like the reference (same CSR, same fingerprint bytes)."""
+        if self._z:
+            return self
+        if self._ztwin is None:
+            if self.matrix is None:
+                raise ConfigError("b200: the complex path needs the host CSR (single-GPU operators)")
+            m = self.matrix
+            z = CsrMatrix.__new__(CsrMatrix)
+            z.n_rows, z.n_cols, z.row_ptr, z.col_idx = m.n_rows, m.n_cols, m.row_ptr, m.col_idx
+            z.values = _c128(m.values)
+            t = CsrOperator.__new__(CsrOperator)
+            t.ctx, t.lib, t.matrix, t._ztwin, t._z = self.ctx, self.lib, z, None, True
+            h = C.c_void_p()
+            _check(self.lib, self.lib.dll.mstab_operator_create_csr_z(
+                self.ctx.h, z.n_rows, i64ptr(z.row_ptr), i64ptr(z.col_idx), z.values.ctypes.data, C.byref(h)))
+            t.h = h
+            self._ztwin = t
+        return self._ztwin
 
     def apply(self, x, y=None):
+        if self._z or _is_complex(x):
+            op = self._complex_twin()
+            xz = _c128(x)
+            if xz.size != self.size():
+                raise DimensionMismatch("spmv: dimension mismatch")
+            out = np.empty_like(xz)
+            _check(self.lib, self.lib.dll.mstab_operator_apply_z(self.ctx.h, op.h, xz.ctypes.data, out.ctypes.data,
+                                                                 _capi.MEM_HOST))
+            return out
         ptr, mem = _dev_ptr(x, self.size(), self.ctx, "spmv x")
         if mem == _capi.MEM_DEVICE:
             yptr, ymem = _dev_ptr(y, self.size(), self.ctx, "spmv y")
@@ -544,6 +600,7 @@ class PreconditionedOperator(CsrOperator):
         self.ctx = ctx if ctx is not None else default_context()
         self.lib = self.ctx.lib
         self.matrix = a
+        self._ztwin, self._z = None, False
         self.pc = pc
         h = C.c_void_p()
         if pc.kind == PrecondKind.NONE:
@@ -599,14 +656,20 @@ class RecycleData:
         self._omega_count = int(info.omega_count)
         self._blocks = None
         self._omega = None
+        self.is_complex = bool(self.lib.dll.mstab_recycle_is_complex(handle))
 
     def _download(self):
         if self._blocks is None:
             n, s = self.n, self.s
-            p, u, v = (np.empty((s, n)) for _ in range(3))
             om = np.empty(2 * max(self._omega_count, 1))
-            _check(self.lib, self.lib.dll.mstab_recycle_download(self.ctx.h, self.h, dptr(p), dptr(u), dptr(v),
-                                                                 dptr(om)))
+            if self.is_complex:
+                p, u, v = (np.empty((s, n), dtype=np.complex128) for _ in range(3))
+                _check(self.lib, self.lib.dll.mstab_recycle_download_z(
+                    self.ctx.h, self.h, p.ctypes.data, u.ctypes.data, v.ctypes.data, dptr(om)))
+            else:
+                p, u, v = (np.empty((s, n)) for _ in range(3))
+                _check(self.lib, self.lib.dll.mstab_recycle_download(self.ctx.h, self.h, dptr(p), dptr(u), dptr(v),
+                                                                     dptr(om)))
             self._blocks = (p.T, u.T, v.T)  # n x s views of the column-major data
             self._omega = om[0:2 * self._omega_count:2] + 1j * om[1:2 * self._omega_count:2]
         return self._blocks
@@ -637,21 +700,45 @@ class RecycleData:
 def fetch(p, u, v, omega_history, level_j, fingerprint, ctx: Optional[Context] = None) -> RecycleData:
     """Deep-copy constructor of RecycleData (recycle.cpp:26-38)."""
     ctx = ctx if ctx is not None else default_context()
-    p, u, v = (np.asfortranarray(_f64(a)) for a in (p, u, v))
-    n, s = p.shape
     om = np.asarray(omega_history, dtype=np.complex128).ravel()
     omr = np.empty(2 * max(om.size, 1))
     omr[0:2 * om.size:2] = om.real
     omr[1:2 * om.size:2] = om.imag
     h = C.c_void_p()
+    if any(_is_complex(a) for a in (p, u, v)):
+        p, u, v = (np.asfortranarray(np.asarray(a, dtype=np.complex128)) for a in (p, u, v))
+        n, s = p.shape
+        _check(ctx.lib, ctx.lib.dll.mstab_recycle_create_z(
+            ctx.h, n, s, p.ctypes.data, u.ctypes.data, v.ctypes.data, _capi.MEM_HOST, dptr(omr), om.size,
+            int(level_j), int(fingerprint), C.byref(h)))
+        return RecycleData(ctx, h)
+    p, u, v = (np.asfortranarray(_f64(a)) for a in (p, u, v))
+    n, s = p.shape
     _check(ctx.lib, ctx.lib.dll.mstab_recycle_create(
         ctx.h, n, s, p.ctypes.data, u.ctypes.data, v.ctypes.data, _capi.MEM_HOST, dptr(omr), om.size,
         int(level_j), int(fingerprint), C.byref(h)))
     return RecycleData(ctx, h)
 
 
+def _complex_recycle(data: RecycleData, ctx: Context) -> RecycleData:
+    """Real recycle data re-created as complex blocks (+0.0 imaginary parts): a real hand-off continuing
+    into a complex solve, as the reference's single complex type allows."""
+    h = C.c_void_p()
+    p, u, v = (np.asfortranarray(np.asarray(a, dtype=np.complex128)) for a in (data.p, data.u, data.v))
+    om = np.asarray(data.omega_history, dtype=np.complex128).ravel()
+    omr = np.empty(2 * max(om.size, 1))
+    omr[0:2 * om.size:2] = om.real
+    omr[1:2 * om.size:2] = om.imag
+    _check(ctx.lib, ctx.lib.dll.mstab_recycle_create_z(
+        ctx.h, data.n, data.s, p.ctypes.data, u.ctypes.data, v.ctypes.data, _capi.MEM_HOST, dptr(omr), om.size,
+        int(data.level_J), int(data.matrix_fingerprint), C.byref(h)))
+    return RecycleData(ctx, h)
+
+
 def validate(data: RecycleData, op: CsrOperator) -> ValidationReport:
     r = _capi.ValidationReportC()
+    if data.is_complex:
+        op = op._complex_twin()
     _check(op.lib, op.lib.dll.mstab_recycle_validate(op.ctx.h, data.h, op.h, C.byref(r)))
     return ValidationReport(r.max_deviation, r.sigma_min_ratio, bool(r.low_rank_warning))
 
@@ -699,8 +786,12 @@ class SolveResult:
     @property
     def x(self) -> np.ndarray:
         if self._x is None:
-            out = np.empty(self.n)
-            _check(self.lib, self.lib.dll.mstab_result_x(self.ctx.h, self.h, out.ctypes.data, _capi.MEM_HOST))
+            if self.lib.dll.mstab_result_is_complex(self.h):
+                out = np.empty(self.n, dtype=np.complex128)
+                _check(self.lib, self.lib.dll.mstab_result_x_z(self.ctx.h, self.h, out.ctypes.data, _capi.MEM_HOST))
+            else:
+                out = np.empty(self.n)
+                _check(self.lib, self.lib.dll.mstab_result_x(self.ctx.h, self.h, out.ctypes.data, _capi.MEM_HOST))
             self._x = out
         return self._x
 
@@ -742,6 +833,30 @@ def idrstab_solve(a: CsrOperator, b, x0=None, cfg: Optional[SolverConfig] = None
     cfg = cfg if cfg is not None else SolverConfig()
     ctx, lib = a.ctx, a.lib
     n = a.size()
+    x0_given = x0 is not None and (not hasattr(x0, "__len__") or len(x0) > 0)
+    if (not a.is_real() or _is_complex(b) or (x0_given and _is_complex(x0))
+            or (recycle is not None and recycle.is_complex)):
+        # complex128 data: the reference's complex arithmetic on the device
+        if recycle is not None and not recycle.is_complex:
+            recycle = _complex_recycle(recycle, ctx)
+        az = a._complex_twin()
+        bz = _c128(b)
+        if bz.size != n:
+            raise DimensionMismatch("idrstab: rhs size")
+        xz = None
+        if x0_given:
+            xz = _c128(x0)
+            if xz.size != n:
+                raise DimensionMismatch("idrstab: guess size")
+        c = cfg._c()
+        fp = _capi.FetchPolicyC(fetch_policy.kind, 0, fetch_policy.cycle) if fetch_policy is not None else None
+        h = C.c_void_p()
+        _check(lib, lib.dll.mstab_solve_z(ctx.h, az.h, bz.ctypes.data, xz.ctypes.data if xz is not None else None,
+                                          _capi.MEM_HOST, C.byref(c), recycle.h if recycle else None,
+                                          C.byref(fp) if fp is not None else None, C.byref(h)))
+        res = SolveResult(ctx, h)
+        res.n = n
+        return res
     bptr, mem = _dev_ptr(b, n, ctx, "rhs")
     keep = []
     if mem == _capi.MEM_HOST:
