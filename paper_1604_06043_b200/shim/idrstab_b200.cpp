@@ -85,6 +85,7 @@ struct Session {
     uint64_t fp = 0;
     size_t nnz = 0;
     mstab_operator* op = nullptr;
+    bool complex = false;  // uploaded through mstab_operator_create_csr_z
   };
   std::list<CachedOp> ops;  // most recent first
   Session() { check(mstab_context_create(-1, &ctx)); }
@@ -153,11 +154,11 @@ mstab_operator* device_operator(Session& ss, const LinearOperator& a) {
   const CsrMatrix& m = *mp;
   const uint64_t fp = a.fingerprint();
   for (auto it = ss.ops.begin(); it != ss.ops.end(); ++it)
-    if (it->m == &m && it->fp == fp && it->nnz == m.nnz()) {
+    if (!it->complex && it->m == &m && it->fp == fp && it->nnz == m.nnz()) {
       ss.ops.splice(ss.ops.begin(), ss.ops, it);
       return it->op;
     }
-  if (!m.is_real()) throw ConfigError("b200: complex operator not supported (real fp64 path)");
+  if (!m.is_real()) throw ConfigError("b200: complex operator on a real fp64 entry point (only idrstab_solve / mstab_solve take complex data)");
   const int64_t n = (int64_t)m.n_rows;
   const Csr64 am(m, "operator");
   mstab_operator* op = nullptr;
@@ -169,7 +170,39 @@ mstab_operator* device_operator(Session& ss, const LinearOperator& a) {
   } else {
     check(mstab_operator_create_csr(ss.ctx, n, am.rp.data(), am.ci.data(), am.va.data(), &op));
   }
-  ss.ops.push_front({&m, fp, m.nnz(), op});
+  ss.ops.push_front({&m, fp, m.nnz(), op, false});
+  while (ss.ops.size() > 8) {
+    mstab_operator_destroy(ss.ops.back().op);
+    ss.ops.pop_back();
+  }
+  return op;
+}
+
+// ---- complex128 data: std::complex<double> arrays are the interleaved (re, im)
+// layout of the *_z entry points ----
+bool has_imag(std::span<const Complex> v) {
+  for (const Complex& z : v)
+    if (z.imag() != 0.0) return true;
+  return false;
+}
+const double* as_re_im(const Complex* p) { return reinterpret_cast<const double*>(p); }
+
+// The operator with complex values (a real matrix goes up with +0.0 imaginary parts when the
+// vectors are complex: the reference has a single complex type). Plain CsrOperator only.
+mstab_operator* device_operator_z(Session& ss, const LinearOperator& a) {
+  const auto* csr = dynamic_cast<const CsrOperator*>(&a);
+  if (!csr) throw ConfigError("b200: complex data needs a plain CsrOperator (no preconditioner) on the device path");
+  const CsrMatrix& m = csr->matrix();
+  const uint64_t fp = a.fingerprint();
+  for (auto it = ss.ops.begin(); it != ss.ops.end(); ++it)
+    if (it->complex && it->m == &m && it->fp == fp && it->nnz == m.nnz()) {
+      ss.ops.splice(ss.ops.begin(), ss.ops, it);
+      return it->op;
+    }
+  const std::vector<int64_t> rp(m.row_ptr.begin(), m.row_ptr.end()), ci(m.col_idx.begin(), m.col_idx.end());
+  mstab_operator* op = nullptr;
+  check(mstab_operator_create_csr_z(ss.ctx, (int64_t)m.n_rows, rp.data(), ci.data(), as_re_im(m.values.data()), &op));
+  ss.ops.push_front({&m, fp, m.nnz(), op, true});
   while (ss.ops.size() > 8) {
     mstab_operator_destroy(ss.ops.back().op);
     ss.ops.pop_back();
@@ -202,10 +235,37 @@ void upload_recycle(Session& ss, const RecycleData& rd, RecycleHandle& out) {
                              (int64_t)rd.level_J, rd.matrix_fingerprint, &out.h));
 }
 
+void upload_recycle_z(Session& ss, const RecycleData& rd, RecycleHandle& out) {
+  const int64_t n = (int64_t)rd.p.rows(), s = (int64_t)rd.s;
+  if ((int64_t)rd.p.cols() != s || (int64_t)rd.u.rows() != n || (int64_t)rd.u.cols() != s ||
+      (int64_t)rd.v.rows() != n || (int64_t)rd.v.cols() != s)
+    throw DimensionMismatch("recycle data has inconsistent shapes");
+  check(mstab_recycle_create_z(ss.ctx, n, s, as_re_im(rd.p.data().data()), as_re_im(rd.u.data().data()),
+                               as_re_im(rd.v.data().data()), MSTAB_MEM_HOST,
+                               rd.omega_history.empty() ? nullptr : as_re_im(rd.omega_history.data()),
+                               (int64_t)rd.omega_history.size(), (int64_t)rd.level_J, rd.matrix_fingerprint, &out.h));
+}
+
 RecycleData download_recycle(Session& ss, mstab_recycle* h) {
   mstab_recycle_info info{};
   check(mstab_recycle_info_get(h, &info));
   const size_t n = (size_t)info.n, s = (size_t)info.s;
+  if (mstab_recycle_is_complex(h)) {
+    RecycleData rz;
+    rz.p = DenseMatrix(n, s);
+    rz.u = DenseMatrix(n, s);
+    rz.v = DenseMatrix(n, s);
+    rz.omega_history.resize((size_t)info.omega_count);
+    check(mstab_recycle_download_z(ss.ctx, h, reinterpret_cast<double*>(rz.p.data().data()),
+                                   reinterpret_cast<double*>(rz.u.data().data()),
+                                   reinterpret_cast<double*>(rz.v.data().data()),
+                                   rz.omega_history.empty() ? nullptr
+                                                            : reinterpret_cast<double*>(rz.omega_history.data())));
+    rz.level_J = (size_t)info.level_j;
+    rz.s = s;
+    rz.matrix_fingerprint = info.fingerprint;
+    return rz;
+  }
   std::vector<double> p(n * s), u(n * s), v(n * s), om(2 * (size_t)info.omega_count);
   check(mstab_recycle_download(ss.ctx, h, p.data(), u.data(), v.data(), om.empty() ? nullptr : om.data()));
   RecycleData rd;
@@ -228,10 +288,14 @@ RecycleData download_recycle(Session& ss, mstab_recycle* h) {
 void read_result(Session& ss, mstab_result* res, size_t n, size_t cfg_ell, Vector& x_out, SolveReport& rep) {
   mstab_report r{};
   check(mstab_result_report(res, &r));
-  std::vector<double> x(n);
-  check(mstab_result_x(ss.ctx, res, x.data(), MSTAB_MEM_HOST));
   x_out.resize(n);
-  for (size_t i = 0; i < n; ++i) x_out[i] = Complex(x[i]);
+  if (mstab_result_is_complex(res)) {
+    check(mstab_result_x_z(ss.ctx, res, reinterpret_cast<double*>(x_out.data()), MSTAB_MEM_HOST));
+  } else {
+    std::vector<double> x(n);
+    check(mstab_result_x(ss.ctx, res, x.data(), MSTAB_MEM_HOST));
+    for (size_t i = 0; i < n; ++i) x_out[i] = Complex(x[i]);
+  }
   rep.h_mv = r.h_mv;
   rep.h_mv_aux = r.h_mv_aux;
   rep.h_rd = r.h_rd;
@@ -283,11 +347,23 @@ SolveResult idrstab_solve(const LinearOperator& a, const Vector& b, const Vector
   if (!x0.empty()) ensure_finite(x0, "idrstab guess");
 
   Session& ss = session();
-  mstab_operator* op = device_operator(ss, a);
-  const std::vector<double> bh = real_parts(b, "rhs");
-  const std::vector<double> xh = real_parts(x0, "guess");
+  // complex data anywhere (operator, b, x0, recycle blocks) takes the complex128 entry points
+  const bool cplx = !a.is_real() || has_imag(b) || has_imag(x0) ||
+                    (recycle && (has_imag(recycle->p.data()) || has_imag(recycle->u.data()) ||
+                                 has_imag(recycle->v.data())));
+  mstab_operator* op = cplx ? device_operator_z(ss, a) : device_operator(ss, a);
+  std::vector<double> bh, xh;
+  if (!cplx) {
+    bh = real_parts(b, "rhs");
+    xh = real_parts(x0, "guess");
+  }
   RecycleHandle rh;
-  if (recycle) upload_recycle(ss, *recycle, rh);
+  if (recycle) {
+    if (cplx)
+      upload_recycle_z(ss, *recycle, rh);
+    else
+      upload_recycle(ss, *recycle, rh);
+  }
 
   mstab_solver_config c = to_c(cfg);
   mstab_fetch_policy fp{};
@@ -298,8 +374,12 @@ SolveResult idrstab_solve(const LinearOperator& a, const Vector& b, const Vector
     fp.cycle = (int64_t)fetch_policy->cycle;
   }
   mstab_result* res = nullptr;
-  check(::mstab_solve(ss.ctx, op, bh.data(), x0.empty() ? nullptr : xh.data(), MSTAB_MEM_HOST, &c, rh.h,
-                    fetch_policy ? &fp : nullptr, &res));
+  if (cplx)
+    check(::mstab_solve_z(ss.ctx, op, as_re_im(b.data()), x0.empty() ? nullptr : as_re_im(x0.data()), MSTAB_MEM_HOST,
+                          &c, rh.h, fetch_policy ? &fp : nullptr, &res));
+  else
+    check(::mstab_solve(ss.ctx, op, bh.data(), x0.empty() ? nullptr : xh.data(), MSTAB_MEM_HOST, &c, rh.h,
+                        fetch_policy ? &fp : nullptr, &res));
   std::unique_ptr<mstab_result, void (*)(mstab_result*)> guard(res, mstab_result_destroy);
 
   SolveResult out;

@@ -44,6 +44,14 @@ def test_reference_suite_on_b200_shim(suite):
 
 
 @pytest.mark.gpu
+def test_complex_data_through_the_shim():
+    """tests/shim/test_complex_shim.cpp: complex128 operators, right-hand sides and recycle data in
+    the reference's own C++ types go through mstab::idrstab_solve / mstab_solve of the shim onto the
+    B200 and are compared with the unmodified reference solve linked into the same binary."""
+    assert run_suite(SUITE_DIR / "b200_test_complex_shim") == 3
+
+
+@pytest.mark.gpu
 def test_helper_cases_launch_kernels_through_the_shim():
     """The Arnoldi / BicgProjection / LevelIteration / PolyCombination cases of test_solvers.cpp run
     the shim's device-backed helpers: the library reports the kernels it launched at exit."""
