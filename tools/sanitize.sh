@@ -7,7 +7,7 @@
 set -u
 OUT=gpurun_out/sanitize
 mkdir -p $OUT
-SEL="${SAN_TESTS:-tests/test_gpu_kernels.py tests/test_gpu_solve.py tests/test_gpu_precond.py}"
+SEL="${SAN_TESTS:-tests/test_gpu_kernels.py tests/test_gpu_solve.py tests/test_gpu_precond.py tests/test_gpu_complex.py}"
 for tool in ${SAN_TOOLS:-memcheck racecheck synccheck}; do
   timeout ${SAN_TIMEOUT:-1500} /usr/local/cuda/bin/compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 \
     --log-file $OUT/$tool.log python -m pytest $SEL -m gpu -x -q -p no:cacheprovider > $OUT/$tool.pytest.log 2>&1
