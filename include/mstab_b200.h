@@ -144,6 +144,10 @@ int mstab_context_create(int32_t device, mstab_context** out);
 void mstab_context_destroy(mstab_context* ctx);
 /* Blocks until all work queued on the context's stream is complete. */
 int mstab_context_synchronize(mstab_context* ctx);
+/* Releases what the context keeps between solves (cycle workspace and graphs, cached cut-space,
+ * recycled result blocks) and returns the memory to the device; the next solve rebuilds them.
+ * Handles (operators, recycle data, results) stay valid. */
+int mstab_context_trim(mstab_context* ctx);
 /* The CUDA stream (cudaStream_t) the context launches on, as an opaque pointer (NULL on host impls). */
 void* mstab_context_stream(mstab_context* ctx);
 

@@ -166,6 +166,7 @@ int mstab_context_create(int32_t device, mstab_context** out) {
 }
 void mstab_context_destroy(mstab_context* ctx) { delete ctx; }
 int mstab_context_synchronize(mstab_context*) { return MSTAB_OK; }
+int mstab_context_trim(mstab_context*) { return MSTAB_OK; }
 void* mstab_context_stream(mstab_context*) { return nullptr; }
 
 int mstab_operator_create_csr(mstab_context*, int64_t n, const int64_t* row_ptr,

@@ -113,6 +113,13 @@ int mstab_context_synchronize(mstab_context* ctx) {
   });
 }
 
+int mstab_context_trim(mstab_context* ctx) {
+  return guarded([&] {
+    bind(ctx);
+    ctx->impl->trim();
+  });
+}
+
 void* mstab_context_stream(mstab_context* ctx) {
   return ctx && ctx->impl ? static_cast<void*>(ctx->impl->stream()) : nullptr;
 }

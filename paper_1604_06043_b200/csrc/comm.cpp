@@ -75,6 +75,9 @@ class NcclComm final : public Comm {
   }
   ~NcclComm() override {
     if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
+    if (e0_) cudaEventDestroy(e0_);
+    if (e1_) cudaEventDestroy(e1_);
+    if (side_) cudaStreamDestroy(side_);
   }
   bool capturable() const override { return true; }
   const char* name() const override { return "nccl"; }
@@ -94,9 +97,36 @@ class NcclComm final : public Comm {
       nccl_ok(api.Recv(x + r.offset, (size_t)r.count, ncclFloat64, r.peer, comm_, st), "ncclRecv");
     nccl_ok(api.GroupEnd(), "ncclGroupEnd");
   }
+  // The exchange on a side stream forked from (and later joined to) the solver stream with
+  // events, so the interior rows of the product run while NVLink moves the halo planes. Inside a
+  // stream capture the fork and join become graph edges.
+  void halo_begin(double* x, const HaloPlan& plan, cudaStream_t st) override {
+    if (plan.empty()) return;
+    if (!side_) {
+      cuda_ok(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "halo side stream");
+      cuda_ok(cudaEventCreateWithFlags(&e0_, cudaEventDisableTiming), "halo event");
+      cuda_ok(cudaEventCreateWithFlags(&e1_, cudaEventDisableTiming), "halo event");
+    }
+    cuda_ok(cudaEventRecord(e0_, st), "halo fork");
+    cuda_ok(cudaStreamWaitEvent(side_, e0_, 0), "halo fork");
+    halo(x, plan, side_);
+    cuda_ok(cudaEventRecord(e1_, side_), "halo join");
+    pending_ = true;
+  }
+  void halo_end(cudaStream_t st) override {
+    if (!pending_) return;
+    cuda_ok(cudaStreamWaitEvent(st, e1_, 0), "halo join");
+    pending_ = false;
+  }
 
  private:
+  static void cuda_ok(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Error(MSTAB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
   ncclComm_t comm_ = nullptr;
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t e0_ = nullptr, e1_ = nullptr;
+  bool pending_ = false;
 };
 
 // ---- host callbacks ---------------------------------------------------------------------------

@@ -57,6 +57,11 @@ class Comm {
   virtual void allreduce_sum(double* dev, int64_t count, cudaStream_t st) = 0;
   virtual void allgather(const double* dev_in, double* dev_out, int64_t count, cudaStream_t st) = 0;
   virtual void halo(double* x_owned, const HaloPlan& plan, cudaStream_t st) = 0;
+  // Split form: halo_begin starts the exchange (a communicator that can run it beside the solver
+  // stream does: NcclComm forks onto a side stream), halo_end makes `st` wait for it. Work enqueued
+  // on `st` between the two must not read the halo rows. Default: the blocking exchange.
+  virtual void halo_begin(double* x_owned, const HaloPlan& plan, cudaStream_t st) { halo(x_owned, plan, st); }
+  virtual void halo_end(cudaStream_t) {}
   virtual const char* name() const = 0;
 
  protected:

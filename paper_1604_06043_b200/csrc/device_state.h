@@ -47,6 +47,7 @@ struct DevState {
   // totals here instead of running the dense step; the host allreduces (or allgathers) them over
   // the ranks and launches the matching finaliser kernel (kernels.h launch_fin_*).
   double xred[kMaxXred];
+  double xred2[kMaxS + 1];  // totals of the interior launch of a split SpMV (Reducer::xbase)
   // least squares (kls.cu): CholeskyQR2 state between its two passes
   int32_t ls_mode;                      // 1: CholeskyQR2 path, 0: Givens TSQR fallback
   int32_t _pad_ls;

@@ -34,7 +34,10 @@ struct MaskOf {
 // rows grid-stride and publish their partial sums through the sentinel slots.
 constexpr int kCdiaBlock = 512;
 
-template <int S, bool TRUE_RES, int ND>
+// SEL: the launch covers a row selection (DevCsr::sel_*: the interior or the boundary rows of a row
+// slab). A template parameter because the streaming loop is instruction- and register-bound: with
+// the selection tested at run time the c2 kernel went from 30.2 to 36.5 us.
+template <int S, bool TRUE_RES, int ND, bool SEL>
 __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
     k_spmv_cdia(DevCsr a, const double* __restrict__ x, double* __restrict__ y,
                 const double* __restrict__ p, int64_t ld, const double* __restrict__ b,
@@ -60,7 +63,8 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
       TL_CLK(11);
     }
     if (red.xred) {  // row-sharded: the rank-local totals go to the cross-rank reduction
-      if (threadIdx.x < NS) red.xred[threadIdx.x] = blk[threadIdx.x];
+      if (threadIdx.x < NS)
+        red.xred[threadIdx.x] = red.xbase ? red.xbase[threadIdx.x] + blk[threadIdx.x] : blk[threadIdx.x];
       return;
     }
     finisher_finish<S>(fin, blk, ds, pl);
@@ -78,15 +82,21 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
   for (int i = 0; i < NS; ++i) part[i] = 0.0;
   // The gathers of a row are predicated on its mask, so the mask is loaded one iteration ahead
   // (the first measured version waited for it: two dependent memory latencies per row).
-  auto load_mask = [&](int32_t r) -> uint32_t {
-    if (r >= (int32_t)n) return 0u;
+  // row selection (DevCsr::sel_*): virtual index v -> row
+  const int32_t na = SEL ? a.sel_a1 - a.sel_a0 : 0, nb = SEL ? a.sel_b1 - a.sel_b0 : 0;
+  const int32_t nv = SEL ? na + nb : (int32_t)n;
+  auto row_of = [&](int32_t v) -> int32_t { return !SEL ? v : (v < na ? a.sel_a0 + v : a.sel_b0 + (v - na)); };
+  auto load_mask = [&](int32_t v) -> uint32_t {
+    if (v >= nv) return 0u;
+    const int32_t r = row_of(v);
     if (ND > 0) return (uint32_t)__ldg(static_cast<const typename MaskOf<ND>::T*>(a.dia_mask) + r);
     return mb == 1 ? (uint32_t)__ldg(static_cast<const uint8_t*>(a.dia_mask) + r)
                    : (mb == 2 ? (uint32_t)__ldg(static_cast<const uint16_t*>(a.dia_mask) + r)
                               : __ldg(static_cast<const uint32_t*>(a.dia_mask) + r));
   };
   const int32_t rstride = (gridDim.x - 1) * blockDim.x;
-  const int32_t row0 = (blockIdx.x - 1) * blockDim.x + threadIdx.x;
+  const int32_t v0 = (blockIdx.x - 1) * blockDim.x + threadIdx.x;
+  const int32_t row0 = v0 < nv ? row_of(v0) : (int32_t)n;
   // The masks never change and, inside a cycle, neither do P and b: the first row's mask, P row
   // and b are loaded before waiting on the producer of x (programmatic dependent launch), so that
   // DRAM round trip overlaps the predecessor's tail. A plain product (kFinStore) may pass a
@@ -96,7 +106,7 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
     TL_MIN(0);
     TL_MAX(1);
   }
-  uint32_t mnext = load_mask(row0);
+  uint32_t mnext = load_mask(v0);
   double pv[S];
   double bv = 0.0;
   if (early && row0 < (int32_t)n) {
@@ -110,9 +120,10 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
     TL_MAX(3);
   }
   bool first = early;
-  for (int32_t row = row0; row < (int32_t)n; row += rstride) {
+  for (int32_t v = v0; v < nv; v += rstride) {
+    const int32_t row = row_of(v);
     const uint32_t m = mnext;
-    mnext = load_mask(row + rstride);
+    mnext = load_mask(v + rstride);
     if (!first) {
 #pragma unroll
       for (int c = 0; c < S; ++c) pv[c] = __ldg(p + c * ld + row);
@@ -158,12 +169,13 @@ __global__ void __launch_bounds__(kCdiaBlock, S <= 8 ? 2 : 1)
 TL_BIND_FN(kcdia_timeline_bind)
 namespace {
 
-template <int S, bool TRUE_RES, int ND>
+template <int S, bool TRUE_RES, int ND, bool SEL = false>
 void launch_cdia_nd(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
                     int64_t ld, const double* b, const FinParams& fin, const Reducer& red) {
-  auto kfn = k_spmv_cdia<S, TRUE_RES, ND>;
+  auto kfn = k_spmv_cdia<S, TRUE_RES, ND, SEL>;
   // the resident capacity minus the finisher streams; one more CTA (index 0) finishes
-  int grid = occupancy_grid(kfn, a.n + kCdiaBlock, 0, kCdiaBlock);
+  const int64_t rows = (a.sel_a1 | a.sel_b1) ? (int64_t)(a.sel_a1 - a.sel_a0) + (a.sel_b1 - a.sel_b0) : a.n;
+  int grid = occupancy_grid(kfn, rows + kCdiaBlock, 0, kCdiaBlock);
   if (grid < 2) grid = 2;
   launch_pdl(kfn, grid, kCdiaBlock, 0, st, a, x, y, p, ld, b, fin, red);
 }
@@ -172,6 +184,14 @@ void launch_cdia_nd(cudaStream_t st, const DevCsr& a, const double* x, double* y
 template <int S, bool TRUE_RES>
 void launch_cdia_b(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
                    int64_t ld, const double* b, const FinParams& fin, const Reducer& red) {
+  if (a.sel_a1 | a.sel_b1) {  // split product of a row slab: 3-D stencils specialised, the rest generic
+    switch (a.ndiag) {
+      case 7: launch_cdia_nd<S, TRUE_RES, 7, true>(st, a, x, y, p, ld, b, fin, red); break;
+      case 27: launch_cdia_nd<S, TRUE_RES, 27, true>(st, a, x, y, p, ld, b, fin, red); break;
+      default: launch_cdia_nd<S, TRUE_RES, 0, true>(st, a, x, y, p, ld, b, fin, red); break;
+    }
+    return;
+  }
   switch (a.ndiag) {
     case 5: launch_cdia_nd<S, TRUE_RES, 5>(st, a, x, y, p, ld, b, fin, red); break;
     case 7: launch_cdia_nd<S, TRUE_RES, 7>(st, a, x, y, p, ld, b, fin, red); break;

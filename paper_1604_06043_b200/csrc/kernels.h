@@ -49,6 +49,11 @@ struct DevCsr {
   // Largest entry count of any aligned 32-row block (rows 32b .. 32b+31): the TMA-fed banded kernel
   // stages one block's CSR slice at a time (kspmv.cu k_spmv_ring2).
   int32_t blk32_max = 0;
+  // Row selection of one launch (constant-diagonal SpMV only): the rows [sel_a0, sel_a1) followed by
+  // [sel_b0, sel_b1); all four zero = every row. A row-sharded solve computes the interior rows
+  // (no halo column) while the halo exchange is in flight, then the boundary rows (solver.cpp
+  // apply_ph_sharded).
+  int32_t sel_a0 = 0, sel_a1 = 0, sel_b0 = 0, sel_b1 = 0;
 };
 constexpr int kMaxDiag = 64;
 constexpr int kMaxConstDiag = 32;
@@ -64,6 +69,9 @@ struct Reducer {
   // slots that hold an all-ones NaN pattern while empty. A streaming CTA publishes a partial with
   // one relaxed store; the finisher CTA polls the slots, sums them in index order and re-arms them.
   double* slots = nullptr;
+  // Row-sharded, second launch of a split product: totals of the first launch, added (first) to this
+  // launch's totals before they go to xred.
+  const double* xbase = nullptr;
 };
 
 // What the last CTA does with the reduced vector of an SpMV (see kernels.cu, finalize_spmv).

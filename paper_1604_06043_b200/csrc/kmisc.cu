@@ -164,6 +164,7 @@ struct Profiler {
 Profiler g_prof;
 std::mutex g_prof_mu;
 thread_local std::vector<ProfEvent>* t_capture_list = nullptr;
+thread_local cudaStream_t t_capture_stream = nullptr;  // stream of the capture list's last event
 
 // Counts one launch; with profiling on, brackets it with events on its stream.
 }  // namespace
@@ -179,10 +180,19 @@ LaunchScope::LaunchScope(cudaStream_t s, int c, double b) : st(s), cls(c), bytes
   g_launch_count.fetch_add(1, std::memory_order_relaxed);
   if (g_prof.on) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
+    // Inside a captured cycle consecutive launches share ONE boundary event (the previous launch's
+    // end is this launch's start: nothing else is enqueued between the kernels of a cycle), which
+    // halves the event-record nodes the profiling pass puts between kernels. (Row-sharded captures
+    // have the cross-rank collective between two kernels: it is charged to the kernel after it.)
+    if (t_capture_list && !t_capture_list->empty() && t_capture_stream == st) {
+      a = t_capture_list->back().b;
+      return;
+    }
     a = g_prof.get();
     // inside a stream capture an event-record NODE needs the External flag (a plain record only
     // adds a dependency edge)
     cudaEventRecordWithFlags(a, st, t_capture_list ? cudaEventRecordExternal : cudaEventRecordDefault);
+    t_capture_stream = st;
   }
 }
 
@@ -210,7 +220,10 @@ bool prof_enabled() {
   return g_prof.on;
 }
 
-void prof_set_capture_list(std::vector<ProfEvent>* list) { t_capture_list = list; }
+void prof_set_capture_list(std::vector<ProfEvent>* list) {
+  t_capture_list = list;
+  t_capture_stream = nullptr;
+}
 
 void prof_accumulate(const std::vector<ProfEvent>& list) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -226,9 +239,11 @@ void prof_accumulate(const std::vector<ProfEvent>& list) {
 
 void prof_release(std::vector<ProfEvent>& list) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEvent_t prev_b = nullptr;
   for (const ProfEvent& r : list) {
-    g_prof.pool.push_back(r.a);
+    if (r.a != prev_b) g_prof.pool.push_back(r.a);  // a shared boundary event is returned once
     g_prof.pool.push_back(r.b);
+    prev_b = r.b;
   }
   list.clear();
 }

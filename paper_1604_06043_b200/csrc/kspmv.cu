@@ -728,7 +728,11 @@ void launch_fin_spmv(cudaStream_t st, int s, const FinParams& fin, DevState* ds)
 void launch_spmv_ph(cudaStream_t st, const DevCsr& a, const double* x, double* y, const double* p,
                     int64_t ld, int s, const double* b, const FinParams& fin, const Reducer& red) {
   // CSR + gathered x + y + P^H epilogue (+ b for the true-residual form)
-  LaunchScope ls(st, kKSpmv, csr_bytes(a) + vbytes(a.n, 2.0 + s + (b ? 1.0 : 0.0)));
+  // a split launch (DevCsr::sel_*) is charged its share of the rows
+  const double share = (a.sel_a1 | a.sel_b1) && a.n > 0
+                           ? (double)((a.sel_a1 - a.sel_a0) + (a.sel_b1 - a.sel_b0)) / (double)a.n
+                           : 1.0;
+  LaunchScope ls(st, kKSpmv, share * (csr_bytes(a) + vbytes(a.n, 2.0 + s + (b ? 1.0 : 0.0))));
   static const bool use_tma = std::getenv("MSTAB_TMA") != nullptr;  // experimental, off by default
   if (a.ndiag > 0 && a.mask_bytes > 0) {
     launch_spmv_cdia(st, a, x, y, p, ld, s, b, fin, red);  // kcdia.cu

@@ -119,6 +119,7 @@ struct Context {
   DevPtr alloc(size_t bytes) { return std::make_shared<DevMem>(sh, bytes); }
   DevPtr alloc_vecs(int64_t n, int64_t cols);
   void sync();
+  void trim();
   explicit Context(int device);
   ~Context();
 };
@@ -141,6 +142,8 @@ struct Operator {
   // row slab (mstab_operator_create_csr_slab): global size, first row, x index range, halo plan
   int64_t n_global = 0, row0 = 0, xlo = 0, xhi = 0;
   HaloPlan halo;
+  // interior rows [int_lo, int_hi) of a row slab: no column outside the owned rows (0, 0: none known)
+  int64_t int_lo = 0, int_hi = 0;
   DevCsr csr() const {
     DevCsr c;
     c.n = n;

@@ -174,6 +174,10 @@ class Context:
         _check(self.lib, self.lib.dll.mstab_context_create(int(device), C.byref(h)))
         self.h = h
 
+    def trim(self):
+        """Release the cached cycle workspace, graphs and result blocks (mstab_context_trim)."""
+        _check(self.lib, self.lib.dll.mstab_context_trim(self.h))
+
     def synchronize(self):
         _check(self.lib, self.lib.dll.mstab_context_synchronize(self.h))
 

@@ -52,8 +52,10 @@ def _slabs(n, world):
     return np.array([(n * r) // world for r in range(world + 1)], dtype=np.int64)  # not plane-aligned on purpose
 
 
-def _worker(rank, world, port, name, b, b2, q, local=False):
+def _worker(rank, world, port, name, b, b2, q, local=False, overlap=True):
     try:
+        if not overlap:  # the one-launch product after a blocking exchange (read once per process)
+            os.environ["MSTAB_NO_HALO_OVERLAP"] = "1"
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         import torch.distributed as dist
@@ -95,10 +97,13 @@ def _worker(rank, world, port, name, b, b2, q, local=False):
         q.put((rank, None, None, None, None, None, None, None, None, traceback.format_exc() + repr(e)))
 
 
-@pytest.mark.parametrize("name,world,local", [("c1_64", 2, False), ("c2_48", 3, False), ("c2_48_dia", 2, False),
-                                              ("c3_20000", 2, False), ("c4_24", 2, True), ("c4_24", 3, True),
-                                              ("c3_20000", 3, True)])
-def test_sharded_matches_single_gpu(gpu_ctx, name, world, local):
+# The constant-diagonal cases (c1, c2, c4 shapes) run the split product: interior rows while the halo
+# is exchanged, then the boundary rows (solver.cpp apply_ph_sharded); "c2_48 / False" pins the
+# one-launch product the other operator forms use.
+@pytest.mark.parametrize("name,world,local,overlap", [
+    ("c1_64", 2, False, True), ("c2_48", 3, False, True), ("c2_48", 2, False, False), ("c2_48_dia", 2, False, True),
+    ("c3_20000", 2, False, True), ("c4_24", 2, True, True), ("c4_24", 3, True, True), ("c3_20000", 3, True, True)])
+def test_sharded_matches_single_gpu(gpu_ctx, name, world, local, overlap):
     cfg, A = _matrix(name)
     n = A.n_rows
     # single-GPU runs first: they also define the teacher-forced second right-hand side
@@ -115,7 +120,7 @@ def test_sharded_matches_single_gpu(gpu_ctx, name, world, local):
     ctxm = mp.get_context("spawn")
     q = ctxm.Queue()
     port = _free_port()
-    procs = [ctxm.Process(target=_worker, args=(r, world, port, name, b, b2, q, local)) for r in range(world)]
+    procs = [ctxm.Process(target=_worker, args=(r, world, port, name, b, b2, q, local, overlap)) for r in range(world)]
     for p in procs:
         p.start()
     out = {}
