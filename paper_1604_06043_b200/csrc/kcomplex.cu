@@ -131,6 +131,64 @@ __global__ void __launch_bounds__(kBlock) k_zdiff(int64_t n, const double2* __re
   commit_to<2>(part, 2, out, red);
 }
 
+// One pass over the rows for ALL lower levels of a level iteration: level k is final; levels
+// i = k-1 .. -1 are rebuilt top-down, each needing only level i+1 (final, held in registers from the
+// previous step) and level i (updated in q order). Element for element the arithmetic of the
+// per-column passes it replaces (axpy chains in column order), so the result is bit-identical.
+template <int S>
+__global__ void __launch_bounds__(kBlock, S <= 8 ? 2 : 1)
+    k_zrebuild_deferred(int64_t n, int64_t ld, int k, ZDeferredArgs a, const double2* __restrict__ coef) {
+  __shared__ double2 et[S * S];
+  __shared__ double2 gm[S];
+  for (int i = threadIdx.x; i < S * S; i += blockDim.x) et[i] = coef[i];
+  if (threadIdx.x < S) gm[threadIdx.x] = coef[S * S + threadIdx.x];
+  __syncthreads();
+  // eta is re-read from shared memory (broadcast) at every use: hoisting its S*S values into
+  // registers would spill the level columns
+  const volatile double* etv = reinterpret_cast<const volatile double*>(et);
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    double2 ln[S], lc[S];
+    const double2* top = reinterpret_cast<const double2*>(a.lv[k + 1]);
+#pragma unroll
+    for (int c = 0; c < S; ++c) ln[c] = top[c * ld + row];
+    double2 r_above = reinterpret_cast<const double2*>(a.r[k])[row];
+    for (int i = k - 1; i >= -1; --i) {
+      double2* cur = reinterpret_cast<double2*>(a.lv[i + 1]);
+#pragma unroll
+      for (int c = 0; c < S; ++c) lc[c] = cur[c * ld + row];
+      // step (a) at this level with its pre-rebuild columns: gemv from zero in column order
+      double2 corr = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < S; ++c) corr = cadd(corr, cmul(gm[c], lc[c]));
+      double2 ri = make_double2(0.0, 0.0);
+      if (i >= 0) {
+        double2* rp = reinterpret_cast<double2*>(a.r[i]);
+        ri = csub(rp[row], corr);
+        rp[row] = ri;
+      } else {
+        double2* xp = reinterpret_cast<double2*>(a.x);
+        xp[row] = cadd(xp[row], corr);
+      }
+      // step (c) at level i for every column q in order: newcol = r^(i+1) + sum_c (-eta_q[c]) mixed_c
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        double2 nc = r_above;
+#pragma unroll
+        for (int c = 0; c < S; ++c)
+          nc = cadd(nc, cmul(make_double2(etv[2 * (q * S + c)], etv[2 * (q * S + c) + 1]), (c < q) ? ln[c] : lc[c]));
+        lc[q] = nc;
+      }
+#pragma unroll
+      for (int c = 0; c < S; ++c) {
+        cur[c * ld + row] = lc[c];
+        ln[c] = lc[c];
+      }
+      r_above = ri;
+    }
+  }
+}
+
 int zgrid(int64_t n) {
   int64_t want = (n + kBlock - 1) / kBlock;
   const int64_t cap = (int64_t)g_num_sms * 4;
@@ -173,6 +231,15 @@ void launch_zdots(cudaStream_t st, int64_t n, const ZTerms& cols, const double* 
     LaunchScope ls(st, kKOther, 16.0 * (double)n * (t.m + (y ? 1.0 : 0.0)));
     k_zdots<<<zgrid(n), kBlock, 0, st>>>(n, t, reinterpret_cast<const double2*>(y), out + 2 * c0, red);
   }
+}
+
+void launch_zrebuild_deferred(cudaStream_t st, int64_t n, int64_t ld, int s, int k, const ZDeferredArgs& a,
+                              const double* coef) {
+  // reads x, r^(0..k), V^(-1..k); writes x, r^(0..k-1), V^(-1..k-1) (complex: 16 bytes per entry)
+  LaunchScope ls(st, kKRebuildDeferred, 2.0 * vbytes(n, (k + 1.0) + 1.0 + (k + 2.0) * s + k + 1.0 + (k + 1.0) * s));
+  MSTAB_DISPATCH_S(s, {
+    k_zrebuild_deferred<S><<<zgrid(n), kBlock, 0, st>>>(n, ld, k, a, reinterpret_cast<const double2*>(coef));
+  });
 }
 
 void launch_zstats(cudaStream_t st, int64_t n, const double* x, double* out, const Reducer& red) {

@@ -311,6 +311,19 @@ void launch_zsub(cudaStream_t st, int64_t n, double* r, const double* b, const d
 void launch_zdots(cudaStream_t st, int64_t n, const ZTerms& cols, const double* y, double* out, const Reducer& red);
 // out: sum |x|^2, #non-finite, #nonzero, #entries with a nonzero imaginary part
 void launch_zstats(cudaStream_t st, int64_t n, const double* x, double* out, const Reducer& red);
+// Deferred lower levels of level k of the complex level iteration (the complex twin of
+// launch_rebuild_deferred): for every row, top-down over the levels i = k-1 .. -1, the BiCG update
+// of r^(i) (x for i = -1) with gamma and the column rebuilds of level i for q = 0..s-1 in order
+// (idrstab.cpp:113-121,140-148), in place. coef (device, complex pairs): eta as s rows of s
+// coefficients ALREADY NEGATED (row q = -eta_q), then gamma (s). lv[i + 1] = V^(i) for i = -1..k,
+// r[i] = r^(i) for i = 0..k.
+struct ZDeferredArgs {
+  double* lv[kMaxEll + 2] = {};
+  double* r[kMaxEll + 1] = {};
+  double* x = nullptr;
+};
+void launch_zrebuild_deferred(cudaStream_t st, int64_t n, int64_t ld, int s, int k, const ZDeferredArgs& a,
+                              const double* coef);
 // out: sum |v - au|^2, sum |v|^2
 void launch_zdiff(cudaStream_t st, int64_t n, const double* v, const double* au, double* out, const Reducer& red);
 

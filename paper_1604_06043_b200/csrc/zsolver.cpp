@@ -154,14 +154,25 @@ struct ZDev {
   int64_t n, ld;
   cudaStream_t st;
   DevPtr red;          // reduction landing area (device)
+  DevPtr coef;         // eta / gamma of one level for the deferred rebuild (device)
   double* host = nullptr;  // pinned mirror
+  double* host_coef = nullptr;  // pinned staging of coef
   static constexpr int kRed = 2 * kZMaxTerms * kZMaxTerms + 64;
   ZDev(Context& c, int64_t n_) : ctx(c), n(n_), ld(padded_ld(n_)), st(c.stream()) {
     red = ctx.alloc(sizeof(double) * kRed);
+    coef = ctx.alloc(sizeof(double) * 2 * (kMaxS * kMaxS + kMaxS));
     CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host), sizeof(double) * kRed));
+    CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host_coef), sizeof(double) * 2 * (kMaxS * kMaxS + kMaxS)));
   }
   ~ZDev() {
     if (host) cudaFreeHost(host);
+    if (host_coef) cudaFreeHost(host_coef);
+  }
+  // every launch that read the previous contents is behind a stream synchronisation (the dots of
+  // the column loop), so the staging buffer is free to overwrite
+  void upload_coef(const std::vector<Z>& c) {
+    std::memcpy(host_coef, c.data(), sizeof(Z) * c.size());
+    CUDA_OK(cudaMemcpyAsync(coef->ptr, host_coef, sizeof(Z) * c.size(), cudaMemcpyHostToDevice, st));
   }
   DevPtr block(int64_t cols) { return ctx.alloc(sizeof(double) * 2 * (size_t)ld * (size_t)std::max<int64_t>(cols, 1)); }
   double* col(const DevPtr& b, int64_t c) const { return static_cast<double*>(b->ptr) + 2 * ld * c; }
@@ -642,38 +653,48 @@ std::unique_ptr<ZResult> solve_z(Context& ctx, const ZOperator& a, const double*
           g = d.dots(pcols, d.col(R[0], 0));
         }
         const std::vector<Z> gamma = solve_small(Ma, g);
-        for (int i = 0; i <= k; ++i) {
-          std::vector<const double*> cols(s);
-          for (int c = 0; c < s; ++c) cols[c] = d.col(vl(i), c);
-          d.axpys(2, d.col(R[i], 0), d.col(R[i], 0), cols, gamma);
-        }
+        // top level now; the levels below (and x) take the same gamma in the deferred pass
         {
           std::vector<const double*> cols(s);
-          for (int c = 0; c < s; ++c) cols[c] = d.col(vl(-1), c);
-          d.axpys(1, d.col(xw, 0), d.col(xw, 0), cols, gamma);
+          for (int c = 0; c < s; ++c) cols[c] = d.col(vl(k), c);
+          d.axpys(2, d.col(R[k], 0), d.col(R[k], 0), cols, gamma);
         }
         // (b) raise the residual one level
         d.spmv(a, d.col(R[k], 0), d.col(R[k + 1], 0));
         rep.h_mv++;
-        // (c) rebuild the columns against the mixed block, raise each one level (idrstab.cpp:127-151)
+        // (c) rebuild the columns against the mixed block, raise each one level (idrstab.cpp:127-151).
+        // Only the top level's column feeds the next product; levels -1..k-1 are rebuilt after the
+        // loop in one pass with the same coefficients (launch_zrebuild_deferred).
         const std::vector<Z> rhs = d.dots(pcols, d.col(R[k + 1], 0));
+        std::vector<Z> coef((size_t)s * s + s);
         for (int q = 0; q < s; ++q) {
           ZMat msys(s);
           for (int c = 0; c < s; ++c)
             for (int i = 0; i < s; ++i) msys(i, c) = c < q ? Mn(i, c) : Ma(i, c);
           std::vector<Z> eta = solve_small(msys, rhs);
-          for (Z& e : eta) e = -e;
-          for (int i = -1; i <= k; ++i) {
-            std::vector<const double*> cols(s);
-            for (int c = 0; c < s; ++c) cols[c] = c < q ? d.col(vl(i + 1), c) : d.col(vl(i), c);
-            // level i's column q is also an input (c == q): each thread reads index t of every
-            // input before it writes index t, so the column is rebuilt in place
-            d.axpys(0, d.col(vl(i), q), d.col(R[i + 1], 0), cols, eta);
+          for (int c = 0; c < s; ++c) {
+            eta[c] = -eta[c];
+            coef[(size_t)q * s + c] = eta[c];
           }
+          std::vector<const double*> cols(s);
+          for (int c = 0; c < s; ++c) cols[c] = c < q ? d.col(vl(k + 1), c) : d.col(vl(k), c);
+          // column q of level k is also an input (c == q): each thread reads index t of every
+          // input before it writes index t, so the column is rebuilt in place
+          d.axpys(0, d.col(vl(k), q), d.col(R[k + 1], 0), cols, eta);
           d.spmv(a, d.col(vl(k), q), d.col(vl(k + 1), q));
           rep.h_mv++;
           const std::vector<Z> mq = d.dots(pcols, d.col(vl(k + 1), q));
           for (int i = 0; i < s; ++i) Mn(i, q) = mq[i];
+        }
+        {
+          for (int c = 0; c < s; ++c) coef[(size_t)s * s + c] = gamma[c];
+          d.upload_coef(coef);
+          ZDeferredArgs da;
+          for (int i = -1; i <= k; ++i) da.lv[i + 1] = d.col(vl(i), 0);
+          for (int i = 0; i <= k; ++i) da.r[i] = d.col(R[i], 0);
+          da.x = d.col(xw, 0);
+          launch_zrebuild_deferred(d.st, n, d.ld, s, k, da, static_cast<const double*>(d.coef->ptr));
+          d.check();
         }
         Ma = Mn;   // P^H V^(k+1) for the next level's projection
         g = rhs;   // P^H r^(k+1)
