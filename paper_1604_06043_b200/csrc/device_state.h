@@ -33,6 +33,13 @@ struct CycleStatus {
   int32_t pending_singular;// gamma_0 for the NEXT cycle came out singular (raised when it starts)
 };
 
+// What a persistent cycle writes straight into mapped host memory (one slot per in-flight cycle):
+// the cycle's status and, last, the launch's sequence number the host polls for.
+struct HostCycleSlot {
+  CycleStatus st;
+  volatile uint64_t seq;
+};
+
 struct DevState {
   CycleStatus st;
   double Ma[kMaxS * kMaxS];    // P^H V^(k), column-major s x s (ld = s)
@@ -54,6 +61,10 @@ struct DevState {
   double ls_r1[(kMaxEll + 1) * (kMaxEll + 2) / 2];     // first Cholesky factor (packed upper)
   double ls_r1inv[(kMaxEll + 1) * (kMaxEll + 2) / 2];  // its inverse
   double ls_cn[kMaxEll];                // column sums of squares of Z
+  // Set by the persistent cycle kernel when its cycle ended the solve (converged below the
+  // threshold it was given, or broke down): a cycle launched speculatively behind it returns at once
+  // without touching anything (solver.cpp, pipelined persistent cycles). Cleared by reset_status.
+  int32_t stop;
   uint32_t ticket;             // last-CTA-done counter (reset by the finaliser)
   uint32_t tile_next;          // dynamic tile scheduler counter (reset by the finaliser)
 };

@@ -872,6 +872,39 @@ __device__ void finisher_prepare(const FinParams& f, DevState* ds, PreLU& pl) {
   }
 }
 
+// The same preparation by ONE warp with no block-wide barrier (the persistent cycle kernel runs it
+// on warp 1 while thread 0 polls the grid barrier; `ds` is then the CTA's shared-memory copy of the
+// state, which no other warp touches during the wait).
+template <int S>
+__device__ void finisher_prepare_warp(const FinParams& f, DevState* ds, PreLU& pl) {
+  const int lane = threadIdx.x & 31;
+  int nc = 0;
+  bool with_rhs = false, solve = false;
+  if (f.op == kFinRhsEta0 || f.op == kFinTrueRes) {
+    for (int i = lane; i < S * S; i += 32) pl.lu[i] = ds->Ma[i];
+    nc = S;
+    solve = true;
+  } else if (f.op == kFinColEta) {
+    const int q = f.q;
+    for (int i = lane; i < S * (S - 1); i += 32) {
+      const int j = i / S, rw = i - j * S;
+      pl.lu[i] = j < q ? ds->Mn[rw + j * S] : ds->Ma[rw + (j + 1) * S];
+    }
+    if (lane < S) pl.y[lane] = ds->rhs[lane];
+    nc = S - 1;
+    with_rhs = true;
+    solve = (q + 1 < S) || (f.k + 1 < f.ell);
+  }
+  __syncwarp();
+  if (f.op == kFinColEta && f.q + 1 == S) {
+    for (int i = lane; i < S * (S - 1); i += 32) ds->Ma[i] = ds->Mn[i];
+    if (lane < S) ds->g[lane] = ds->rhs[lane];
+  }
+  if (lane == 0) pl.solve = solve ? 1 : 0;
+  __syncwarp();
+  if (solve) fin_prefactor<S>(pl, nc, with_rhs);
+}
+
 // Finisher CTA, after slots_collect (and a __syncthreads): the bookkeeping of finalize_spmv, and
 // warp 0 finishes the solve.
 template <int S>

@@ -213,7 +213,11 @@ bool launch_persist_cycle(cudaStream_t st, const DevCsr& a, int64_t n, int64_t l
                           const double* x_in, const double* r_in, const double* u_in, const double* v_in,
                           double* x_out, double* r_out, double* u_out, double* v_out, const double* p,
                           const double* b, double* xbuf, double* partials, DevState* ds, unsigned* bar,
-                          bool probe_only);
+                          bool probe_only, double stop_below = -1.0, HostCycleSlot* hslot = nullptr,
+                          uint64_t seq = 0);
+// stop_below: the kernel sets DevState::stop when the cycle breaks down or ends with a residual norm
+// <= stop_below (negative: never on convergence); hslot (mapped host memory) receives the status
+// and then `seq`.
 
 // ---- validate (recycle.cpp:40-83): ||V - A U||^2, ||V||^2 per column, P^H P, V^H V ----------
 // Results land in ds->scal[0..1] (dev_num, dev_den) and ds->gram (P^H P then V^H V).

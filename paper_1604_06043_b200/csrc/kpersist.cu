@@ -43,6 +43,9 @@ struct PersistArgs {
   double* partials;  // 2 x kPSlots x gridDim doubles
   DevState* ds;
   unsigned* bar;     // grid barrier counter (zeroed by the host before every launch)
+  double stop_below; // residual norm at or below which the cycle ends the solve (DevState::stop)
+  HostCycleSlot* hslot;  // mapped host memory: status + sequence number of this launch (or nullptr)
+  unsigned long long seq;
   int debug;         // MSTAB_PERSIST_DEBUG: CTA 0 prints phase stamps of the first operator application
 };
 
@@ -92,12 +95,29 @@ __global__ void __launch_bounds__(kPBlock, 1) k_cycle(PersistArgs pa) {
   // targets, so no reset inside the kernel), thread 0 polling with an acquire load. The
   // cooperative launch guarantees that every CTA is resident.
   unsigned bar_target = 0;
+  // side(): work for the other warps while thread 0 waits (no block-wide barrier inside)
+  auto grid_sync_with = [&](auto&& side) {
+    __syncthreads();
+    bar_target += gridDim.x;
+    if (threadIdx.x == 0) {
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(pa.bar) : "memory");
+      unsigned seen;
+      do {
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(seen) : "l"(pa.bar) : "memory");
+      } while (seen < bar_target);
+    } else {
+      side();
+    }
+    __syncthreads();
+  };
   auto grid_sync = [&]() {
     __syncthreads();
     bar_target += gridDim.x;
     if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(pa.bar, 1u);
+      // arrival as a fire-and-forget reduction with release semantics (orders the CTA's writes before
+      // it, cumulative over the __syncthreads above): unlike atomicAdd the thread does not wait for
+      // the old value to come back before it starts polling, one L2 round trip less per barrier
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(pa.bar) : "memory");
       unsigned seen;
       do {
         asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(seen) : "l"(pa.bar) : "memory");
@@ -106,7 +126,7 @@ __global__ void __launch_bounds__(kPBlock, 1) k_cycle(PersistArgs pa) {
     __syncthreads();
   };
   __shared__ DevState sds;
-  __shared__ FinStage fs;
+  __shared__ PreLU pl;
   __shared__ double scratch[32 * 32];  // block_totals: NS * 32 doubles, NS <= 32 per reduction
   __shared__ double blk[32];
   __shared__ double redv[32];
@@ -140,11 +160,22 @@ __global__ void __launch_bounds__(kPBlock, 1) k_cycle(PersistArgs pa) {
       __syncthreads();
       const double* src = reinterpret_cast<const double*>(&sds);
       double* dst = reinterpret_cast<double*>(pa.ds);
-      // everything but the ticket / tile counters at the end of DevState (the last 8 bytes)
-      const int cnt = whole ? (int)(sizeof(DevState) / sizeof(double)) - 1 : (int)(sizeof(CycleStatus) / sizeof(double));
+      // the status head, or everything up to (not including) the stop flag and the counters
+      const int cnt = whole ? (int)(offsetof(DevState, stop) / sizeof(double)) : (int)(sizeof(CycleStatus) / sizeof(double));
       for (int i = t; i < cnt; i += kPBlock) dst[i] = src[i];
+      if (t == 0) {
+        // a cycle launched behind this one must not run when this one ended the solve
+        const bool stop = sds.st.breakdown != 0 || (whole && sds.st.resnorm <= pa.stop_below);
+        pa.ds->stop = stop ? 1 : 0;
+        if (pa.hslot) {  // the host polls seq: status first, system-wide fence, then the number
+          pa.hslot->st = sds.st;
+          __threadfence_system();
+          pa.hslot->seq = pa.seq;
+        }
+      }
     }
   };
+  if (sds.stop) return;  // speculative launch behind a cycle that ended the solve (uniform: see DevState::stop)
   if (sds.st.pending_singular) {  // gamma_0 of this cycle came out singular (level_update's check)
     if (t == 0) set_breakdown(&sds, kBreakSingular, 0);
     publish(false);
@@ -152,7 +183,7 @@ __global__ void __launch_bounds__(kPBlock, 1) k_cycle(PersistArgs pa) {
   }
   int parity = 0;
   // Sum of NS per-thread values over the whole grid, identical on every CTA, into redv[0..NS).
-  auto grid_reduce = [&](auto& vals, auto ns_tag) {
+  auto grid_reduce_with = [&](auto& vals, auto ns_tag, auto&& side) {
     constexpr int NS = decltype(ns_tag)::value;
     static_assert(NS <= 32, "reduction wider than the staging arrays");
     double* part = pa.partials + (size_t)parity * kPSlots * G;
@@ -160,7 +191,7 @@ __global__ void __launch_bounds__(kPBlock, 1) k_cycle(PersistArgs pa) {
     block_totals<NS>(vals, blk, scratch);
     for (int i = t; i < NS; i += kPBlock) part[(size_t)i * G + blockIdx.x] = blk[i];
     stamp();  // block totals done
-    grid_sync();
+    grid_sync_with(side);
     stamp();  // reduction barrier passed
     const int lane = t & 31, w = t >> 5, nw = kPBlock >> 5;
     for (int i = w; i < NS; i += nw) {
@@ -179,6 +210,7 @@ __global__ void __launch_bounds__(kPBlock, 1) k_cycle(PersistArgs pa) {
     __syncthreads();
     stamp();  // partials summed
   };
+  auto grid_reduce = [&](auto& vals, auto ns_tag) { grid_reduce_with(vals, ns_tag, [] {}); };
   // y = A v for this thread's row, v published through xbuf
   auto apply = [&](double v) -> double {
     if (valid) pa.xbuf[row] = v;
@@ -198,10 +230,14 @@ __global__ void __launch_bounds__(kPBlock, 1) k_cycle(PersistArgs pa) {
 #pragma unroll
     for (int c = 0; c < S; ++c) part[c] = pv[c] * y;
     part[S] = extra;
-    grid_reduce(part, std::integral_constant<int, S + 1>{});
-    fin_prestage(fin, &sds, fs);
-    __syncthreads();
-    finalize_spmv<S>(fin, redv, &sds, fs);
+    // The known part of the step's small system is factored by warp 1 WHILE thread 0 waits at the
+    // reduction barrier (kcommon.cuh, finisher protocol: the new column is taken last); after the
+    // sums only that column's elimination and the substitutions remain (dense step 1.7-2.1 us ->
+    // r02 stamps below).
+    grid_reduce_with(part, std::integral_constant<int, S + 1>{}, [&] {
+      if ((t >> 5) == 1) finisher_prepare_warp<S>(fin, &sds, pl);
+    });
+    finisher_finish<S>(fin, redv, &sds, pl);
     __syncthreads();
     stamp();  // dense step done
   };
@@ -410,8 +446,11 @@ bool launch_persist_cycle(cudaStream_t st, const DevCsr& a, int64_t n, int64_t l
                           const double* x_in, const double* r_in, const double* u_in, const double* v_in,
                           double* x_out, double* r_out, double* u_out, double* v_out, const double* p,
                           const double* b, double* xbuf, double* partials, DevState* ds, unsigned* bar,
-                          bool probe_only) {
+                          bool probe_only, double stop_below, HostCycleSlot* hslot, uint64_t seq) {
   PersistArgs pa;
+  pa.stop_below = stop_below;
+  pa.hslot = hslot;
+  pa.seq = seq;
   pa.a = a;
   pa.n = n;
   pa.ld = ld;

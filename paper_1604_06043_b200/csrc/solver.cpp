@@ -170,6 +170,8 @@ Context::Context(int dev) {
   CUDA_OK(cudaMemsetAsync(slots->ptr, 0xff, slots->bytes, stream()));  // every slot empty
   CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host_status), sizeof(CycleStatus)));
   CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host_scal), sizeof(double) * 64));
+  CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&hslots), sizeof(HostCycleSlot) * 2, cudaHostAllocMapped));
+  std::memset(hslots, 0, sizeof(HostCycleSlot) * 2);
   sync();
 }
 
@@ -177,6 +179,7 @@ Context::~Context() {
   if (sh && sh->stream) cudaStreamSynchronize(sh->stream);
   if (host_status) cudaFreeHost(host_status);
   if (host_scal) cudaFreeHost(host_scal);
+  if (hslots) cudaFreeHost(hslots);
 }
 
 void Context::sync() { CUDA_OK(cudaStreamSynchronize(stream())); }
@@ -207,8 +210,10 @@ DevPtr Context::alloc_vecs(int64_t n, int64_t cols) {
 // ---- small device<->host helpers ----------------------------------------------------------
 void reset_status(Context& ctx) {
   CUDA_OK(cudaMemsetAsync(ctx.ds(), 0, sizeof(CycleStatus), ctx.stream()));
-  CUDA_OK(cudaMemsetAsync(reinterpret_cast<char*>(ctx.ds()) + offsetof(DevState, ticket), 0,
-                          sizeof(uint32_t), ctx.stream()));
+  // the stop flag of the persistent cycles and the ticket counter (adjacent)
+  static_assert(offsetof(DevState, ticket) == offsetof(DevState, stop) + sizeof(int32_t), "stop precedes ticket");
+  CUDA_OK(cudaMemsetAsync(reinterpret_cast<char*>(ctx.ds()) + offsetof(DevState, stop), 0,
+                          sizeof(int32_t) + sizeof(uint32_t), ctx.stream()));
 }
 
 double* scal(Context& ctx, int i) { return ctx.ds()->scal + i; }
@@ -1263,14 +1268,16 @@ void enqueue_full_cycle(Context& ctx, const Operator& op, Workspace& w, int p) {
 
 // Runs one cycle: replays the captured graph of parity p (capturing it on first use), or
 // launches the kernels directly when graphs are off.
-void run_cycle(Context& ctx, const Operator& op, Workspace& w, int p) {
+void run_cycle(Context& ctx, const Operator& op, Workspace& w, int p, double stop_below = -1.0,
+               HostCycleSlot* hslot = nullptr, uint64_t seq = 0) {
   cudaStream_t st = ctx.stream();
   if (w.persist) {
     const WSet& S = w.set[p];
     const WSet& D = w.set[1 - p];
     launch_persist_cycle(st, op.csr(), op.n, ctx.ld(op.n), w.s, w.ell, S.x->d(), S.r->d(), S.U->d(), S.V->d(),
                          D.x->d(), D.r->d(), D.U->d(), D.V->d(), w.P->d(), w.tres ? w.b->d() : nullptr, w.xbuf->d(),
-                         ctx.partials->d(), ctx.ds(), reinterpret_cast<unsigned*>(w.xbuf->d() + ctx.ld(op.n)), false);
+                         ctx.partials->d(), ctx.ds(), reinterpret_cast<unsigned*>(w.xbuf->d() + ctx.ld(op.n)), false,
+                         stop_below, hslot, seq);
     check_launch();
     return;
   }
@@ -1315,6 +1322,50 @@ const CycleStatus& run_cycle_sync(Context& ctx, const Operator& op, Workspace& w
   run_cycle(ctx, op, w, p);
   const CycleStatus* cs = &read_status(ctx);
   if (w.persist && cs->breakdown == kBreakFallback) {
+    w.persist = false;
+    reset_status(ctx);
+    run_cycle(ctx, op, w, p);
+    cs = &read_status(ctx);
+  }
+  return *cs;
+}
+
+// Persistent cycles, pipelined (L2-resident systems: a cycle is ~90 us, so the host's status read
+// and relaunch, ~16 us, were 13% of it). The cycle of this iteration is in flight or launched now;
+// when `ahead` allows, the NEXT cycle is launched behind it before its outcome is known: the kernel
+// sets DevState::stop when its cycle ends the solve (residual <= stop_below, or a breakdown) and a
+// cycle launched behind it returns without touching anything, so speculation never changes a
+// result. The status does not come back through the stream (a copy would queue behind the
+// speculative launch): CTA 0 writes it into one of two mapped host slots and the host polls the
+// slot's sequence number.
+const CycleStatus& persist_next(Context& ctx, const Operator& op, Workspace& w, int p, double stop_below, bool ahead) {
+  HostCycleSlot* dslots = nullptr;
+  CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dslots), ctx.hslots, 0));
+  auto launch = [&](int parity) {
+    const uint64_t seq = ++ctx.pipe_launched;
+    run_cycle(ctx, op, w, parity, stop_below, dslots + (seq & 1), seq);
+  };
+  if (ctx.pipe_launched == ctx.pipe_consumed) launch(p);
+  if (ahead && ctx.pipe_launched == ctx.pipe_consumed + 1) launch(1 - p);
+  const uint64_t want = ctx.pipe_consumed + 1;
+  HostCycleSlot& slot = ctx.hslots[want & 1];
+  for (uint64_t spins = 0; slot.seq != want; ++spins) {
+    if ((spins & 0xfff) == 0xfff) {  // a failed launch or a device fault would never write the slot
+      cudaError_t e = cudaStreamQuery(ctx.stream());
+      if (e != cudaSuccess && e != cudaErrorNotReady)
+        throw Error(MSTAB_E_CUDA, std::string("persistent cycle: ") + cudaGetErrorString(e));
+      if (e == cudaSuccess && slot.seq != want) throw Error(MSTAB_E_CUDA, "persistent cycle: no status written");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  ctx.pipe_consumed = want;
+  *ctx.host_status = slot.st;
+  const CycleStatus* cs = ctx.host_status;
+  if (cs->breakdown == kBreakFallback) {
+    // the least squares left the CholeskyQR2 regime: the cycle wrote nothing (and stopped the one
+    // behind it); rerun it, and the rest of the solve, on the stream of kernels
+    ctx.sync();
+    ctx.pipe_launched = ctx.pipe_consumed;
     w.persist = false;
     reset_status(ctx);
     run_cycle(ctx, op, w, p);
@@ -1447,9 +1498,17 @@ std::unique_ptr<SolveResultImpl> solve(Context& ctx, const Operator& op, const d
   const double threshold = cfg.tol * rep.bnorm;
 
   bool broke = false;
+  static const bool pipelined = std::getenv("MSTAB_NO_PERSIST_PIPELINE") == nullptr;
+  ctx.pipe_launched = ctx.pipe_consumed = 0;
+  ctx.hslots[0].seq = ctx.hslots[1].seq = 0;
   while (resnorm > threshold && rep.h_mv < cfg.max_mv) {
     const CycleStatus& cs = [&]() -> const CycleStatus& {
       StallTrace tr("mstab: cycle");
+      if (w.persist && pipelined) {
+        // no speculation past the product budget: the cycle after this one must still be allowed
+        const bool ahead = rep.h_mv + 2 * (int64_t)ell * (s + 1) < cfg.max_mv;
+        return persist_next(ctx, op, w, p, threshold, ahead);
+      }
       return run_cycle_sync(ctx, op, w, p);
     }();
     if (w.graph[p].profiled) prof_accumulate(w.graph[p].prof);

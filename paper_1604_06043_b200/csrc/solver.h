@@ -96,6 +96,10 @@ struct Context {
   DevPtr partials;      // reduction partials
   DevPtr slots;         // sentinel-armed partial slots of the finisher protocol (Reducer::slots)
   CycleStatus* host_status = nullptr;  // pinned
+  // Pipelined persistent cycles (solver.cpp persist_next): two slots in mapped pinned memory the
+  // cycle kernels write their status into, and the launch / consume counters of the current solve.
+  HostCycleSlot* hslots = nullptr;
+  uint64_t pipe_launched = 0, pipe_consumed = 0;
   double* host_scal = nullptr;         // pinned, 64 doubles
   std::unique_ptr<Workspace> ws;       // cycle buffers + captured cycle graphs
   bool use_graphs = true;
