@@ -365,6 +365,9 @@ uint64_t mstab_fnv_fold_values(uint64_t h, const double* values, int64_t count);
  * number of local rows. */
 int64_t mstab_operator_row_begin(const mstab_operator* op);
 int64_t mstab_operator_global_size(const mstab_operator* op);
+/* Interior rows [lo, hi) of a row slab (local indices): rows with no column outside the owned rows,
+ * computed while the halo exchange of a split product is in flight (0, 0 for a non-slab operator). */
+void mstab_operator_interior_rows(const mstab_operator* op, int64_t* lo, int64_t* hi);
 
 /* ---- evidence hooks (no reference counterpart; the reference implementation reports zeros) --- */
 /* Number of kernel launches issued by this library since load. */

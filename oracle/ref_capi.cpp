@@ -167,6 +167,10 @@ int mstab_context_create(int32_t device, mstab_context** out) {
 void mstab_context_destroy(mstab_context* ctx) { delete ctx; }
 int mstab_context_synchronize(mstab_context*) { return MSTAB_OK; }
 int mstab_context_trim(mstab_context*) { return MSTAB_OK; }
+void mstab_operator_interior_rows(const mstab_operator*, int64_t* lo, int64_t* hi) {
+  if (lo) *lo = 0;
+  if (hi) *hi = 0;
+}
 void* mstab_context_stream(mstab_context*) { return nullptr; }
 
 int mstab_operator_create_csr(mstab_context*, int64_t n, const int64_t* row_ptr,

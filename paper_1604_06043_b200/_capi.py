@@ -80,6 +80,7 @@ ABI = [
     ("mstab_context_destroy", None, [_P]),
     ("mstab_context_synchronize", C.c_int, [_P]),
     ("mstab_context_trim", C.c_int, [_P]),
+    ("mstab_operator_interior_rows", None, [_P, _I64, _I64]),
     ("mstab_context_stream", _P, [_P]),
     ("mstab_operator_create_csr", C.c_int, [_P, C.c_int64, _I64, _I64, _D, C.POINTER(_P)]),
     ("mstab_operator_destroy", None, [_P]),

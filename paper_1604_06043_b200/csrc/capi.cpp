@@ -197,6 +197,10 @@ uint64_t mstab_fnv_fold_values(uint64_t h, const double* values, int64_t count) 
 
 int64_t mstab_operator_row_begin(const mstab_operator* op) { return op->impl->row0; }
 int64_t mstab_operator_global_size(const mstab_operator* op) { return op->impl->n_global; }
+void mstab_operator_interior_rows(const mstab_operator* op, int64_t* lo, int64_t* hi) {
+  if (lo) *lo = op && op->impl ? op->impl->int_lo : 0;
+  if (hi) *hi = op && op->impl ? op->impl->int_hi : 0;
+}
 
 void mstab_operator_destroy(mstab_operator* op) { delete op; }
 int64_t mstab_operator_size(const mstab_operator* op) { return op->z ? op->z->n : op->impl->n; }

@@ -465,6 +465,13 @@ class CsrOperator:
         return int(self.lib.dll.mstab_operator_row_begin(self.h))
 
     @property
+    def interior_rows(self) -> tuple:
+        """[lo, hi) of the slab's rows that reference owned columns only (mstab_operator_interior_rows)."""
+        lo, hi = C.c_int64(), C.c_int64()
+        self.lib.dll.mstab_operator_interior_rows(self.h, C.byref(lo), C.byref(hi))
+        return int(lo.value), int(hi.value)
+
+    @property
     def global_size(self) -> int:
         return int(self.lib.dll.mstab_operator_global_size(self.h))
 

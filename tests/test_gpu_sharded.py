@@ -83,6 +83,16 @@ def _worker(rank, world, port, name, b, b2, q, local=False, overlap=True):
         else:
             op = m.CsrOperator(A, ctx, slabs=slabs)
         assert op.row_begin == lo and op.size() == hi - lo and op.global_size == n
+        # the interior range of the split product: exactly the middle rows without a halo column
+        rp_g, ci_g = np.asarray(A.row_ptr), np.asarray(A.col_idx)
+        touches = np.array([np.any((ci_g[rp_g[i]:rp_g[i + 1]] < lo) | (ci_g[rp_g[i]:rp_g[i + 1]] >= hi))
+                            for i in range(lo, hi)])
+        ilo, ihi = op.interior_rows
+        mid = (hi - lo) // 2
+        want_lo = int(np.max(np.nonzero(touches[:mid])[0]) + 1) if touches[:mid].any() else 0
+        want_hi = int(mid + np.min(np.nonzero(touches[mid:])[0])) if touches[mid:].any() else hi - lo
+        assert (ilo, ihi) == (want_lo, max(want_lo, want_hi)), (ilo, ihi, want_lo, want_hi)
+        assert not touches[ilo:ihi].any()
         rng = np.random.default_rng(7)
         xg = rng.standard_normal(n)
         y = op.apply(xg[lo:hi])
