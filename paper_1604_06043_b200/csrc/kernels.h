@@ -74,7 +74,7 @@ struct Reducer {
   const double* xbase = nullptr;
 };
 
-// What the last CTA does with the reduced vector of an SpMV (see kernels.cu, finalize_spmv).
+// What the finalising CTA (the last one to finish, or the finisher CTA of kcdia.cu) does with the reduced vector of an SpMV (kcommon.cuh finalize_spmv / finisher_finish).
 enum FinOp : int32_t {
   kFinStore = 0,    // copy the reduced values to `dst`
   kFinRhsEta0 = 1,  // level k step (b): rhs := P^H r^(k+1); eta_0 := solve(Ma, rhs)
