@@ -3,8 +3,10 @@ rebuild of column q+1) from the ktimeline.cuh probes (developer tool; needs `mak
 
     python tools/timeline.py [config] [iters]
 Prints, in microseconds from the SpMV's first CTA start: ramp (last CTA start), PDL wait release,
-streaming done (first / last CTA), ticket winner, reduction done, LU done, SpMV end, then the
-rebuild's start / wait release / end."""
+streaming done (first / last CTA), reduction done (the finisher CTA has every partial summed), dense
+step done, SpMV end, then the rebuild's start / wait release / end. "ticket" and the reduce-phase
+cycle count belong to the last-CTA scheme the constant-diagonal SpMV no longer uses (NaN there);
+they still apply to the other SpMV forms."""
 import ctypes as C
 import json
 import os
