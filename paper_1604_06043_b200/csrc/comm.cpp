@@ -72,6 +72,10 @@ class NcclComm final : public Comm {
     std::memcpy(&id, uid, sizeof(id));
     cudaSetDevice(device);
     nccl_ok(api.CommInitRank(&comm_, world, id, rank), "ncclCommInitRank");
+    // the halo side stream and its fork / join events exist before any stream capture starts
+    cuda_ok(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "halo side stream");
+    cuda_ok(cudaEventCreateWithFlags(&e0_, cudaEventDisableTiming), "halo event");
+    cuda_ok(cudaEventCreateWithFlags(&e1_, cudaEventDisableTiming), "halo event");
   }
   ~NcclComm() override {
     if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
@@ -102,11 +106,6 @@ class NcclComm final : public Comm {
   // stream capture the fork and join become graph edges.
   void halo_begin(double* x, const HaloPlan& plan, cudaStream_t st) override {
     if (plan.empty()) return;
-    if (!side_) {
-      cuda_ok(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "halo side stream");
-      cuda_ok(cudaEventCreateWithFlags(&e0_, cudaEventDisableTiming), "halo event");
-      cuda_ok(cudaEventCreateWithFlags(&e1_, cudaEventDisableTiming), "halo event");
-    }
     cuda_ok(cudaEventRecord(e0_, st), "halo fork");
     cuda_ok(cudaStreamWaitEvent(side_, e0_, 0), "halo fork");
     halo(x, plan, side_);
